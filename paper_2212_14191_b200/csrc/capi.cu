@@ -1,0 +1,578 @@
+// C ABI (include/tfhe_b200.h): context lifetime, argument validation and the
+// native orchestration of the CKKS operators (key switch = ModUp / inner
+// product / ModDown, hmult, rescale, hrotate) on top of the kernels in
+// ntt_tc.cu and poly_ops.cu.  Everything is stream-ordered; no host syncs.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tfhe_b200.h"
+#include "poly_ops.h"
+#include "tfhe_internal.h"
+
+struct TfheCtx {
+  tfhe::Ctx c;
+  int n_chain = 0, n_special = 0;
+};
+
+namespace tfhe {
+
+thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+
+uint32_t powmod(uint64_t b, uint64_t e, uint32_t q) {
+  uint64_t r = 1 % q, x = b % q;
+  while (e) {
+    if (e & 1) r = r * x % q;
+    x = x * x % q;
+    e >>= 1;
+  }
+  return (uint32_t)r;
+}
+uint32_t invmod(uint64_t a, uint32_t q) { return powmod(a % q, q - 2, q); }
+uint32_t shoup(uint32_t w, uint32_t q) { return (uint32_t)(((uint64_t)w << 32) / q); }
+
+// bump allocator over the caller's workspace
+struct Carve {
+  uint8_t* p;
+  size_t left;
+  bool ok = true;
+  template <class T>
+  T* take(size_t bytes) {
+    size_t b = (bytes + 255) & ~(size_t)255;
+    if (b > left) {
+      ok = false;
+      return nullptr;
+    }
+    T* r = reinterpret_cast<T*>(p);
+    p += b;
+    left -= b;
+    return r;
+  }
+};
+
+struct CkksGeom {
+  int Lc, K, alpha, l1, E;
+  bool need_conv;
+};
+
+CkksGeom geom(const TfheCtx* h, int level, int dnum) {
+  CkksGeom g;
+  g.Lc = h->n_chain;
+  g.K = h->n_special;
+  g.alpha = dnum > 0 ? g.Lc / dnum : 1;
+  g.l1 = level + 1;
+  g.E = g.l1 + g.K;
+  g.need_conv = g.alpha > 1 || g.K > 1;
+  return g;
+}
+
+// prime index of extended-basis position r at level (chain 0..level, then specials)
+inline int ext_prime(const CkksGeom& g, int r) { return r < g.l1 ? r : g.Lc + (r - g.l1); }
+
+size_t ks_bytes(const CkksGeom& g, int batch, int n) {
+  const size_t U = (size_t)batch * n * 4;
+  size_t rows = g.l1 /*y*/ + g.E /*raised*/ + 2 * g.E /*acc*/ +
+                std::max({g.E, 2 * g.l1, 2 * g.K}) /*ntt ws*/ + 2 * g.K /*ysp*/ +
+                (g.need_conv ? std::max(g.E, 2 * g.l1) : 0);
+  return rows * U + 16 * 256;
+}
+
+int fill_bconv(const Ctx& c, const std::vector<int>& src, const std::vector<int>& dst,
+               BconvArgs& ba) {
+  if ((int)src.size() > kMaxBconvSrc || (int)dst.size() > kMaxBconvDst) {
+    set_error("base conversion too wide");
+    return TFHE_EINVAL;
+  }
+  memset(&ba, 0, sizeof(ba));
+  ba.n_src = (int)src.size();
+  ba.n_dst = (int)dst.size();
+  for (size_t s = 0; s < src.size(); ++s) {
+    const uint32_t qs = c.primes[src[s]];
+    uint64_t prod = 1;
+    for (size_t o = 0; o < src.size(); ++o)
+      if (o != s) prod = prod * (c.primes[src[o]] % qs) % qs;
+    ba.src_prime[s] = (int16_t)src[s];
+    ba.qhat_inv[s] = invmod(prod, qs);
+    ba.qhat_inv_shoup[s] = shoup(ba.qhat_inv[s], qs);
+  }
+  for (size_t t = 0; t < dst.size(); ++t) {
+    const uint32_t pt = c.primes[dst[t]];
+    ba.dst_prime[t] = (int16_t)dst[t];
+    ba.copy_from[t] = -1;
+    for (size_t s = 0; s < src.size(); ++s)
+      if (c.primes[src[s]] == pt) ba.copy_from[t] = (int16_t)s;
+    for (size_t s = 0; s < src.size(); ++s) {
+      uint64_t prod = 1;
+      for (size_t o = 0; o < src.size(); ++o)
+        if (o != s) prod = prod * (c.primes[src[o]] % pt) % pt;
+      ba.factor[s * kMaxBconvDst + t] = (uint32_t)prod;
+    }
+  }
+  return 0;
+}
+
+// key switch of d (l1, B, n) -> out (2, l1, B, n) [+ add rows base_row]
+int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const uint32_t* key,
+                   int dnum, uint32_t* out, const uint32_t* base, const int16_t* base_rows,
+                   Carve& cv, cudaStream_t st) {
+  const Ctx& c = h->c;
+  const CkksGeom g = geom(h, level, dnum);
+  const size_t U = (size_t)batch * c.n;  // elements per limb row
+  uint32_t* y = cv.take<uint32_t>(g.l1 * U * 4);
+  uint32_t* raised = cv.take<uint32_t>(g.E * U * 4);
+  uint32_t* acc = cv.take<uint32_t>(2 * g.E * U * 4);
+  const int ntt_rows = std::max({g.E, 2 * g.l1, 2 * g.K});
+  const size_t ntt_ws_bytes = ntt_rows * U * 4;
+  uint32_t* ntt_ws = cv.take<uint32_t>(ntt_ws_bytes);
+  uint32_t* ysp = cv.take<uint32_t>(2 * g.K * U * 4);
+  uint32_t* conv = g.need_conv ? cv.take<uint32_t>(std::max(g.E, 2 * g.l1) * U * 4) : nullptr;
+  if (!cv.ok) {
+    set_error("ckks workspace too small");
+    return TFHE_EINVAL;
+  }
+  const size_t key_pair = (size_t)2 * (g.Lc + g.K) * c.n;  // elements per (b_j, a_j)
+  int rc;
+
+  // 1. y = INTT(d), every limb of the level  (ModUp's to_coeff, ckks.py:362)
+  LimbMap m;
+  m.n = g.l1;
+  for (int r = 0; r < g.l1; ++r) m.prime[r] = m.in_row[r] = m.out_row[r] = (int16_t)r;
+  if ((rc = launch_ntt(c, d, y, m, batch, 1, nullptr, ntt_ws, ntt_ws_bytes, st))) return rc;
+
+  // 2. per GKS slice: ModUp + inner product  (ckks.py:337-351)
+  int16_t row_prime[kMaxRows];
+  int32_t key_row[kMaxRows];
+  for (int r = 0; r < g.E; ++r) {
+    row_prime[r] = (int16_t)ext_prime(g, r);
+    key_row[r] = ext_prime(g, r);  // key rows are over the full ext basis
+  }
+  int first = 1;
+  for (int j = 0; j < dnum; ++j) {
+    const int lo = j * g.alpha;
+    if (lo > level) break;
+    const int hi = std::min((j + 1) * g.alpha, g.l1);
+    LimbMap mu;
+    mu.n = 0;
+    std::vector<int> src, dst;
+    for (int s = lo; s < hi; ++s) src.push_back(s);
+    for (int r = 0; r < g.E; ++r) {
+      if (r >= lo && r < hi) continue;
+      mu.prime[mu.n] = (int16_t)ext_prime(g, r);
+      mu.out_row[mu.n] = (int16_t)r;
+      mu.in_row[mu.n] = (int16_t)(hi - lo == 1 ? lo : mu.n);
+      dst.push_back(ext_prime(g, r));
+      ++mu.n;
+    }
+    const uint32_t* ntt_in = y;
+    if (hi - lo > 1) {
+      BconvArgs ba;
+      if ((rc = fill_bconv(c, src, dst, ba))) return rc;
+      if ((rc = launch_bconv(c, y + (size_t)lo * U, conv, ba, batch, st))) return rc;
+      ntt_in = conv;
+    }
+    // alpha = 1: fast_basis_conv is the identity on the slice's coefficients
+    // (Q = q_lo, Q/q = 1), so the NTT reads y's row directly and reduces it
+    // mod each target prime inside the byte-sliced GEMM.
+    if ((rc = launch_ntt(c, ntt_in, raised, mu, batch, 0, nullptr, ntt_ws, ntt_ws_bytes, st)))
+      return rc;
+    // slice rows are reused unchanged (ckks.py:361-364)
+    if (cudaMemcpyAsync(raised + (size_t)lo * U, d + (size_t)lo * U, (hi - lo) * U * 4,
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+      set_error("slice copy failed");
+      return TFHE_ECUDA;
+    }
+    const uint32_t* kb = key + (size_t)j * key_pair;
+    const uint32_t* ka = kb + (size_t)(g.Lc + g.K) * c.n;
+    if ((rc = launch_ks_mac(c, raised, kb, ka, acc, acc + g.E * U, row_prime, key_row, g.E, batch,
+                            first, st)))
+      return rc;
+    first = 0;
+  }
+
+  // 3. ModDown of acc_b and acc_a  (ckks.py:367-381)
+  LimbMap ms;
+  ms.n = 2 * g.K;
+  for (int cmp = 0; cmp < 2; ++cmp)
+    for (int k = 0; k < g.K; ++k) {
+      const int l = cmp * g.K + k;
+      ms.prime[l] = (int16_t)(g.Lc + k);
+      ms.in_row[l] = (int16_t)(cmp * g.E + g.l1 + k);
+      ms.out_row[l] = (int16_t)l;
+    }
+  if ((rc = launch_ntt(c, acc, ysp, ms, batch, 1, nullptr, ntt_ws, ntt_ws_bytes, st))) return rc;
+
+  const uint32_t* md_in = ysp;
+  if (g.K > 1) {
+    std::vector<int> src, dst;
+    for (int k = 0; k < g.K; ++k) src.push_back(g.Lc + k);
+    for (int i = 0; i < g.l1; ++i) dst.push_back(i);
+    BconvArgs ba;
+    if ((rc = fill_bconv(c, src, dst, ba))) return rc;
+    for (int cmp = 0; cmp < 2; ++cmp)
+      if ((rc = launch_bconv(c, ysp + (size_t)cmp * g.K * U, conv + (size_t)cmp * g.l1 * U, ba,
+                             batch, st)))
+        return rc;
+    md_in = conv;
+  }
+  uint64_t big_p_mod[kMaxLimbs];
+  for (int i = 0; i < g.l1; ++i) {
+    uint64_t pm = 1;
+    for (int k = 0; k < g.K; ++k) pm = pm * (c.primes[g.Lc + k] % c.primes[i]) % c.primes[i];
+    big_p_mod[i] = pm;
+  }
+  LimbMap md;
+  EpiArgs ep;
+  memset(&ep, 0, sizeof(ep));
+  ep.mode = EPI_SUB_SCALE;
+  ep.x = acc;
+  ep.base = base;
+  md.n = 2 * g.l1;
+  for (int cmp = 0; cmp < 2; ++cmp)
+    for (int i = 0; i < g.l1; ++i) {
+      const int l = cmp * g.l1 + i;
+      const uint32_t q = c.primes[i];
+      md.prime[l] = (int16_t)i;
+      md.in_row[l] = (int16_t)(g.K > 1 ? cmp * g.l1 + i : cmp);
+      md.out_row[l] = (int16_t)l;
+      ep.x_row[l] = (int16_t)(cmp * g.E + i);
+      ep.base_row[l] = base ? base_rows[l] : (int16_t)-1;
+      ep.s[l] = invmod(big_p_mod[i], q);
+      ep.s_shoup[l] = shoup(ep.s[l], q);
+    }
+  return launch_ntt(c, md_in, out, md, batch, 0, &ep, ntt_ws, ntt_ws_bytes, st);
+}
+
+int check_ctx(const TfheCtx* h) {
+  if (!h) {
+    set_error("null context");
+    return TFHE_EINVAL;
+  }
+  return 0;
+}
+
+int check_limbs(const TfheCtx* h, const int32_t* primes, int n) {
+  if (n < 0 || n > kMaxLimbs) {
+    set_error("limb count out of range (max " + std::to_string(kMaxLimbs) + ")");
+    return TFHE_EINVAL;
+  }
+  for (int i = 0; i < n; ++i)
+    if (primes[i] < 0 || primes[i] >= h->c.n_primes) {
+      set_error("prime index out of range");
+      return TFHE_EINVAL;
+    }
+  return 0;
+}
+
+int check_level(const TfheCtx* h, int level, int batch, int dnum) {
+  if (level < 0 || level >= h->n_chain || batch <= 0) {
+    set_error("bad level or batch");
+    return TFHE_EINVAL;
+  }
+  if (dnum != 0 && (dnum < 0 || h->n_chain % dnum != 0)) {
+    set_error("dnum must divide L+1");
+    return TFHE_EINVAL;
+  }
+  if (h->n_special <= 0 && dnum != 0) {
+    set_error("context has no special primes");
+    return TFHE_EINVAL;
+  }
+  if (2 * (level + 1) > kMaxLimbs || level + 1 + h->n_special > kMaxLimbs) {
+    set_error("too many limbs for one launch");
+    return TFHE_EINVAL;
+  }
+  return 0;
+}
+
+}  // namespace
+}  // namespace tfhe
+
+using namespace tfhe;
+
+extern "C" {
+
+int tfhe_abi_version(void) { return TFHE_ABI_VERSION; }
+const char* tfhe_last_error(void) { return g_last_error.c_str(); }
+
+int tfhe_ctx_create(int device, int log_n, const uint32_t* primes, const uint32_t* psis,
+                    int n_chain, int n_special, TfheCtx** out) {
+  if (!out || !primes || !psis || log_n < 4 || log_n > 17 || n_chain < 1 || n_special < 0 ||
+      n_chain + n_special > 200) {
+    set_error("tfhe_ctx_create: bad arguments");
+    return TFHE_EINVAL;
+  }
+  const uint32_t n = 1u << log_n;
+  for (int i = 0; i < n_chain + n_special; ++i) {
+    const uint32_t q = primes[i];
+    if (q >= (1u << 31) || q % (2 * n) != 1) {
+      set_error("prime " + std::to_string(q) + " is not 1 mod 2n or >= 2^31");
+      return TFHE_EINVAL;
+    }
+    if (powmod(psis[i], n, q) != q - 1) {
+      set_error("psi is not a negacyclic root for prime " + std::to_string(q));
+      return TFHE_EINVAL;
+    }
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    set_error("cudaSetDevice failed");
+    return TFHE_ECUDA;
+  }
+  TfheCtx* h = new TfheCtx();
+  Ctx& c = h->c;
+  c.dev = device;
+  c.log_n = log_n;
+  c.n = (int)n;
+  c.n1 = 1 << (log_n / 2);  // params.build_ntt_plan (MAX_N1 never binds for n <= 2^17)
+  c.n2 = c.n / c.n1;
+  c.n_primes = n_chain + n_special;
+  c.primes.assign(primes, primes + c.n_primes);
+  c.psis.assign(psis, psis + c.n_primes);
+  h->n_chain = n_chain;
+  h->n_special = n_special;
+  int rc = build_ntt_tables(c);
+  if (rc) {
+    tfhe_ctx_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return 0;
+}
+
+void tfhe_ctx_destroy(TfheCtx* h) {
+  if (!h) return;
+  Ctx& c = h->c;
+  cudaFree(c.d_pc);
+  for (int i = 0; i < 2; ++i) {
+    for (int s = 0; s < 2; ++s) cudaFree(c.d_tw[i][s]);
+    cudaFree(c.d_w2[i]);
+    cudaFree(c.d_w2s[i]);
+  }
+  delete h;
+}
+
+int tfhe_ctx_plan(const TfheCtx* h, int* n1, int* n2) {
+  if (check_ctx(h)) return TFHE_EINVAL;
+  if (n1) *n1 = h->c.n1;
+  if (n2) *n2 = h->c.n2;
+  return 0;
+}
+
+size_t tfhe_ntt_workspace_bytes(const TfheCtx* h, int n_limbs, int batch) {
+  return h ? ntt_workspace_bytes(h->c, n_limbs, batch) : 0;
+}
+
+int tfhe_ntt(TfheCtx* h, const uint32_t* in, uint32_t* out, const int32_t* limb_prime,
+             const int32_t* in_rows, const int32_t* out_rows, int n_limbs, int batch, int inverse,
+             void* ws, size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_ctx(h)) || (rc = check_limbs(h, limb_prime, n_limbs))) return rc;
+  if (batch < 0 || (n_limbs && (!in || !out || !ws))) {
+    set_error("tfhe_ntt: bad arguments");
+    return TFHE_EINVAL;
+  }
+  LimbMap m;
+  m.n = n_limbs;
+  for (int l = 0; l < n_limbs; ++l) {
+    m.prime[l] = (int16_t)limb_prime[l];
+    m.in_row[l] = (int16_t)(in_rows ? in_rows[l] : l);
+    m.out_row[l] = (int16_t)(out_rows ? out_rows[l] : l);
+  }
+  return launch_ntt(h->c, in, out, m, batch, inverse != 0, nullptr, ws, ws_bytes,
+                    (cudaStream_t)stream);
+}
+
+int tfhe_eltwise(TfheCtx* h, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
+                 const int32_t* row_prime, int rows, int64_t per_row, const uint32_t* scalars,
+                 void* stream) {
+  int rc;
+  if ((rc = check_ctx(h))) return rc;
+  if (rows < 0 || rows > kMaxRows || per_row % 4 || (rows && (!a || !out))) {
+    set_error("tfhe_eltwise: bad shape (rows <= 256, per_row % 4 == 0)");
+    return TFHE_EINVAL;
+  }
+  int16_t rp[kMaxRows];
+  for (int r = 0; r < rows; ++r) {
+    if (row_prime[r] < 0 || row_prime[r] >= h->c.n_primes) {
+      set_error("prime index out of range");
+      return TFHE_EINVAL;
+    }
+    rp[r] = (int16_t)row_prime[r];
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (op) {
+    case TFHE_OP_ADD:
+    case TFHE_OP_SUB:
+    case TFHE_OP_MUL:
+      if (!b) {
+        set_error("binary op needs b");
+        return TFHE_EINVAL;
+      }
+      return launch_binary(h->c, op, a, b, out, rp, rows, per_row, st);
+    case TFHE_OP_NEG: return launch_unary(h->c, OP_NEG, a, out, rp, nullptr, rows, per_row, st);
+    case TFHE_OP_SCALAR:
+      if (!scalars) {
+        set_error("scalar op needs scalars");
+        return TFHE_EINVAL;
+      }
+      return launch_unary(h->c, OP_SCALAR, a, out, rp, scalars, rows, per_row, st);
+  }
+  set_error("unknown op");
+  return TFHE_EINVAL;
+}
+
+int tfhe_automorphism(TfheCtx* h, const uint32_t* in, uint32_t* out, uint32_t galois_t,
+                      int ntt_domain, const int32_t* row_prime, int rows, int batch,
+                      void* stream) {
+  int rc;
+  if ((rc = check_ctx(h))) return rc;
+  if ((galois_t & 1) == 0 || rows < 0 || rows > kMaxRows || in == out) {
+    set_error("tfhe_automorphism: bad arguments (odd t, out != in)");
+    return TFHE_EINVAL;
+  }
+  int16_t rp[kMaxRows];
+  for (int r = 0; r < rows; ++r) rp[r] = (int16_t)(row_prime ? row_prime[r] : 0);
+  return launch_automorph(h->c, in, out, galois_t, ntt_domain, rp, rows, batch,
+                          (cudaStream_t)stream);
+}
+
+int tfhe_bconv(TfheCtx* h, const uint32_t* in, uint32_t* out, const int32_t* src_prime,
+               int n_src, const int32_t* dst_prime, int n_dst, int batch, void* stream) {
+  int rc;
+  if ((rc = check_ctx(h)) || (rc = check_limbs(h, src_prime, n_src)) ||
+      (rc = check_limbs(h, dst_prime, n_dst)))
+    return rc;
+  std::vector<int> s(src_prime, src_prime + n_src), d(dst_prime, dst_prime + n_dst);
+  BconvArgs ba;
+  if ((rc = fill_bconv(h->c, s, d, ba))) return rc;
+  return launch_bconv(h->c, in, out, ba, batch, (cudaStream_t)stream);
+}
+
+size_t tfhe_ckks_workspace_bytes(const TfheCtx* h, int level, int batch) {
+  if (!h) return 0;
+  // worst case over dnum: general base conversion buffers included
+  CkksGeom g = geom(h, level, 1);
+  g.need_conv = true;
+  const size_t U = (size_t)batch * h->c.n * 4;
+  return ks_bytes(g, batch, h->c.n) + 3 * (size_t)g.l1 * U + 256;
+}
+
+int tfhe_keyswitch(TfheCtx* h, const uint32_t* d, int level, int batch, const uint32_t* key,
+                   int dnum, uint32_t* out, const uint32_t* add, void* ws, size_t ws_bytes,
+                   void* stream) {
+  int rc;
+  if ((rc = check_ctx(h)) || (rc = check_level(h, level, batch, dnum ? dnum : -1))) return rc;
+  Carve cv{static_cast<uint8_t*>(ws), ws_bytes};
+  int16_t rows[kMaxLimbs];
+  for (int l = 0; l < 2 * (level + 1); ++l) rows[l] = (int16_t)l;
+  return keyswitch_impl(h, d, level, batch, key, dnum, out, add, rows, cv, (cudaStream_t)stream);
+}
+
+int tfhe_hmult(TfheCtx* h, const uint32_t* ct0, const uint32_t* ct1, int level, int batch,
+               const uint32_t* rlk, int dnum, uint32_t* out, void* ws, size_t ws_bytes,
+               void* stream) {
+  int rc;
+  if ((rc = check_ctx(h)) || (rc = check_level(h, level, batch, dnum ? dnum : -1))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int l1 = level + 1;
+  const size_t P = (size_t)l1 * batch * h->c.n;  // elements per component
+  Carve cv{static_cast<uint8_t*>(ws), ws_bytes};
+  uint32_t* dd = cv.take<uint32_t>(3 * P * 4);  // d0 | d1 | d2
+  if (!cv.ok) {
+    set_error("ckks workspace too small");
+    return TFHE_EINVAL;
+  }
+  int16_t rp[kMaxRows];
+  for (int i = 0; i < l1; ++i) rp[i] = (int16_t)i;
+  if ((rc = launch_tensor(h->c, ct0, ct0 + P, ct1, ct1 + P, dd, dd + P, dd + 2 * P, rp, l1,
+                          (int64_t)batch * h->c.n, st)))
+    return rc;
+  int16_t rows[kMaxLimbs];
+  for (int l = 0; l < 2 * l1; ++l) rows[l] = (int16_t)l;  // (d0, d1) added to (ksb, ksa)
+  return keyswitch_impl(h, dd + 2 * P, level, batch, rlk, dnum, out, dd, rows, cv, st);
+}
+
+int tfhe_rescale(TfheCtx* h, const uint32_t* ct, int level, int batch, uint32_t* out, void* ws,
+                 size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_ctx(h)) || (rc = check_level(h, level, batch, 0))) return rc;
+  if (level < 1) {
+    set_error("no levels left to rescale");
+    return TFHE_EINVAL;
+  }
+  const Ctx& c = h->c;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int l1 = level + 1;
+  const size_t U = (size_t)batch * c.n;
+  Carve cv{static_cast<uint8_t*>(ws), ws_bytes};
+  uint32_t* t = cv.take<uint32_t>(2 * U * 4);
+  const size_t nws = (size_t)2 * level * U * 4;
+  uint32_t* nw = cv.take<uint32_t>(nws);
+  if (!cv.ok) {
+    set_error("ckks workspace too small");
+    return TFHE_EINVAL;
+  }
+  // t = INTT_{q_top}(c_top) for b and a
+  LimbMap m;
+  m.n = 2;
+  for (int cmp = 0; cmp < 2; ++cmp) {
+    m.prime[cmp] = (int16_t)level;
+    m.in_row[cmp] = (int16_t)(cmp * l1 + level);
+    m.out_row[cmp] = (int16_t)cmp;
+  }
+  if ((rc = launch_ntt(c, ct, t, m, batch, 1, nullptr, nw, nws, st))) return rc;
+  // out_i = (c_i - NTT_{q_i}(t)) * q_top^-1 : the NTT-domain form of
+  // _rescale_poly (ckks.py:301-311), bit-identical by linearity of the NTT
+  LimbMap mr;
+  EpiArgs ep;
+  memset(&ep, 0, sizeof(ep));
+  ep.mode = EPI_SUB_SCALE;
+  ep.x = ct;
+  mr.n = 2 * level;
+  const uint32_t q_top = c.primes[level];
+  for (int cmp = 0; cmp < 2; ++cmp)
+    for (int i = 0; i < level; ++i) {
+      const int l = cmp * level + i;
+      mr.prime[l] = (int16_t)i;
+      mr.in_row[l] = (int16_t)cmp;
+      mr.out_row[l] = (int16_t)l;
+      ep.x_row[l] = (int16_t)(cmp * l1 + i);
+      ep.base_row[l] = -1;
+      ep.s[l] = invmod(q_top, c.primes[i]);
+      ep.s_shoup[l] = shoup(ep.s[l], c.primes[i]);
+    }
+  return launch_ntt(c, t, out, mr, batch, 0, &ep, nw, nws, st);
+}
+
+int tfhe_hrotate(TfheCtx* h, const uint32_t* ct, int level, int batch, uint32_t galois_t,
+                 const uint32_t* key, int dnum, uint32_t* out, void* ws, size_t ws_bytes,
+                 void* stream) {
+  int rc;
+  if ((rc = check_ctx(h)) || (rc = check_level(h, level, batch, dnum ? dnum : -1))) return rc;
+  if ((galois_t & 1) == 0) {
+    set_error("galois element must be odd");
+    return TFHE_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int l1 = level + 1;
+  const size_t P = (size_t)l1 * batch * h->c.n;
+  Carve cv{static_cast<uint8_t*>(ws), ws_bytes};
+  uint32_t* phi = cv.take<uint32_t>(2 * P * 4);
+  if (!cv.ok) {
+    set_error("ckks workspace too small");
+    return TFHE_EINVAL;
+  }
+  int16_t rp[kMaxRows];
+  for (int i = 0; i < 2 * l1; ++i) rp[i] = (int16_t)(i % l1);
+  if ((rc = launch_automorph(h->c, ct, phi, galois_t, 1, rp, 2 * l1, batch, st))) return rc;
+  int16_t rows[kMaxLimbs];
+  for (int i = 0; i < l1; ++i) {
+    rows[i] = (int16_t)i;   // b' = phi(b) + ksb
+    rows[l1 + i] = -1;      // a' = ksa
+  }
+  return keyswitch_impl(h, phi + P, level, batch, key, dnum, out, phi, rows, cv, st);
+}
+
+}  // extern "C"

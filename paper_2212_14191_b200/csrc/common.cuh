@@ -1,0 +1,161 @@
+// Shared device helpers for the sm_100a kernels: modular arithmetic on
+// canonical u32 residues (q < 2^31) and thin inline-PTX wrappers for the
+// Blackwell async machinery (mbarrier, bulk copy, tcgen05 / TMEM).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define TFHE_DEV __device__ __forceinline__
+
+namespace tfhe {
+
+// ---------------------------------------------------------------------------
+// modular arithmetic (all residues canonical in [0, q), q < 2^31)
+// ---------------------------------------------------------------------------
+
+TFHE_DEV uint32_t add_mod(uint32_t a, uint32_t b, uint32_t q) {
+  uint32_t s = a + b;
+  return s >= q ? s - q : s;
+}
+TFHE_DEV uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t q) {
+  return a >= b ? a - b : a + q - b;
+}
+// w * b mod q with wp = floor(w * 2^32 / q) (Shoup); exact for b < 2^32.
+TFHE_DEV uint32_t mul_shoup(uint32_t b, uint32_t w, uint32_t wp, uint32_t q) {
+  uint32_t t = __umulhi(wp, b);
+  uint32_t r = w * b - t * q;
+  return r >= q ? r - q : r;
+}
+// x mod q for x < 2^64 with mu = floor(2^64 / q) (Barrett, one correction
+// suffices because q < 2^31 keeps the quotient error below 2).
+TFHE_DEV uint32_t reduce64(uint64_t x, uint32_t q, uint64_t mu) {
+  uint64_t t = __umul64hi(x, mu);
+  uint64_t r = x - t * q;
+  r = r >= q ? r - q : r;
+  return (uint32_t)(r >= q ? r - q : r);
+}
+TFHE_DEV uint32_t mul_mod(uint32_t a, uint32_t b, uint32_t q, uint64_t mu) {
+  return reduce64((uint64_t)a * b, q, mu);
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory addresses, mbarriers, bulk async copies
+// ---------------------------------------------------------------------------
+
+TFHE_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+TFHE_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+TFHE_DEV void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+TFHE_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+TFHE_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+TFHE_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared through the TMA engine; completes tx bytes
+// on `bar`.  Size multiple of 16, addresses 16-byte aligned.
+TFHE_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// make this thread's generic-proxy smem writes visible to the async proxy
+// (tensor core reads of the operand tiles)
+TFHE_DEV void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 / TMEM
+// ---------------------------------------------------------------------------
+
+template <uint32_t kCols>
+TFHE_DEV void tmem_alloc(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "n"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <uint32_t kCols>
+TFHE_DEV void tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
+               : "memory");
+}
+TFHE_DEV void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+TFHE_DEV void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem], u8 x u8 -> s32, issued by ONE thread.
+TFHE_DEV void mma_i8_ss(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on `bar` once all previously issued tcgen05 ops of this thread finish
+TFHE_DEV void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// 32 lanes x 32 bit, 16 consecutive columns per thread
+TFHE_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+TFHE_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory matrix descriptor, SWIZZLE_NONE ("interleaved") K-major:
+// core matrices of 8 rows x 16 bytes stored as 128 contiguous bytes;
+// lbo = byte stride between core matrices along K, sbo = along M/N.
+TFHE_DEV uint64_t smem_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  // base_offset = 0, lbo_mode = 0, layout_type = 0 (SWIZZLE_NONE)
+  return d;
+}
+
+// instruction descriptor: kind::i8, u8 x u8 -> s32, both operands K-major
+__host__ __device__ constexpr uint32_t idesc_i8(uint32_t m, uint32_t n) {
+  return (2u << 4)              // c_format = S32
+         | (0u << 7)            // a_format = u8
+         | (0u << 10)           // b_format = u8
+         | ((n >> 3) << 17)     // N
+         | ((m >> 4) << 24);    // M
+}
+
+}  // namespace tfhe

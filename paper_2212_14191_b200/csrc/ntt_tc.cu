@@ -1,0 +1,427 @@
+// Batched negacyclic NTT / INTT on the int8 tensor cores (tcgen05, sm_100a).
+//
+// TensorFHE's formulation (§IV; reference emulation
+// pkg/src/rnsckks/ntt.py:212-222 "gemm", :249-340 "segmented"): with
+// n = n1*n2 and A[i1][i2] = a[i1*n2 + i2],
+//     S = W1 @ A,   P = S .* W2,   Y = P @ W3,   out[n1*k2 + k1] = Y[k1][k2]
+// (inverse: same with the inverse twiddles and a final n^-1, ntt.py:218-222).
+//
+// Each mod-q matrix product is computed EXACTLY on u8 x u8 -> s32 MMAs.  The
+// data operand X is split into byte planes X_j (j = 0..3).  The constant
+// twiddle operand T is pre-multiplied, V_j = 2^(8j) T mod q, and V_j is split
+// into bytes V_{j,i}.  Then
+//     T X = sum_j V_j X_j = sum_i 2^(8i) C_i  (mod q),   C_i = sum_j V_{j,i} X_j
+// i.e. 4 s32 accumulators C_i (in TMEM), each a K' = 4K contraction of bytes
+// (C_i < 4 K 255^2 < 2^31 for K <= 8192).  This is SURVEY Appendix B's
+// 4-accumulator form; the epilogue folds sum_i 2^(8i) C_i, reduces mod q
+// (Barrett), applies the Hadamard twiddle (stage 1) or the fused output
+// epilogue (stage 2) and stores.  Because every step is exact modular
+// arithmetic the result is bit-identical to the reference's butterfly backend.
+//
+// Roles ("data-as-A"): the MMA M dimension runs over data rows, N over the
+// twiddle's output index, K over the contraction:
+//   stage 1:  D[(b,i2)][k1] = sum_i1 A_b[i1][i2] * W1[k1][i1]   -> P (workspace)
+//   stage 2:  D[(b,k1)][k2] = sum_i2 P_b[k1][i2] * W3[i2][k2]   -> out[k2*n1+k1]
+// so both epilogues store coalesced along the TMEM lane (= data row) index.
+//
+// v1 kernel structure: one 128-row x BN-column output tile per CTA;
+// warps 0-3 load + byte-split data into smem and later run the epilogue,
+// one thread bulk-copies (TMA engine) the pre-split twiddle tiles, warp 4
+// owns TMEM and issues the MMAs; a 2-stage mbarrier ring overlaps loads with
+// MMAs.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "tfhe_internal.h"
+
+namespace tfhe {
+
+namespace {
+
+constexpr int kRows = 128;        // MMA M (data rows per tile)
+constexpr int kStages = 2;        // smem pipeline depth
+constexpr int kKC = 32;           // K values per pipeline stage (one MMA K-step per plane)
+constexpr int kThreads = 160;     // 4 load/epilogue warps + 1 MMA warp
+constexpr int kATile = kRows * kKC;  // bytes of one A plane tile (4 KB)
+
+struct StageArgs {
+  const uint32_t* in;    // stage 1: (rows, batch, n) input; stage 2: P workspace (L, batch, n)
+  uint32_t* out;         // stage 1: P workspace; stage 2: (rows, batch, n) output
+  const uint8_t* tw;     // twiddle tiles for this (direction, stage)
+  size_t tw_stride;      // bytes per prime
+  const uint32_t* w2;    // stage 1: hadamard twiddles (prime, n1*n2)
+  const uint32_t* w2s;
+  const PrimeConst* pc;
+  int n, n1, n2, batch;
+  int R;                 // data rows per member (stage 1: n2, stage 2: n1)
+  int K, KC;             // contraction length, number of 32-chunks (padded)
+  int Ntw;               // twiddle columns
+  int total_rows;        // batch * R
+  LimbMap map;
+  EpiArgs epi;
+};
+
+__host__ __device__ constexpr int tmem_cols_for(int bn) {
+  return 4 * bn <= 32 ? 32 : 4 * bn <= 64 ? 64 : 4 * bn <= 128 ? 128 : 4 * bn <= 256 ? 256 : 512;
+}
+
+// offset of (row r, k) inside a K-major SWIZZLE_NONE tile of `rows` x 32 bytes
+TFHE_DEV uint32_t tile_off(int r, int k, int rows) {
+  return (uint32_t)((k >> 4) * (rows * 16) + (r >> 3) * 128 + (r & 7) * 16 + (k & 15));
+}
+
+// 4x4 byte transpose: plane j gets byte j of v0..v3 (v0 in the low byte)
+TFHE_DEV void byte_planes(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, uint32_t (&w)[4]) {
+  uint32_t lo01 = __byte_perm(v0, v1, 0x5140), hi01 = __byte_perm(v0, v1, 0x7362);
+  uint32_t lo23 = __byte_perm(v2, v3, 0x5140), hi23 = __byte_perm(v2, v3, 0x7362);
+  w[0] = __byte_perm(lo01, lo23, 0x5410);
+  w[1] = __byte_perm(lo01, lo23, 0x7632);
+  w[2] = __byte_perm(hi01, hi23, 0x5410);
+  w[3] = __byte_perm(hi01, hi23, 0x7632);
+}
+
+template <int STAGE, int BN>
+__global__ void __launch_bounds__(kThreads, 1) ntt_stage_kernel(const __grid_constant__ StageArgs a) {
+  constexpr int kBTile = BN * kKC;             // bytes of one twiddle tile
+  constexpr int kStageBytes = 4 * kATile + 16 * kBTile;
+  constexpr uint32_t kTmemCols = tmem_cols_for(BN);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int limb = blockIdx.z, ct = blockIdx.y;
+  const int r0 = blockIdx.x * kRows;
+  const int prime = a.map.prime[limb];
+  const PrimeConst pc = a.pc[prime];
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 129);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 4) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ producer
+    const int gr = r0 + tid;
+    const bool valid = gr < a.total_rows;
+    const int b = valid ? gr / a.R : 0;
+    const int x = valid ? gr % a.R : 0;
+    const uint32_t* src;
+    if (STAGE == 1) {
+      src = a.in + ((size_t)a.map.in_row[limb] * a.batch + b) * a.n + x;  // X[k][x] = src[k*n2]
+    } else {
+      src = a.in + ((size_t)limb * a.batch + b) * a.n + (size_t)x * a.n2;  // P[x][k] = src[k]
+    }
+    const uint8_t* twp = a.tw + (size_t)prime * a.tw_stride + (size_t)ct * a.KC * 16 * kBTile;
+    for (int kc = 0; kc < a.KC; ++kc) {
+      const int s = kc % kStages;
+      if (kc >= kStages) mbar_wait(&empty[s], ((kc / kStages) & 1) ^ 1);
+      uint8_t* sA = smem + s * kStageBytes;
+      uint8_t* sB = sA + 4 * kATile;
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&full[s], 16 * kBTile);
+        bulk_g2s(sB, twp + (size_t)kc * 16 * kBTile, 16 * kBTile, &full[s]);
+      }
+#pragma unroll
+      for (int kq = 0; kq < kKC / 4; ++kq) {
+        const int k = kc * kKC + kq * 4;
+        uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+        if (valid && k < a.K) {
+          if (STAGE == 1) {
+            const uint32_t* p = src + (size_t)k * a.n2;
+            v0 = __ldg(p);
+            v1 = __ldg(p + a.n2);
+            v2 = __ldg(p + 2 * a.n2);
+            v3 = __ldg(p + 3 * a.n2);
+          } else {
+            uint4 v = __ldg(reinterpret_cast<const uint4*>(src + k));
+            v0 = v.x; v1 = v.y; v2 = v.z; v3 = v.w;
+          }
+        }
+        uint32_t w[4];
+        byte_planes(v0, v1, v2, v3, w);
+        const uint32_t off = tile_off(tid, kq * 4, kRows);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) *reinterpret_cast<uint32_t*>(sA + j * kATile + off) = w[j];
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&full[s]);
+    }
+
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t acc[4][16];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tmem_ld16(lane_base + i * BN + c0, acc[i]);
+      tmem_ld_wait();
+      if (!valid) continue;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int col = ct * BN + c0 + e;
+        if (col >= a.Ntw) break;
+        uint64_t v = (uint64_t)acc[0][e] + ((uint64_t)acc[1][e] << 8) +
+                     ((uint64_t)acc[2][e] << 16) + ((uint64_t)acc[3][e] << 24);
+        uint32_t y = reduce64(v, pc.q, pc.mu);
+        if (STAGE == 1) {
+          // P[k1=col][i2=x] = S * W2[k1][i2]
+          const size_t widx = (size_t)prime * a.n + (size_t)col * a.n2 + x;
+          y = mul_shoup(y, __ldg(a.w2 + widx), __ldg(a.w2s + widx), pc.q);
+          a.out[((size_t)limb * a.batch + b) * a.n + (size_t)col * a.n2 + x] = y;
+        } else {
+          // out[n1*k2 + k1], k2 = col, k1 = x
+          const size_t pos = (size_t)col * a.n1 + x;
+          const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n;
+          if (a.epi.mode == EPI_SUB_SCALE) {
+            const uint32_t xv = a.epi.x[((size_t)a.epi.x_row[limb] * a.batch + b) * a.n + pos];
+            y = mul_shoup(sub_mod(xv, y, pc.q), a.epi.s[limb], a.epi.s_shoup[limb], pc.q);
+            const int br = a.epi.base_row[limb];
+            if (br >= 0)
+              y = add_mod(a.epi.base[((size_t)br * a.batch + b) * a.n + pos], y, pc.q);
+          }
+          a.out[orow + pos] = y;
+        }
+      }
+    }
+  } else if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = idesc_i8(kRows, BN);
+    for (int kc = 0; kc < a.KC; ++kc) {
+      const int s = kc % kStages;
+      mbar_wait(&full[s], (kc / kStages) & 1);
+      tc_fence_after();
+      const uint32_t sA = smem_u32(smem + s * kStageBytes);
+      const uint32_t sB = sA + 4 * kATile;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t adesc = smem_desc_kmajor(sA + j * kATile, kRows * 16, 128);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint64_t bdesc = smem_desc_kmajor(sB + (j * 4 + i) * kBTile, BN * 16, 128);
+          mma_i8_ss(tmem + i * BN, adesc, bdesc, idesc, (kc | j) != 0);
+        }
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(tfull);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+template <int STAGE, int BN>
+int launch_stage(const StageArgs& a, int npad, int n_limbs, cudaStream_t st) {
+  constexpr int kStageBytes = 4 * kATile + 16 * BN * kKC;
+  const int smem = kStages * kStageBytes + 2 * kStages * 8 + 8 + 16;
+  auto kern = ntt_stage_kernel<STAGE, BN>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  dim3 grid((a.total_rows + kRows - 1) / kRows, npad / BN, n_limbs);
+  kern<<<grid, kThreads, smem, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("ntt stage launch: ") + cudaGetErrorString(e));
+    return 3;
+  }
+  return 0;
+}
+
+template <int STAGE>
+int launch_stage_bn(int bn, const StageArgs& a, int npad, int n_limbs, cudaStream_t st) {
+  switch (bn) {
+    case 16: return launch_stage<STAGE, 16>(a, npad, n_limbs, st);
+    case 32: return launch_stage<STAGE, 32>(a, npad, n_limbs, st);
+    case 64: return launch_stage<STAGE, 64>(a, npad, n_limbs, st);
+    case 128: return launch_stage<STAGE, 128>(a, npad, n_limbs, st);
+  }
+  set_error("unsupported tile width");
+  return 2;
+}
+
+// --------------------------------------------------------------- host tables
+
+uint32_t mulmod_h(uint64_t a, uint64_t b, uint32_t q) { return (uint32_t)(a * b % q); }
+uint32_t powmod_h(uint64_t b, uint64_t e, uint32_t q) {
+  uint64_t r = 1, x = b % q;
+  while (e) {
+    if (e & 1) r = r * x % q;
+    x = x * x % q;
+    e >>= 1;
+  }
+  return (uint32_t)r;
+}
+uint32_t shoup_h(uint32_t w, uint32_t q) { return (uint32_t)(((uint64_t)w << 32) / q); }
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+}  // namespace
+
+size_t ntt_workspace_bytes(const Ctx& c, int n_limbs, int batch) {
+  return (size_t)n_limbs * batch * c.n * sizeof(uint32_t);
+}
+
+int build_ntt_tables(Ctx& c) {
+  const int n = c.n, n1 = c.n1, n2 = c.n2, np = c.n_primes;
+  const uint64_t two_n = 2ull * n;
+  // geometry per stage: stage 0 contracts over n1 (twiddle cols n1), stage 1 over n2
+  for (int s = 0; s < 2; ++s) {
+    const int ntw = s == 0 ? n1 : n2;
+    c.bn[s] = ntw >= 128 ? 128 : ntw >= 64 ? 64 : ntw >= 32 ? 32 : 16;
+    c.npad[s] = round_up(ntw, c.bn[s]);
+    c.kpad[s] = round_up(ntw, kKC);
+    c.tw_stride[s] = (size_t)c.npad[s] * c.kpad[s] * 16;
+  }
+  c.h_pc.resize(np);
+  std::vector<uint8_t> tw;
+  std::vector<uint32_t> w2((size_t)np * n), w2s((size_t)np * n);
+  std::vector<uint32_t> pw(two_n), T;
+  for (int inv = 0; inv < 2; ++inv) {
+    for (int s = 0; s < 2; ++s) {
+      const int ntw = s == 0 ? n1 : n2, K = ntw, BN = c.bn[s], KC = c.kpad[s] / kKC;
+      tw.assign(c.tw_stride[s] * np, 0);
+      T.resize((size_t)ntw * K);
+      for (int p = 0; p < np; ++p) {
+        const uint32_t q = c.primes[p];
+        uint32_t root = inv ? powmod_h(c.psis[p], q - 2, q) : c.psis[p];
+        pw[0] = 1;
+        for (uint64_t e = 1; e < two_n; ++e) pw[e] = mulmod_h(pw[e - 1], root, q);
+        const uint32_t n_inv = powmod_h(n, q - 2, q);
+        if (inv == 0 && s == 0) {
+          PrimeConst& k = c.h_pc[p];
+          k.q = q;
+          k.n_inv = n_inv;
+          k.n_inv_shoup = shoup_h(n_inv, q);
+          k.mu = (uint64_t)(~0ull / q);  // floor((2^64-1)/q) == floor(2^64/q) for non-power-of-2 q
+          k.pad = 0;
+        }
+        // T[c][k]: value multiplying data index k for output column c
+        for (int cc = 0; cc < ntw; ++cc)
+          for (int k = 0; k < K; ++k) {
+            uint64_t e;
+            if (s == 0)  // W1[k1=cc][i1=k]
+              e = inv ? (uint64_t)n2 * (2ull * cc * k) : (uint64_t)n2 * (2ull * cc * k + k);
+            else  // W3[i2=k][k2=cc]
+              e = inv ? (uint64_t)n1 * (2ull * k * cc + cc) : (uint64_t)n1 * (2ull * k * cc);
+            uint32_t v = pw[e % two_n];
+            if (s == 1 && inv) v = mulmod_h(v, n_inv, q);
+            T[(size_t)cc * K + k] = v;
+          }
+        uint8_t* base = tw.data() + (size_t)p * c.tw_stride[s];
+        for (int cc = 0; cc < ntw; ++cc) {
+          const int ct = cc / BN, cr = cc % BN;
+          for (int k = 0; k < K; ++k) {
+            const int kc = k / kKC, kr = k % kKC;
+            uint32_t t = T[(size_t)cc * K + k];
+            for (int j = 0; j < 4; ++j) {
+              uint32_t vj = mulmod_h(t, 1ull << (8 * j), q);
+              for (int i = 0; i < 4; ++i) {
+                size_t tile = ((size_t)(ct * KC + kc) * 4 + j) * 4 + i;
+                size_t off = tile * (BN * kKC) + (kr >> 4) * (BN * 16) + (cr >> 3) * 128 +
+                             (cr & 7) * 16 + (kr & 15);
+                base[off] = (uint8_t)(vj >> (8 * i));
+              }
+            }
+          }
+        }
+        if (s == 0) {
+          for (int k1 = 0; k1 < n1; ++k1)
+            for (int i2 = 0; i2 < n2; ++i2) {
+              uint64_t e = inv ? (2ull * k1 * i2 + k1) : (2ull * k1 * i2 + i2);
+              uint32_t v = pw[e % two_n];
+              w2[(size_t)p * n + (size_t)k1 * n2 + i2] = v;
+              w2s[(size_t)p * n + (size_t)k1 * n2 + i2] = shoup_h(v, q);
+            }
+        }
+      }
+      if (cudaMalloc(&c.d_tw[inv][s], tw.size()) != cudaSuccess ||
+          cudaMemcpy(c.d_tw[inv][s], tw.data(), tw.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        set_error("twiddle upload failed");
+        return 3;
+      }
+      if (s == 0) {
+        size_t bytes = w2.size() * 4;
+        if (cudaMalloc(&c.d_w2[inv], bytes) != cudaSuccess ||
+            cudaMalloc(&c.d_w2s[inv], bytes) != cudaSuccess ||
+            cudaMemcpy(c.d_w2[inv], w2.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(c.d_w2s[inv], w2s.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+          set_error("hadamard twiddle upload failed");
+          return 3;
+        }
+      }
+    }
+  }
+  if (cudaMalloc(&c.d_pc, sizeof(PrimeConst) * np) != cudaSuccess ||
+      cudaMemcpy(c.d_pc, c.h_pc.data(), sizeof(PrimeConst) * np, cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
+    set_error("prime constant upload failed");
+    return 3;
+  }
+  return 0;
+}
+
+int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& map, int batch,
+               int inverse, const EpiArgs* epi, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (map.n <= 0 || batch <= 0) return 0;
+  if (ws_bytes < ntt_workspace_bytes(c, map.n, batch)) {
+    set_error("ntt workspace too small");
+    return 2;
+  }
+  StageArgs a;
+  memset(&a, 0, sizeof(a));
+  a.pc = c.d_pc;
+  a.n = c.n;
+  a.n1 = c.n1;
+  a.n2 = c.n2;
+  a.batch = batch;
+  a.map = map;
+  if (epi) a.epi = *epi;
+  else a.epi.mode = EPI_STORE;
+  uint32_t* P = static_cast<uint32_t*>(ws);
+  // stage 1: columns of W1 (k1), contraction over i1, rows (b, i2)
+  a.in = in;
+  a.out = P;
+  a.tw = c.d_tw[inverse][0];
+  a.tw_stride = c.tw_stride[0];
+  a.w2 = c.d_w2[inverse];
+  a.w2s = c.d_w2s[inverse];
+  a.R = c.n2;
+  a.K = c.n1;
+  a.KC = c.kpad[0] / kKC;
+  a.Ntw = c.n1;
+  a.total_rows = batch * c.n2;
+  int rc = launch_stage_bn<1>(c.bn[0], a, c.npad[0], map.n, st);
+  if (rc) return rc;
+  // stage 2: columns of W3 (k2), contraction over i2, rows (b, k1)
+  a.in = P;
+  a.out = out;
+  a.tw = c.d_tw[inverse][1];
+  a.tw_stride = c.tw_stride[1];
+  a.R = c.n1;
+  a.K = c.n2;
+  a.KC = c.kpad[1] / kKC;
+  a.Ntw = c.n2;
+  a.total_rows = batch * c.n1;
+  return launch_stage_bn<2>(c.bn[1], a, c.npad[1], map.n, st);
+}
+
+}  // namespace tfhe

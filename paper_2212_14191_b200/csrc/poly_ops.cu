@@ -1,0 +1,336 @@
+// HBM-bound element-wise, automorphism and base-conversion kernels.
+//
+// All operate on level-major buffers (rows, batch, n) of canonical u32
+// residues, one prime per row (reference layout, batch.py:22-47).  Row r of a
+// launch uses prime `row_prime[r]`; the prime table lives in the context.
+//
+//   ele_add / ele_sub / hada_mult / negate / scalar_rows_mult  kernels.py:33-67
+//   tensor product (hmult's d0, d1, d2)                       ckks.py:265-271
+//   key-switch inner product acc += raised * key              ckks.py:345-351
+//   NTT-domain automorphism gather / coeff-domain signed scatter kernels.py:77-107
+//   fast base conversion                                      rns.py:118-152
+//
+// Each thread moves 16-byte vectors (uint4) with a grid-stride loop; grids
+// are sized as a multiple of the SM count.
+#include <cstring>
+
+#include "common.cuh"
+#include "poly_ops.h"
+
+namespace tfhe {
+
+namespace {
+
+struct RowPrimes {
+  int16_t prime[kMaxRows];
+};
+
+TFHE_DEV uint4 ld4(const uint32_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+TFHE_DEV void st4(uint32_t* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
+
+template <int OP>
+TFHE_DEV uint32_t binop(uint32_t x, uint32_t y, const PrimeConst& pc) {
+  if (OP == OP_ADD) return add_mod(x, y, pc.q);
+  if (OP == OP_SUB) return sub_mod(x, y, pc.q);
+  return mul_mod(x, y, pc.q, pc.mu);
+}
+
+// out = a (op) b, row-wise primes; per_row elements per row (multiple of 4)
+template <int OP>
+__global__ void binary_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                              uint32_t* __restrict__ out, const PrimeConst* __restrict__ pcs,
+                              const __grid_constant__ RowPrimes rp, int64_t per_row) {
+  const int row = blockIdx.y;
+  const PrimeConst pc = pcs[rp.prime[row]];
+  const int64_t base = (int64_t)row * per_row;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+    uint4 x = ld4(a + base + i), y = ld4(b + base + i), r;
+    r.x = binop<OP>(x.x, y.x, pc);
+    r.y = binop<OP>(x.y, y.y, pc);
+    r.z = binop<OP>(x.z, y.z, pc);
+    r.w = binop<OP>(x.w, y.w, pc);
+    st4(out + base + i, r);
+  }
+}
+
+struct ScalarArgs {
+  int16_t prime[kMaxRows];
+  uint32_t s[kMaxRows], s_shoup[kMaxRows];
+};
+
+// out = a * s_row (OP_SCALAR) or q - a (OP_NEG)
+template <int OP>
+__global__ void unary_kernel(const uint32_t* __restrict__ a, uint32_t* __restrict__ out,
+                             const PrimeConst* __restrict__ pcs,
+                             const __grid_constant__ ScalarArgs sa, int64_t per_row) {
+  const int row = blockIdx.y;
+  const uint32_t q = pcs[sa.prime[row]].q;
+  const uint32_t s = sa.s[row], sp = sa.s_shoup[row];
+  const int64_t base = (int64_t)row * per_row;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+    uint4 x = ld4(a + base + i), r;
+    if (OP == OP_NEG) {
+      r.x = x.x ? q - x.x : 0;
+      r.y = x.y ? q - x.y : 0;
+      r.z = x.z ? q - x.z : 0;
+      r.w = x.w ? q - x.w : 0;
+    } else {
+      r.x = mul_shoup(x.x, s, sp, q);
+      r.y = mul_shoup(x.y, s, sp, q);
+      r.z = mul_shoup(x.z, s, sp, q);
+      r.w = mul_shoup(x.w, s, sp, q);
+    }
+    st4(out + base + i, r);
+  }
+}
+
+// hmult tensor product: d0 = b0 b1, d1 = a0 b1 + a1 b0, d2 = a0 a1
+__global__ void tensor_kernel(const uint32_t* __restrict__ b0, const uint32_t* __restrict__ a0,
+                              const uint32_t* __restrict__ b1, const uint32_t* __restrict__ a1,
+                              uint32_t* __restrict__ d0, uint32_t* __restrict__ d1,
+                              uint32_t* __restrict__ d2, const PrimeConst* __restrict__ pcs,
+                              const __grid_constant__ RowPrimes rp, int64_t per_row) {
+  const int row = blockIdx.y;
+  const PrimeConst pc = pcs[rp.prime[row]];
+  const int64_t base = (int64_t)row * per_row;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+    const int64_t o = base + i;
+    uint4 xb0 = ld4(b0 + o), xa0 = ld4(a0 + o), xb1 = ld4(b1 + o), xa1 = ld4(a1 + o);
+    uint4 r0, r1, r2;
+#define TFHE_TP(c)                                                                  \
+  r0.c = mul_mod(xb0.c, xb1.c, pc.q, pc.mu);                                        \
+  r1.c = add_mod(mul_mod(xa0.c, xb1.c, pc.q, pc.mu), mul_mod(xa1.c, xb0.c, pc.q, pc.mu), \
+                 pc.q);                                                             \
+  r2.c = mul_mod(xa0.c, xa1.c, pc.q, pc.mu);
+    TFHE_TP(x) TFHE_TP(y) TFHE_TP(z) TFHE_TP(w)
+#undef TFHE_TP
+    st4(d0 + o, r0);
+    st4(d1 + o, r1);
+    st4(d2 + o, r2);
+  }
+}
+
+struct MacArgs {
+  int16_t prime[kMaxRows];
+  int32_t key_row[kMaxRows];  // row of the (rows_key, n) key matrices
+};
+
+// acc_b[r] (+)= x[r] * kb[key_row[r]], acc_a[r] (+)= x[r] * ka[key_row[r]];
+// keys are (rows, n) and broadcast over the batch.  first != 0 overwrites.
+__global__ void ks_mac_kernel(const uint32_t* __restrict__ x, const uint32_t* __restrict__ kb,
+                              const uint32_t* __restrict__ ka, uint32_t* __restrict__ acc_b,
+                              uint32_t* __restrict__ acc_a, const PrimeConst* __restrict__ pcs,
+                              const __grid_constant__ MacArgs ma, int batch, int n, int first) {
+  const int row = blockIdx.y;
+  const PrimeConst pc = pcs[ma.prime[row]];
+  const int64_t per_row = (int64_t)batch * n;
+  const int64_t base = (int64_t)row * per_row;
+  const uint32_t* kbr = kb + (int64_t)ma.key_row[row] * n;
+  const uint32_t* kar = ka + (int64_t)ma.key_row[row] * n;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+    const int64_t o = base + i;
+    const int coef = (int)(i % n);
+    uint4 v = ld4(x + o), wb = ld4(kbr + coef), wa = ld4(kar + coef);
+    uint4 ob = first ? make_uint4(0, 0, 0, 0) : ld4(acc_b + o);
+    uint4 oa = first ? make_uint4(0, 0, 0, 0) : ld4(acc_a + o);
+#define TFHE_MAC(c)                                                  \
+  ob.c = add_mod(ob.c, mul_mod(v.c, wb.c, pc.q, pc.mu), pc.q);       \
+  oa.c = add_mod(oa.c, mul_mod(v.c, wa.c, pc.q, pc.mu), pc.q);
+    TFHE_MAC(x) TFHE_MAC(y) TFHE_MAC(z) TFHE_MAC(w)
+#undef TFHE_MAC
+    st4(acc_b + o, ob);
+    st4(acc_a + o, oa);
+  }
+}
+
+// NTT domain: out[k] = in[((t (2k+1) mod 2n) - 1) / 2]   (kernels.py:77-96)
+__global__ void automorph_ntt_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                     uint32_t t, int log_n, int64_t rows) {
+  const uint32_t n = 1u << log_n, mask2n = 2 * n - 1;
+  const int64_t total = rows << log_n;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < total;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+    const int64_t rbase = i & ~(int64_t)(n - 1);
+    const uint32_t k = (uint32_t)(i & (n - 1));
+    uint4 r;
+    r.x = __ldg(in + rbase + (((t * (2 * k + 1)) & mask2n) >> 1));
+    r.y = __ldg(in + rbase + (((t * (2 * k + 3)) & mask2n) >> 1));
+    r.z = __ldg(in + rbase + (((t * (2 * k + 5)) & mask2n) >> 1));
+    r.w = __ldg(in + rbase + (((t * (2 * k + 7)) & mask2n) >> 1));
+    st4(out + i, r);
+  }
+}
+
+// coefficient domain: x^i -> +-x^{t i mod n}  (kernels.py:97-107)
+__global__ void automorph_coeff_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                       const PrimeConst* __restrict__ pcs,
+                                       const __grid_constant__ RowPrimes rp, uint32_t t, int log_n,
+                                       int batch) {
+  const uint32_t n = 1u << log_n;
+  const int row = blockIdx.y;
+  const uint32_t q = pcs[rp.prime[row]].q;
+  const int64_t per_row = (int64_t)batch << log_n;
+  const int64_t base = (int64_t)row * per_row;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per_row;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pbase = base + (i & ~(int64_t)(n - 1));
+    const uint32_t c = (uint32_t)(i & (n - 1));
+    const uint32_t e = (uint32_t)(((uint64_t)t * c) & (2 * n - 1));
+    uint32_t v = __ldg(in + base + i);
+    if (e >= n) v = v ? q - v : 0;
+    out[pbase + (e & (n - 1))] = v;
+  }
+}
+
+// fast base conversion (rns.py:118-152), one output row per blockIdx.y
+__global__ void bconv_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                             const PrimeConst* __restrict__ pcs,
+                             const __grid_constant__ BconvArgs ba, int64_t per_row) {
+  const int t = blockIdx.y;
+  const int copy = ba.copy_from[t];
+  const PrimeConst pt = pcs[ba.dst_prime[t]];
+  uint32_t* o = out + (int64_t)t * per_row;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+    if (copy >= 0) {
+      st4(o + i, ld4(in + (int64_t)copy * per_row + i));
+      continue;
+    }
+    uint64_t acc[4] = {0, 0, 0, 0};
+    for (int s = 0; s < ba.n_src; ++s) {
+      const PrimeConst ps = pcs[ba.src_prime[s]];
+      uint4 x = ld4(in + (int64_t)s * per_row + i);
+      const uint32_t hi = ba.qhat_inv[s], hs = ba.qhat_inv_shoup[s];
+      const uint32_t f = ba.factor[s * kMaxBconvDst + t];
+      uint32_t y0 = mul_shoup(x.x, hi, hs, ps.q), y1 = mul_shoup(x.y, hi, hs, ps.q);
+      uint32_t y2 = mul_shoup(x.z, hi, hs, ps.q), y3 = mul_shoup(x.w, hi, hs, ps.q);
+      // y < 2^31, f < 2^31: each product < 2^62; reduce every term
+      acc[0] += reduce64((uint64_t)y0 * f, pt.q, pt.mu);
+      acc[1] += reduce64((uint64_t)y1 * f, pt.q, pt.mu);
+      acc[2] += reduce64((uint64_t)y2 * f, pt.q, pt.mu);
+      acc[3] += reduce64((uint64_t)y3 * f, pt.q, pt.mu);
+    }
+    st4(o + i, make_uint4(reduce64(acc[0], pt.q, pt.mu), reduce64(acc[1], pt.q, pt.mu),
+                          reduce64(acc[2], pt.q, pt.mu), reduce64(acc[3], pt.q, pt.mu)));
+  }
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+dim3 grid_rows(int64_t per_row, int rows, int threads) {
+  // enough blocks per row to cover it with 4-wide threads, capped so the
+  // whole grid is a few waves of the SM count
+  int64_t need = (per_row / 4 + threads - 1) / threads;
+  int64_t cap = std::max<int64_t>(1, (int64_t)sm_count() * 8 / std::max(rows, 1));
+  return dim3((unsigned)std::max<int64_t>(1, std::min(need, cap)), rows);
+}
+
+int check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return 3;
+  }
+  return 0;
+}
+
+}  // namespace
+
+int launch_binary(const Ctx& c, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
+                  const int16_t* row_prime, int rows, int64_t per_row, cudaStream_t st) {
+  if (rows <= 0 || per_row <= 0) return 0;
+  RowPrimes rp;
+  memcpy(rp.prime, row_prime, sizeof(int16_t) * rows);
+  dim3 g = grid_rows(per_row, rows, 256);
+  switch (op) {
+    case OP_ADD: binary_kernel<OP_ADD><<<g, 256, 0, st>>>(a, b, out, c.d_pc, rp, per_row); break;
+    case OP_SUB: binary_kernel<OP_SUB><<<g, 256, 0, st>>>(a, b, out, c.d_pc, rp, per_row); break;
+    case OP_MUL: binary_kernel<OP_MUL><<<g, 256, 0, st>>>(a, b, out, c.d_pc, rp, per_row); break;
+    default: set_error("bad binary op"); return 2;
+  }
+  return check("binary kernel");
+}
+
+int launch_unary(const Ctx& c, int op, const uint32_t* a, uint32_t* out, const int16_t* row_prime,
+                 const uint32_t* scalars, int rows, int64_t per_row, cudaStream_t st) {
+  if (rows <= 0 || per_row <= 0) return 0;
+  ScalarArgs sa;
+  for (int r = 0; r < rows; ++r) {
+    sa.prime[r] = row_prime[r];
+    const uint32_t q = c.h_pc[row_prime[r]].q;
+    sa.s[r] = scalars ? scalars[r] % q : 0;
+    sa.s_shoup[r] = (uint32_t)(((uint64_t)sa.s[r] << 32) / q);
+  }
+  dim3 g = grid_rows(per_row, rows, 256);
+  if (op == OP_NEG) unary_kernel<OP_NEG><<<g, 256, 0, st>>>(a, out, c.d_pc, sa, per_row);
+  else if (op == OP_SCALAR) unary_kernel<OP_SCALAR><<<g, 256, 0, st>>>(a, out, c.d_pc, sa, per_row);
+  else { set_error("bad unary op"); return 2; }
+  return check("unary kernel");
+}
+
+int launch_tensor(const Ctx& c, const uint32_t* b0, const uint32_t* a0, const uint32_t* b1,
+                  const uint32_t* a1, uint32_t* d0, uint32_t* d1, uint32_t* d2,
+                  const int16_t* row_prime, int rows, int64_t per_row, cudaStream_t st) {
+  if (rows <= 0 || per_row <= 0) return 0;
+  RowPrimes rp;
+  memcpy(rp.prime, row_prime, sizeof(int16_t) * rows);
+  dim3 g = grid_rows(per_row, rows, 256);
+  tensor_kernel<<<g, 256, 0, st>>>(b0, a0, b1, a1, d0, d1, d2, c.d_pc, rp, per_row);
+  return check("tensor kernel");
+}
+
+int launch_ks_mac(const Ctx& c, const uint32_t* x, const uint32_t* kb, const uint32_t* ka,
+                  uint32_t* acc_b, uint32_t* acc_a, const int16_t* row_prime,
+                  const int32_t* key_row, int rows, int batch, int first, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  MacArgs ma;
+  for (int r = 0; r < rows; ++r) {
+    ma.prime[r] = row_prime[r];
+    ma.key_row[r] = key_row[r];
+  }
+  dim3 g = grid_rows((int64_t)batch * c.n, rows, 256);
+  ks_mac_kernel<<<g, 256, 0, st>>>(x, kb, ka, acc_b, acc_a, c.d_pc, ma, batch, c.n, first);
+  return check("ks mac kernel");
+}
+
+int launch_automorph(const Ctx& c, const uint32_t* in, uint32_t* out, uint32_t t, int ntt_domain,
+                     const int16_t* row_prime, int rows, int batch, cudaStream_t st) {
+  if (rows <= 0 || batch <= 0) return 0;
+  t &= (uint32_t)(2 * c.n - 1);
+  if (ntt_domain) {
+    int64_t total = (int64_t)rows * batch * c.n;
+    int64_t blocks = std::min<int64_t>((total / 4 + 255) / 256, (int64_t)sm_count() * 16);
+    automorph_ntt_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(
+        in, out, t, c.log_n, (int64_t)rows * batch);
+  } else {
+    RowPrimes rp;
+    memcpy(rp.prime, row_prime, sizeof(int16_t) * rows);
+    dim3 g = grid_rows((int64_t)batch * c.n * 4, rows, 256);
+    automorph_coeff_kernel<<<g, 256, 0, st>>>(in, out, c.d_pc, rp, t, c.log_n, batch);
+  }
+  return check("automorphism kernel");
+}
+
+int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,
+                 cudaStream_t st) {
+  if (ba.n_dst <= 0) return 0;
+  int64_t per_row = (int64_t)batch * c.n;
+  dim3 g = grid_rows(per_row, ba.n_dst, 256);
+  bconv_kernel<<<g, 256, 0, st>>>(in, out, c.d_pc, ba, per_row);
+  return check("bconv kernel");
+}
+
+}  // namespace tfhe

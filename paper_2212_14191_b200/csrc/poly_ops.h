@@ -1,0 +1,37 @@
+// Launchers for the HBM-bound polynomial kernels (poly_ops.cu).
+#pragma once
+#include "tfhe_internal.h"
+
+namespace tfhe {
+
+constexpr int kMaxRows = 256;         // rows addressed by one element-wise launch
+constexpr int kMaxBconvSrc = 16;
+constexpr int kMaxBconvDst = 128;
+
+enum PolyOp : int { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_NEG = 3, OP_SCALAR = 4 };
+
+struct BconvArgs {
+  int n_src, n_dst;
+  int16_t src_prime[kMaxBconvSrc];
+  int16_t dst_prime[kMaxBconvDst];
+  int16_t copy_from[kMaxBconvDst];            // >=0: dst row copies src row (shared prime)
+  uint32_t qhat_inv[kMaxBconvSrc], qhat_inv_shoup[kMaxBconvSrc];
+  uint32_t factor[kMaxBconvSrc * kMaxBconvDst];  // (Q/q_s) mod p_t, indexed s*kMaxBconvDst+t
+};
+
+int launch_binary(const Ctx& c, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
+                  const int16_t* row_prime, int rows, int64_t per_row, cudaStream_t st);
+int launch_unary(const Ctx& c, int op, const uint32_t* a, uint32_t* out, const int16_t* row_prime,
+                 const uint32_t* scalars, int rows, int64_t per_row, cudaStream_t st);
+int launch_tensor(const Ctx& c, const uint32_t* b0, const uint32_t* a0, const uint32_t* b1,
+                  const uint32_t* a1, uint32_t* d0, uint32_t* d1, uint32_t* d2,
+                  const int16_t* row_prime, int rows, int64_t per_row, cudaStream_t st);
+int launch_ks_mac(const Ctx& c, const uint32_t* x, const uint32_t* kb, const uint32_t* ka,
+                  uint32_t* acc_b, uint32_t* acc_a, const int16_t* row_prime,
+                  const int32_t* key_row, int rows, int batch, int first, cudaStream_t st);
+int launch_automorph(const Ctx& c, const uint32_t* in, uint32_t* out, uint32_t t, int ntt_domain,
+                     const int16_t* row_prime, int rows, int batch, cudaStream_t st);
+int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,
+                 cudaStream_t st);
+
+}  // namespace tfhe

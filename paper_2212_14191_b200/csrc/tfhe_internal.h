@@ -1,0 +1,71 @@
+// Internal (C++) view of the context and kernel launch interfaces.
+// Not part of the C ABI (that is include/tfhe_b200.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace tfhe {
+
+constexpr int kMaxLimbs = 128;  // rows one launch may address
+
+struct PrimeConst {
+  uint32_t q;
+  uint32_t n_inv;       // n^-1 mod q
+  uint64_t mu;          // floor(2^64 / q)
+  uint32_t n_inv_shoup;
+  uint32_t pad;
+};
+
+// Per-launch limb map: output row l uses prime `prime[l]`, reads input row
+// `in_row[l]` and writes output row `out_row[l]` (rows index the leading
+// axis of (rows, batch, n) buffers).
+struct LimbMap {
+  int n;
+  int16_t prime[kMaxLimbs];
+  int16_t in_row[kMaxLimbs];
+  int16_t out_row[kMaxLimbs];
+};
+
+enum EpiMode : int {
+  EPI_STORE = 0,       // out = NTT(in)
+  EPI_SUB_SCALE = 1,   // out = (x - NTT(in)) * s  [+ base]   (ModDown, rescale)
+};
+
+struct EpiArgs {
+  int mode;
+  const uint32_t* x;      // (x_rows, batch, n): subtrahend source, row = x_row[l]
+  const uint32_t* base;   // optional addend (base_rows, batch, n), row = base_row[l] (-1: none)
+  int16_t x_row[kMaxLimbs];
+  int16_t base_row[kMaxLimbs];
+  uint32_t s[kMaxLimbs];        // per-limb scale
+  uint32_t s_shoup[kMaxLimbs];
+};
+
+struct Ctx {
+  int dev = 0;
+  int log_n = 0, n = 0, n1 = 0, n2 = 0;
+  int n_primes = 0;
+  std::vector<uint32_t> primes, psis;
+  // device tables
+  PrimeConst* d_pc = nullptr;
+  uint8_t* d_tw[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [inverse][stage]
+  size_t tw_stride[2] = {0, 0};                                   // bytes per prime, per stage
+  int kpad[2] = {0, 0}, npad[2] = {0, 0}, bn[2] = {0, 0};
+  uint32_t* d_w2[2] = {nullptr, nullptr};   // [inverse] (prime, n1*n2) hadamard twiddles
+  uint32_t* d_w2s[2] = {nullptr, nullptr};  // Shoup companions
+  std::vector<PrimeConst> h_pc;
+};
+
+// kernels (ntt_tc.cu)
+size_t ntt_workspace_bytes(const Ctx& c, int n_limbs, int batch);
+int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& map, int batch,
+               int inverse, const EpiArgs* epi, void* ws, size_t ws_bytes, cudaStream_t st);
+int build_ntt_tables(Ctx& c);
+
+void set_error(const std::string& msg);
+
+}  // namespace tfhe

@@ -1,0 +1,234 @@
+"""Device contexts and buffer plumbing between the operator API and the C ABI.
+
+PyTorch is used here only as the device-memory / stream plumbing: residues
+live in int32 CUDA tensors (bit-identical views of u32), raw pointers and the
+current stream go to the extension, and nothing is computed by torch.
+
+`DeviceContext` owns one `TfheCtx` (twiddle and constant tables on one GPU)
+for a degree n and an ordered prime list.  Contexts are cached per
+(device, n, primes, n_chain, n_special) so every operator reuses them.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DeviceError, ParameterError
+from .params import find_negacyclic_root
+
+_CTX_CACHE: dict = {}
+_LOCK = threading.Lock()
+
+
+def default_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible: the B200 path has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def to_device(x, device=None):
+    """numpy / torch (u32 or i32) -> contiguous int32 CUDA tensor; (tensor, was_host)."""
+    device = device or default_device()
+    if isinstance(x, torch.Tensor):
+        if x.dtype == torch.uint32:
+            x = x.view(torch.int32)
+        elif x.dtype != torch.int32:
+            x = x.to(torch.int64).to(torch.int32)
+        was_host = x.device.type != "cuda"
+        x = x.to(device, non_blocking=True).contiguous()
+        return x, was_host
+    a = np.ascontiguousarray(np.asarray(x).astype(np.uint32, copy=False))
+    return torch.from_numpy(a.view(np.int32)).to(device), True
+
+
+def to_host(t) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint32)
+
+
+def like_input(t, was_host):
+    return to_host(t) if was_host else t
+
+
+class DeviceContext:
+    """Constant tables for degree n over `primes` (chain first, then specials)."""
+
+    def __init__(self, n: int, primes, n_chain: int | None = None, n_special: int = 0,
+                 device=None):
+        self.lib = _lib.load()
+        self.device = torch.device(device) if device is not None else default_device()
+        self.n = int(n)
+        self.log_n = self.n.bit_length() - 1
+        self.primes = tuple(int(q) for q in primes)
+        self.n_chain = len(self.primes) - n_special if n_chain is None else int(n_chain)
+        self.n_special = int(n_special)
+        if self.n_chain + self.n_special != len(self.primes):
+            raise ParameterError("n_chain + n_special must equal the prime count")
+        self.index = {q: i for i, q in enumerate(self.primes)}
+        psis = [find_negacyclic_root(q, self.n) for q in self.primes]
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.tfhe_ctx_create(
+                self.device.index or 0, self.log_n, _lib.u32_array(self.primes),
+                _lib.u32_array(psis), self.n_chain, self.n_special, ctypes.byref(handle)),
+                "tfhe_ctx_create")
+        self.handle = handle
+        n1, n2 = ctypes.c_int(), ctypes.c_int()
+        self.lib.tfhe_ctx_plan(self.handle, ctypes.byref(n1), ctypes.byref(n2))
+        self.plan = (n1.value, n2.value)
+        self._ws = None
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and getattr(self, "lib", None) is not None:
+            try:
+                self.lib.tfhe_ctx_destroy(h)
+            except Exception:
+                pass
+
+    @classmethod
+    def get(cls, n, primes, n_chain=None, n_special=0, device=None) -> "DeviceContext":
+        dev = torch.device(device) if device is not None else default_device()
+        key = (str(dev), int(n), tuple(int(q) for q in primes), n_chain, n_special)
+        with _LOCK:
+            ctx = _CTX_CACHE.get(key)
+            if ctx is None:
+                ctx = cls(n, primes, n_chain, n_special, dev)
+                _CTX_CACHE[key] = ctx
+        return ctx
+
+    @classmethod
+    def get_for(cls, n, primes, device=None) -> "DeviceContext":
+        """Any cached context of degree n on `device` whose primes cover
+        `primes` (e.g. the CkksContext's extended basis), else a new one."""
+        dev = torch.device(device) if device is not None else default_device()
+        need = set(int(q) for q in primes)
+        with _LOCK:
+            for key, ctx in _CTX_CACHE.items():
+                if key[0] == str(dev) and key[1] == int(n) and need <= set(ctx.primes):
+                    return ctx
+        return cls.get(n, tuple(sorted(need, reverse=True)), device=dev)
+
+    # -- helpers --------------------------------------------------------------
+    def prime_ids(self, primes):
+        try:
+            return [self.index[int(q)] for q in primes]
+        except KeyError as e:
+            raise ParameterError(f"no twiddles prepared for prime {e.args[0]}") from None
+
+    def workspace(self, nbytes: int) -> torch.Tensor:
+        """Cached byte workspace (grown on demand, reused across calls)."""
+        nbytes = max(int(nbytes), 256)
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = None
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def empty(self, *shape):
+        return torch.empty(shape, dtype=torch.int32, device=self.device)
+
+    # -- operators ------------------------------------------------------------
+    def ntt(self, x, limb_primes, inverse=False, in_rows=None, out_rows=None, out=None,
+            out_rows_total=None):
+        """x: (rows, batch, n) int32 CUDA tensor.  Output row l = transform of
+        x[in_rows[l]] mod limb_primes[l] (prime values)."""
+        L = len(limb_primes)
+        batch = x.shape[1]
+        if out is None:
+            out = self.empty(out_rows_total or L, batch, self.n)
+        ws_bytes = self.lib.tfhe_ntt_workspace_bytes(self.handle, L, batch)
+        ws = self.workspace(ws_bytes)
+        _lib.check(self.lib.tfhe_ntt(
+            self.handle, _ptr(x), _ptr(out), _lib.i32_array(self.prime_ids(limb_primes)),
+            _lib.i32_array(in_rows) if in_rows is not None else None,
+            _lib.i32_array(out_rows) if out_rows is not None else None,
+            L, batch, int(bool(inverse)), _ptr(ws), ws.numel(), _stream(self.device)),
+            "tfhe_ntt")
+        return out
+
+    def eltwise(self, op, a, b, row_primes, scalars=None, out=None):
+        rows = a.shape[0]
+        per_row = a.numel() // max(rows, 1)
+        if out is None:
+            out = torch.empty_like(a)
+        _lib.check(self.lib.tfhe_eltwise(
+            self.handle, op, _ptr(a), _ptr(b), _ptr(out),
+            _lib.i32_array(self.prime_ids(row_primes)), rows, per_row,
+            _lib.u32_array(scalars) if scalars is not None else None, _stream(self.device)),
+            "tfhe_eltwise")
+        return out
+
+    def automorphism(self, x, t, ntt_domain, row_primes, out=None):
+        rows, batch = x.shape[0], x.shape[1]
+        if out is None:
+            out = torch.empty_like(x)
+        _lib.check(self.lib.tfhe_automorphism(
+            self.handle, _ptr(x), _ptr(out), int(t), int(bool(ntt_domain)),
+            _lib.i32_array(self.prime_ids(row_primes)), rows, batch, _stream(self.device)),
+            "tfhe_automorphism")
+        return out
+
+    def bconv(self, x, src, dst, out=None):
+        batch = x.shape[1]
+        if out is None:
+            out = self.empty(len(dst), batch, self.n)
+        _lib.check(self.lib.tfhe_bconv(
+            self.handle, _ptr(x), _ptr(out), _lib.i32_array(self.prime_ids(src)), len(src),
+            _lib.i32_array(self.prime_ids(dst)), len(dst), batch, _stream(self.device)),
+            "tfhe_bconv")
+        return out
+
+    def ckks_workspace(self, level, batch):
+        return self.workspace(self.lib.tfhe_ckks_workspace_bytes(self.handle, level, batch))
+
+    def keyswitch(self, d, level, key, dnum, add=None, out=None):
+        batch = d.shape[1]
+        if out is None:
+            out = self.empty(2, level + 1, batch, self.n)
+        ws = self.ckks_workspace(level, batch)
+        _lib.check(self.lib.tfhe_keyswitch(
+            self.handle, _ptr(d), level, batch, _ptr(key), dnum, _ptr(out), _ptr(add),
+            _ptr(ws), ws.numel(), _stream(self.device)), "tfhe_keyswitch")
+        return out
+
+    def hmult(self, ct0, ct1, level, rlk, dnum, out=None):
+        batch = ct0.shape[2]
+        if out is None:
+            out = self.empty(2, level + 1, batch, self.n)
+        ws = self.ckks_workspace(level, batch)
+        _lib.check(self.lib.tfhe_hmult(
+            self.handle, _ptr(ct0), _ptr(ct1), level, batch, _ptr(rlk), dnum, _ptr(out),
+            _ptr(ws), ws.numel(), _stream(self.device)), "tfhe_hmult")
+        return out
+
+    def rescale(self, ct, level, out=None):
+        batch = ct.shape[2]
+        if out is None:
+            out = self.empty(2, level, batch, self.n)
+        ws = self.ckks_workspace(level, batch)
+        _lib.check(self.lib.tfhe_rescale(
+            self.handle, _ptr(ct), level, batch, _ptr(out), _ptr(ws), ws.numel(),
+            _stream(self.device)), "tfhe_rescale")
+        return out
+
+    def hrotate(self, ct, level, galois_t, key, dnum, out=None):
+        batch = ct.shape[2]
+        if out is None:
+            out = self.empty(2, level + 1, batch, self.n)
+        ws = self.ckks_workspace(level, batch)
+        _lib.check(self.lib.tfhe_hrotate(
+            self.handle, _ptr(ct), level, batch, int(galois_t), _ptr(key), dnum, _ptr(out),
+            _ptr(ws), ws.numel(), _stream(self.device)), "tfhe_hrotate")
+        return out
