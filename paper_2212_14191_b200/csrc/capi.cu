@@ -346,7 +346,10 @@ void tfhe_ctx_destroy(TfheCtx* h) {
   Ctx& c = h->c;
   cudaFree(c.d_pc);
   for (int i = 0; i < 2; ++i) {
-    for (int s = 0; s < 2; ++s) cudaFree(c.d_tw[i][s]);
+    for (int s = 0; s < 2; ++s) {
+      cudaFree(c.d_tw[i][s]);
+      cudaFree(c.d_twa[i][s]);
+    }
     cudaFree(c.d_w2[i]);
     cudaFree(c.d_w2s[i]);
   }

@@ -29,6 +29,7 @@
 // one thread bulk-copies (TMA engine) the pre-split twiddle tiles, warp 4
 // owns TMEM and issues the MMAs; a 2-stage mbarrier ring overlaps loads with
 // MMAs.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -312,7 +313,9 @@ int build_ntt_tables(Ctx& c) {
           k.n_inv = n_inv;
           k.n_inv_shoup = shoup_h(n_inv, q);
           k.mu = (uint64_t)(~0ull / q);  // floor((2^64-1)/q) == floor(2^64/q) for non-power-of-2 q
-          k.pad = 0;
+          k.r[0] = powmod_h(2, 32, q);
+          k.r[1] = powmod_h(2, 40, q);
+          k.r[2] = powmod_h(2, 48, q);
         }
         // T[c][k]: value multiplying data index k for output column c
         for (int cc = 0; cc < ntw; ++cc)
@@ -376,6 +379,13 @@ int build_ntt_tables(Ctx& c) {
     set_error("prime constant upload failed");
     return 3;
   }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+  if (c.sms <= 0) c.sms = 148;
+  // twiddle-resident tensor-core path for n1, n2 in {128, 256}
+  c.use_ts = c.n1 >= 128 && c.n2 <= 256;
+  if (c.use_ts) return build_ts_tables(c);
   return 0;
 }
 
@@ -386,6 +396,7 @@ int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& m
     set_error("ntt workspace too small");
     return 2;
   }
+  if (c.use_ts) return launch_ntt_ts(c, in, out, map, batch, inverse, epi, ws, st);
   StageArgs a;
   memset(&a, 0, sizeof(a));
   a.pc = c.d_pc;

@@ -1,0 +1,436 @@
+// Twiddle-resident tensor-core NTT stages (n1, n2 in {128, 256}; N = 2^14..2^16).
+//
+// Same math as ntt_tc.cu (TensorFHE's byte-sliced GEMM formulation, ref
+// ntt.py:212-340), re-tiled so the CONSTANT operand never streams:
+//
+//   D[r][col] = sum_k T[r][k] * X[k][col]        (mod q)
+//     stage 1: r = k1, k = i1, col = (b, i2), T = W1, X = A_b      -> P = D .* W2
+//     stage 2: r = k2, k = i2, col = (b, k1), T = W3^T, X = P_b^T  -> out[k2*n1 + k1]
+//
+// * A operand (twiddle byte planes T_i, i = 0..3) lives in TMEM for the whole
+//   lifetime of a (limb, 128-row half) work group: tcgen05.mma ... [a_tmem]
+//   ("TS" form).  Nothing twiddle-related is re-read per tile.
+// * B operand (data) streams through a 6-stage smem ring: 16 data columns per
+//   chunk, split into byte planes X_j by 4 producer warps and laid out as
+//   B' = [X_0 | X_1 | X_2 | X_3] along N (N = 64).
+// * Byte weights: T X = sum_{s=0..6} 2^(8s) C_s with C_s = sum_{i+j=s} T_i X_j.
+//   One MMA (A = T_i, B = B') writes D[:, 16 j + c] = T_i X_j; placing its
+//   output at column 16 i makes block 16 (i+j) accumulate exactly C_{i+j}
+//   ("shifted window"), so 4 MMAs per K-step produce all 7 accumulators
+//   (7 x 16 TMEM columns, double-buffered).  C_s < 4 * 256 * 255^2 < 2^26.
+// * Epilogue warps fold sum C_s 2^(8s) (2^(8s) mod q for s >= 4) in 64 bits,
+//   Barrett-reduce, apply W2 (stage 1) or the fused output epilogue
+//   (stage 2) and store 64 contiguous bytes per thread.
+//
+// Roles: warps 0-3 data producers, warps 4-7 epilogue (+ twiddle -> TMEM
+// loads), warp 8 TMEM allocation + single-thread MMA issue.  Persistent grid
+// (one CTA per SM); with two 128-row halves the CTAs run in pairs over the
+// same data range so the second read of each data chunk hits L2.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "tfhe_internal.h"
+
+namespace tfhe {
+
+namespace {
+
+constexpr int kNC = 16;                  // data columns per chunk
+constexpr int kRing = 6;                 // smem ring depth (chunks)
+constexpr int kThreadsTS = 288;          // 4 producer + 4 epilogue + 1 MMA warp
+constexpr uint32_t kAccCol0 = 256, kAccCol1 = 384;
+
+struct TsArgs {
+  const uint32_t* in;
+  uint32_t* out;
+  const uint32_t* twa;  // [prime][half][128][4][K/4] words
+  const uint32_t* w2;
+  const uint32_t* w2s;
+  const PrimeConst* pc;
+  int n, n1, n2, batch;
+  int R;      // data columns per member (stage 1: n2, stage 2: n1)
+  int H;      // 128-row twiddle halves
+  int C;      // chunks per limb
+  int n_limbs;
+  LimbMap map;
+  EpiArgs epi;
+};
+
+template <int K>
+__host__ __device__ constexpr int ring_stage_bytes() { return (K / 32) * 2048; }
+
+TFHE_DEV void planes4(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, uint32_t (&w)[4]) {
+  uint32_t lo01 = __byte_perm(v0, v1, 0x5140), hi01 = __byte_perm(v0, v1, 0x7362);
+  uint32_t lo23 = __byte_perm(v2, v3, 0x5140), hi23 = __byte_perm(v2, v3, 0x7362);
+  w[0] = __byte_perm(lo01, lo23, 0x5410);
+  w[1] = __byte_perm(lo01, lo23, 0x7632);
+  w[2] = __byte_perm(hi01, hi23, 0x5410);
+  w[3] = __byte_perm(hi01, hi23, 0x7632);
+}
+
+// byte offset of (B' row, k) inside one chunk stage: per K-step kc a 64-row x
+// 32-byte K-major SWIZZLE_NONE tile (LBO = 1024, SBO = 128)
+TFHE_DEV uint32_t ring_off(int row, int k) {
+  const int kc = k >> 5, kk = k & 31;
+  return (uint32_t)(kc * 2048 + (kk >> 4) * 1024 + (row >> 3) * 128 + (row & 7) * 16 + (kk & 15));
+}
+
+template <int STAGE, int K>
+__global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_constant__ TsArgs a) {
+  constexpr int kStageBytes = ring_stage_bytes<K>();
+  constexpr int KC = K / 32;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(smem + kRing * kStageBytes);
+  uint64_t* b_empty = b_full + kRing;
+  uint64_t* acc_full = b_empty + kRing;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* tw_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tw_full + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // work split: units u = limb * C + chunk over this CTA's half
+  int h, grp, groups;
+  if (a.H == 2) {
+    h = blockIdx.x & 1;
+    grp = blockIdx.x >> 1;
+    groups = gridDim.x >> 1;
+  } else {
+    h = 0;
+    grp = blockIdx.x;
+    groups = gridDim.x;
+  }
+  const long long U = (long long)a.n_limbs * a.C;
+  const long long u0 = U * grp / groups, u1 = U * (grp + 1) / groups;
+
+  if (tid == 0) {
+    for (int s = 0; s < kRing; ++s) {
+      mbar_init(&b_full[s], 128);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 128);
+    }
+    mbar_init(tw_full, 128);
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // ---------------------------------------------------------------- producers
+    long long it = 0;
+    for (long long u = u0; u < u1; ++u, ++it) {
+      const int s = (int)(it % kRing);
+      if (it >= kRing) mbar_wait(&b_empty[s], (uint32_t)(((it / kRing) & 1) ^ 1));
+      const int limb = (int)(u / a.C);
+      const int col0 = (int)(u % a.C) * kNC;
+      const int b = col0 / a.R, x0 = col0 % a.R;
+      uint8_t* st = smem + s * kStageBytes;
+      if (STAGE == 1) {
+        // X_b[k][x0 + c] = src[k * n2 + c]
+        const uint32_t* src = a.in + ((size_t)a.map.in_row[limb] * a.batch + b) * a.n + x0;
+        const int c4 = (tid & 3) * 4, kq = tid >> 2;
+#pragma unroll
+        for (int m = 0; m < K / 128; ++m) {
+          const int k = 4 * kq + 128 * m;
+          uint4 v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            v[e] = __ldg(reinterpret_cast<const uint4*>(src + (size_t)(k + e) * a.n2 + c4));
+          const uint32_t col[4][4] = {{v[0].x, v[1].x, v[2].x, v[3].x},
+                                      {v[0].y, v[1].y, v[2].y, v[3].y},
+                                      {v[0].z, v[1].z, v[2].z, v[3].z},
+                                      {v[0].w, v[1].w, v[2].w, v[3].w}};
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t w[4];
+            planes4(col[cc][0], col[cc][1], col[cc][2], col[cc][3], w);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint32_t*>(st + ring_off(j * 16 + c4 + cc, k)) = w[j];
+          }
+        }
+      } else {
+        // P_b[x0 + r][k] = src[r * n2 + k]
+        const uint32_t* src = a.in + ((size_t)limb * a.batch + b) * a.n + (size_t)x0 * a.n2;
+        const int r = tid & 15, kq = tid >> 4;
+#pragma unroll
+        for (int m = 0; m < K / 32; ++m) {
+          const int k = 4 * kq + 32 * m;
+          uint4 v = __ldg(reinterpret_cast<const uint4*>(src + (size_t)r * a.n2 + k));
+          uint32_t w[4];
+          planes4(v.x, v.y, v.z, v.w, w);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint32_t*>(st + ring_off(j * 16 + r, k)) = w[j];
+        }
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&b_full[s]);
+    }
+  } else if (warp < 8) {
+    // ---------------------------------------------------------------- epilogue
+    const int wq = warp & 3;
+    const int m = wq * 32 + lane;          // TMEM lane = twiddle row within the half
+    const int r_tw = h * 128 + m;          // global twiddle row (k1 or k2)
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    int prev = -1, gi = -1;
+    long long it = 0;
+    for (long long u = u0; u < u1; ++u, ++it) {
+      const int limb = (int)(u / a.C);
+      const int prime = a.map.prime[limb];
+      if (limb != prev) {
+        // load this (limb, half)'s twiddle planes into TMEM columns [0, K)
+        ++gi;
+        prev = limb;
+        const uint32_t* src = a.twa + (((size_t)prime * a.H + h) * 128 + m) * K;
+#pragma unroll 1
+        for (int w0 = 0; w0 < K; w0 += 16) {
+          uint32_t r[16];
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint4 v = __ldg(reinterpret_cast<const uint4*>(src + w0 + 4 * q4));
+            r[4 * q4] = v.x; r[4 * q4 + 1] = v.y; r[4 * q4 + 2] = v.z; r[4 * q4 + 3] = v.w;
+          }
+          tmem_st16(tmem + lane_off + w0, r);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(tw_full);
+      }
+      const int ab = (int)(it & 1);
+      mbar_wait(&acc_full[ab], (uint32_t)((it >> 1) & 1));
+      tc_fence_after();
+      uint32_t acc[7][16];
+      const uint32_t abase = tmem + lane_off + (ab ? kAccCol1 : kAccCol0);
+#pragma unroll
+      for (int s = 0; s < 7; ++s) tmem_ld16(abase + 16 * s, acc[s]);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&acc_empty[ab]);
+
+      const PrimeConst pc = a.pc[prime];
+      const int col0 = (int)(u % a.C) * kNC;
+      const int b = col0 / a.R, x0 = col0 % a.R;
+      uint32_t y[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        uint64_t v = (uint64_t)acc[0][e] + ((uint64_t)acc[1][e] << 8) +
+                     ((uint64_t)acc[2][e] << 16) + ((uint64_t)acc[3][e] << 24) +
+                     (uint64_t)acc[4][e] * pc.r[0] + (uint64_t)acc[5][e] * pc.r[1] +
+                     (uint64_t)acc[6][e] * pc.r[2];
+        y[e] = reduce64(v, pc.q, pc.mu);
+      }
+      if (STAGE == 1) {
+        const size_t widx = (size_t)prime * a.n + (size_t)r_tw * a.n2 + x0;
+        uint32_t* dst = a.out + ((size_t)limb * a.batch + b) * a.n + (size_t)r_tw * a.n2 + x0;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          uint4 w = __ldg(reinterpret_cast<const uint4*>(a.w2 + widx + 4 * q4));
+          uint4 ws = __ldg(reinterpret_cast<const uint4*>(a.w2s + widx + 4 * q4));
+          uint4 o;
+          o.x = mul_shoup(y[4 * q4 + 0], w.x, ws.x, pc.q);
+          o.y = mul_shoup(y[4 * q4 + 1], w.y, ws.y, pc.q);
+          o.z = mul_shoup(y[4 * q4 + 2], w.z, ws.z, pc.q);
+          o.w = mul_shoup(y[4 * q4 + 3], w.w, ws.w, pc.q);
+          *reinterpret_cast<uint4*>(dst + 4 * q4) = o;
+        }
+      } else {
+        const size_t pos = (size_t)r_tw * a.n1 + x0;  // out[n1*k2 + k1], k1 = x0 + e
+        uint32_t* dst = a.out + ((size_t)a.map.out_row[limb] * a.batch + b) * a.n + pos;
+        if (a.epi.mode == EPI_SUB_SCALE) {
+          const uint32_t* xs = a.epi.x + ((size_t)a.epi.x_row[limb] * a.batch + b) * a.n + pos;
+          const uint32_t s = a.epi.s[limb], sp = a.epi.s_shoup[limb];
+          const int br = a.epi.base_row[limb];
+          const uint32_t* bs =
+              br >= 0 ? a.epi.base + ((size_t)br * a.batch + b) * a.n + pos : nullptr;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            uint32_t t = mul_shoup(sub_mod(__ldg(xs + e), y[e], pc.q), s, sp, pc.q);
+            y[e] = bs ? add_mod(__ldg(bs + e), t, pc.q) : t;
+          }
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          *reinterpret_cast<uint4*>(dst + 4 * q4) =
+              make_uint4(y[4 * q4], y[4 * q4 + 1], y[4 * q4 + 2], y[4 * q4 + 3]);
+      }
+    }
+  } else if (lane == 0) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t id64 = idesc_i8(128, 64), id48 = idesc_i8(128, 48),
+                       id16 = idesc_i8(128, 16);
+    int prev = -1, gi = -1;
+    long long it = 0;
+    for (long long u = u0; u < u1; ++u, ++it) {
+      const int limb = (int)(u / a.C);
+      if (limb != prev) {
+        ++gi;
+        prev = limb;
+        mbar_wait(tw_full, (uint32_t)(gi & 1));
+      }
+      const int s = (int)(it % kRing);
+      mbar_wait(&b_full[s], (uint32_t)((it / kRing) & 1));
+      const int ab = (int)(it & 1);
+      if (it >= 2) mbar_wait(&acc_empty[ab], (uint32_t)(((it >> 1) & 1) ^ 1));
+      tc_fence_after();
+      const uint32_t d = tmem + (ab ? kAccCol1 : kAccCol0);
+      const uint32_t sb = smem_u32(smem + s * kStageBytes);
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        const uint32_t bt = sb + kc * 2048;
+        const uint64_t bd = smem_desc_kmajor(bt, 1024, 128);
+        const uint32_t a0 = tmem + 0 * (K / 4) + kc * 8, a1 = tmem + 1 * (K / 4) + kc * 8;
+        const uint32_t a2 = tmem + 2 * (K / 4) + kc * 8, a3 = tmem + 3 * (K / 4) + kc * 8;
+        if (kc == 0) {
+          mma_i8_ts(d + 48, a3, bd, id64, 0);   // blocks 3..6 = T_3 X_0..3 (init)
+          mma_i8_ts(d + 0, a0, bd, id48, 0);    // blocks 0..2 = T_0 X_0..2 (init)
+          mma_i8_ts(d + 48, a0, smem_desc_kmajor(bt + 768, 1024, 128), id16, 1);  // + T_0 X_3
+          mma_i8_ts(d + 16, a1, bd, id64, 1);
+          mma_i8_ts(d + 32, a2, bd, id64, 1);
+        } else {
+          mma_i8_ts(d + 0, a0, bd, id64, 1);
+          mma_i8_ts(d + 16, a1, bd, id64, 1);
+          mma_i8_ts(d + 32, a2, bd, id64, 1);
+          mma_i8_ts(d + 48, a3, bd, id64, 1);
+        }
+      }
+      mma_commit(&b_empty[s]);
+      mma_commit(&acc_full[ab]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int STAGE, int K>
+int launch_ts(const Ctx& c, TsArgs& a, cudaStream_t st) {
+  const int smem = kRing * ring_stage_bytes<K>() + (2 * kRing + 5) * 8 + 16;
+  auto kern = ntt_ts_kernel<STAGE, K>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const long long U = (long long)a.n_limbs * a.C;
+  int grid;
+  if (a.H == 2) grid = 2 * (int)std::min<long long>(c.sms / 2, U);
+  else grid = (int)std::min<long long>(c.sms, U);
+  if (grid <= 0) return 0;
+  kern<<<grid, kThreadsTS, smem, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("ntt ts launch: ") + cudaGetErrorString(e));
+    return 3;
+  }
+  return 0;
+}
+
+template <int STAGE>
+int launch_ts_k(const Ctx& c, int K, TsArgs& a, cudaStream_t st) {
+  if (K == 256) return launch_ts<STAGE, 256>(c, a, st);
+  if (K == 128) return launch_ts<STAGE, 128>(c, a, st);
+  set_error("ts kernel: unsupported contraction length");
+  return 2;
+}
+
+uint32_t mulmod_h(uint64_t x, uint64_t y, uint32_t q) { return (uint32_t)(x * y % q); }
+uint32_t powmod_h(uint64_t b, uint64_t e, uint32_t q) {
+  uint64_t r = 1, x = b % q;
+  while (e) {
+    if (e & 1) r = r * x % q;
+    x = x * x % q;
+    e >>= 1;
+  }
+  return (uint32_t)r;
+}
+
+}  // namespace
+
+int build_ts_tables(Ctx& c) {
+  const int n = c.n, n1 = c.n1, n2 = c.n2, np = c.n_primes;
+  const uint64_t two_n = 2ull * n;
+  std::vector<uint32_t> pw(two_n);
+  for (int inv = 0; inv < 2; ++inv)
+    for (int s = 0; s < 2; ++s) {
+      const int ntw = s == 0 ? n1 : n2, K = ntw, H = ntw / 128;
+      std::vector<uint32_t> tw((size_t)np * ntw * K);  // K words per row (4 planes x K/4)
+      for (int p = 0; p < np; ++p) {
+        const uint32_t q = c.primes[p];
+        const uint32_t root = inv ? powmod_h(c.psis[p], q - 2, q) : c.psis[p];
+        pw[0] = 1;
+        for (uint64_t e = 1; e < two_n; ++e) pw[e] = mulmod_h(pw[e - 1], root, q);
+        const uint32_t n_inv = powmod_h(n, q - 2, q);
+        for (int r = 0; r < ntw; ++r) {
+          const int hh = r / 128, m = r % 128;
+          uint32_t* row = tw.data() + (((size_t)p * H + hh) * 128 + m) * K;
+          for (int kq = 0; kq < K / 4; ++kq) {
+            uint32_t words[4] = {0, 0, 0, 0};
+            for (int e = 0; e < 4; ++e) {
+              const uint64_t k = 4 * kq + e;
+              uint64_t ex;
+              if (s == 0)  // W1[k1 = r][i1 = k]
+                ex = inv ? (uint64_t)n2 * (2ull * r * k) : (uint64_t)n2 * (2ull * r * k + k);
+              else  // W3[i2 = k][k2 = r]
+                ex = inv ? (uint64_t)n1 * (2ull * k * r + r) : (uint64_t)n1 * (2ull * k * r);
+              uint32_t v = pw[ex % two_n];
+              if (s == 1 && inv) v = mulmod_h(v, n_inv, q);
+              for (int i = 0; i < 4; ++i) words[i] |= ((v >> (8 * i)) & 0xFFu) << (8 * e);
+            }
+            for (int i = 0; i < 4; ++i) row[i * (K / 4) + kq] = words[i];
+          }
+        }
+      }
+      const size_t bytes = tw.size() * 4;
+      if (cudaMalloc(&c.d_twa[inv][s], bytes) != cudaSuccess ||
+          cudaMemcpy(c.d_twa[inv][s], tw.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+        set_error("ts twiddle upload failed");
+        return 3;
+      }
+    }
+  return 0;
+}
+
+int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& map, int batch,
+                  int inverse, const EpiArgs* epi, void* ws, cudaStream_t st) {
+  TsArgs a;
+  memset(&a, 0, sizeof(a));
+  a.pc = c.d_pc;
+  a.n = c.n;
+  a.n1 = c.n1;
+  a.n2 = c.n2;
+  a.batch = batch;
+  a.n_limbs = map.n;
+  a.map = map;
+  if (epi) a.epi = *epi;
+  else a.epi.mode = EPI_STORE;
+  uint32_t* P = static_cast<uint32_t*>(ws);
+  // stage 1: rows k1 (n1 twiddle rows), data columns (b, i2)
+  a.in = in;
+  a.out = P;
+  a.twa = c.d_twa[inverse][0];
+  a.w2 = c.d_w2[inverse];
+  a.w2s = c.d_w2s[inverse];
+  a.R = c.n2;
+  a.H = c.n1 / 128;
+  a.C = batch * c.n2 / kNC;
+  int rc = launch_ts_k<1>(c, c.n1, a, st);
+  if (rc) return rc;
+  // stage 2: rows k2 (n2 twiddle rows), data columns (b, k1)
+  a.in = P;
+  a.out = out;
+  a.twa = c.d_twa[inverse][1];
+  a.R = c.n1;
+  a.H = c.n2 / 128;
+  a.C = batch * c.n1 / kNC;
+  return launch_ts_k<2>(c, c.n2, a, st);
+}
+
+}  // namespace tfhe

@@ -17,7 +17,7 @@ struct PrimeConst {
   uint32_t n_inv;       // n^-1 mod q
   uint64_t mu;          // floor(2^64 / q)
   uint32_t n_inv_shoup;
-  uint32_t pad;
+  uint32_t r[3];        // 2^32, 2^40, 2^48 mod q (byte weights 4..6 of the TS kernel)
 };
 
 // Per-launch limb map: output row l uses prime `prime[l]`, reads input row
@@ -57,8 +57,18 @@ struct Ctx {
   int kpad[2] = {0, 0}, npad[2] = {0, 0}, bn[2] = {0, 0};
   uint32_t* d_w2[2] = {nullptr, nullptr};   // [inverse] (prime, n1*n2) hadamard twiddles
   uint32_t* d_w2s[2] = {nullptr, nullptr};  // Shoup companions
+  // twiddle-resident (TS) kernel: per [inverse][stage] words
+  // [prime][half][row 128][plane 4][K/4], used when n1 >= 128
+  uint32_t* d_twa[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  bool use_ts = false;
+  int sms = 148;
   std::vector<PrimeConst> h_pc;
 };
+
+// twiddle-resident tensor-core stages (ntt_ts.cu)
+int build_ts_tables(Ctx& c);
+int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& map, int batch,
+                  int inverse, const EpiArgs* epi, void* ws, cudaStream_t st);
 
 // kernels (ntt_tc.cu)
 size_t ntt_workspace_bytes(const Ctx& c, int n_limbs, int batch);
