@@ -316,6 +316,11 @@ int build_ntt_tables(Ctx& c) {
           k.r[0] = powmod_h(2, 32, q);
           k.r[1] = powmod_h(2, 40, q);
           k.r[2] = powmod_h(2, 48, q);
+          k.w3 = powmod_h(2, 24, q);
+          uint32_t inv = 1;  // Newton iteration for q^-1 mod 2^32
+          for (int t = 0; t < 5; ++t) inv *= 2u - q * inv;
+          k.qneg_inv = 0u - inv;
+          k.pad[0] = k.pad[1] = 0;
         }
         // T[c][k]: value multiplying data index k for output column c
         for (int cc = 0; cc < ntw; ++cc)

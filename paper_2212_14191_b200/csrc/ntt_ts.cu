@@ -77,12 +77,61 @@ TFHE_DEV uint32_t ring_off(int row, int k) {
   return (uint32_t)(kc * 2048 + (kk >> 4) * 1024 + (row >> 3) * 128 + (row & 7) * 16 + (kk & 15));
 }
 
+// iteration state shared by the three roles: every role walks the same unit
+// sequence (limb, chunk) and the same ring / accumulator phases
+struct UnitIter {
+  int limb, c, b, x0;
+  int s;          // ring slot
+  uint32_t rph;   // ring phase parity of slot s
+  int ab;         // accumulator buffer
+  uint32_t aph;   // accumulator phase parity
+  TFHE_DEV void init(long long u0, int C, int logR, int R) {
+    limb = (int)(u0 / C);
+    c = (int)(u0 % C);
+    set_col(logR, R);
+    s = 0; rph = 0; ab = 0; aph = 0;
+  }
+  TFHE_DEV void set_col(int logR, int R) {
+    const int col0 = c * kNC;
+    b = col0 >> logR;
+    x0 = col0 & (R - 1);
+  }
+  TFHE_DEV void next(int C, int logR, int R) {
+    if (++c == C) { c = 0; ++limb; }
+    set_col(logR, R);
+    if (++s == kRing) { s = 0; rph ^= 1; }
+    ab ^= 1;
+    if (ab == 0) aph ^= 1;
+  }
+};
+
+// MN-major variant (stage 1): per K-step a tile of 4 planes x 4 K-groups of
+// 128-byte core matrices (8 k rows x 16 column bytes); LBO (K) = 128,
+// SBO (N, = plane) = 512.  (plane j, column c, k) -> byte offset
+TFHE_DEV uint32_t ring_off_mn(int j, int c, int k) {
+  const int kc = k >> 5, kk = k & 31;
+  return (uint32_t)(kc * 2048 + j * 512 + (kk >> 3) * 128 + (kk & 7) * 16 + c);
+}
+
+TFHE_DEV void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+TFHE_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+TFHE_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+TFHE_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+constexpr int kStgRow = 80;                       // padded staging row (bank-conflict free)
+constexpr int kStgBytes = 128 * kStgRow;          // one staging buffer
+
 template <int STAGE, int K>
 __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_constant__ TsArgs a) {
   constexpr int kStageBytes = ring_stage_bytes<K>();
   constexpr int KC = K / 32;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* b_full = reinterpret_cast<uint64_t*>(smem + kRing * kStageBytes);
+  uint8_t* stg = smem + kRing * kStageBytes;  // 2 epilogue staging buffers
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(stg + 2 * kStgBytes);
   uint64_t* b_empty = b_full + kRing;
   uint64_t* acc_full = b_empty + kRing;
   uint64_t* acc_empty = acc_full + 2;
@@ -102,7 +151,9 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     groups = gridDim.x;
   }
   const long long U = (long long)a.n_limbs * a.C;
-  const long long u0 = U * grp / groups, u1 = U * (grp + 1) / groups;
+  const long long u0 = U * grp / groups;
+  const int cnt = (int)(U * (grp + 1) / groups - u0);
+  const int C = a.C, R = a.R, logR = 31 - __clz(a.R);
 
   if (tid == 0) {
     for (int s = 0; s < kRing; ++s) {
@@ -121,58 +172,84 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  UnitIter w;
+  w.init(u0, C, logR, R);
 
   if (warp < 4) {
     // ---------------------------------------------------------------- producers
-    long long it = 0;
-    for (long long u = u0; u < u1; ++u, ++it) {
-      const int s = (int)(it % kRing);
-      if (it >= kRing) mbar_wait(&b_empty[s], (uint32_t)(((it / kRing) & 1) ^ 1));
-      const int limb = (int)(u / a.C);
-      const int col0 = (int)(u % a.C) * kNC;
-      const int b = col0 / a.R, x0 = col0 % a.R;
-      uint8_t* st = smem + s * kStageBytes;
+    // Stage 1 (X_b[k][x0 + c], columns contiguous): B' is stored MN-major --
+    // each thread loads 16 B (4 columns of one k row) and writes one 4-byte
+    // word per byte plane; a warp covers 8 k rows x 64 B = one conflict-free
+    // 128-byte span per plane.
+    // Stage 2 (P_b[x0 + r][k], k contiguous): B' is stored K-major -- each
+    // thread loads 16 consecutive k of one row and writes one 16-byte vector
+    // per plane; a quarter warp covers 8 rows = 8 distinct 16-byte slots.
+    // Software-pipelined: the next chunk's global loads are issued before the
+    // current chunk is split and stored, so load latency overlaps the ring.
+    constexpr int kVals = K / 8;   // u32 values per thread per chunk
+    const int c4 = (tid & 3) * 4, krow0 = tid >> 2;   // stage 1 mapping
+    const int col = tid & 15, kb0 = tid >> 4;         // stage 2 mapping
+    auto load_chunk = [&](const UnitIter& it, uint32_t (&v)[kVals]) {
       if (STAGE == 1) {
-        // X_b[k][x0 + c] = src[k * n2 + c]
-        const uint32_t* src = a.in + ((size_t)a.map.in_row[limb] * a.batch + b) * a.n + x0;
-        const int c4 = (tid & 3) * 4, kq = tid >> 2;
-#pragma unroll
-        for (int m = 0; m < K / 128; ++m) {
-          const int k = 4 * kq + 128 * m;
-          uint4 v[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            v[e] = __ldg(reinterpret_cast<const uint4*>(src + (size_t)(k + e) * a.n2 + c4));
-          const uint32_t col[4][4] = {{v[0].x, v[1].x, v[2].x, v[3].x},
-                                      {v[0].y, v[1].y, v[2].y, v[3].y},
-                                      {v[0].z, v[1].z, v[2].z, v[3].z},
-                                      {v[0].w, v[1].w, v[2].w, v[3].w}};
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            uint32_t w[4];
-            planes4(col[cc][0], col[cc][1], col[cc][2], col[cc][3], w);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              *reinterpret_cast<uint32_t*>(st + ring_off(j * 16 + c4 + cc, k)) = w[j];
-          }
-        }
-      } else {
-        // P_b[x0 + r][k] = src[r * n2 + k]
-        const uint32_t* src = a.in + ((size_t)limb * a.batch + b) * a.n + (size_t)x0 * a.n2;
-        const int r = tid & 15, kq = tid >> 4;
+        const uint32_t* src =
+            a.in + ((size_t)a.map.in_row[it.limb] * a.batch + it.b) * a.n + it.x0 + c4;
 #pragma unroll
         for (int m = 0; m < K / 32; ++m) {
-          const int k = 4 * kq + 32 * m;
-          uint4 v = __ldg(reinterpret_cast<const uint4*>(src + (size_t)r * a.n2 + k));
-          uint32_t w[4];
-          planes4(v.x, v.y, v.z, v.w, w);
+          uint4 x = __ldg(reinterpret_cast<const uint4*>(src + (size_t)(krow0 + 32 * m) * a.n2));
+          v[4 * m] = x.x; v[4 * m + 1] = x.y; v[4 * m + 2] = x.z; v[4 * m + 3] = x.w;
+        }
+      } else {
+        const uint32_t* src =
+            a.in + ((size_t)it.limb * a.batch + it.b) * a.n + (size_t)(it.x0 + col) * a.n2;
+#pragma unroll
+        for (int t = 0; t < K / 128; ++t)
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint4 x = __ldg(reinterpret_cast<const uint4*>(src + (kb0 + 8 * t) * 16 + 4 * q4));
+            v[16 * t + 4 * q4] = x.x; v[16 * t + 4 * q4 + 1] = x.y;
+            v[16 * t + 4 * q4 + 2] = x.z; v[16 * t + 4 * q4 + 3] = x.w;
+          }
+      }
+    };
+    uint32_t cur[kVals], nxt[kVals];
+    UnitIter ahead = w;
+    if (cnt > 0) load_chunk(ahead, nxt);
+    for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
+#pragma unroll
+      for (int e = 0; e < kVals; ++e) cur[e] = nxt[e];
+      if (i + 1 < cnt) {
+        ahead.next(C, logR, R);
+        load_chunk(ahead, nxt);
+      }
+      if (i >= kRing) mbar_wait(&b_empty[w.s], w.rph ^ 1);
+      uint8_t* st = smem + w.s * kStageBytes;
+      if (STAGE == 1) {
+#pragma unroll
+        for (int m = 0; m < K / 32; ++m) {
+          const int k = krow0 + 32 * m;
+          uint32_t pw[4];
+          planes4(cur[4 * m], cur[4 * m + 1], cur[4 * m + 2], cur[4 * m + 3], pw);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<uint32_t*>(st + ring_off(j * 16 + r, k)) = w[j];
+            *reinterpret_cast<uint32_t*>(st + ring_off_mn(j, c4, k)) = pw[j];
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < K / 128; ++t) {
+          const int k0 = (kb0 + 8 * t) * 16;
+          uint32_t pw[4][4];  // [group][plane]
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            planes4(cur[16 * t + 4 * g], cur[16 * t + 4 * g + 1], cur[16 * t + 4 * g + 2],
+                    cur[16 * t + 4 * g + 3], pw[g]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(st + ring_off(j * 16 + col, k0)) =
+                make_uint4(pw[0][j], pw[1][j], pw[2][j], pw[3][j]);
         }
       }
       fence_proxy_async_smem();
-      mbar_arrive(&b_full[s]);
+      mbar_arrive(&b_full[w.s]);
     }
   } else if (warp < 8) {
     // ---------------------------------------------------------------- epilogue
@@ -180,14 +257,13 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     const int m = wq * 32 + lane;          // TMEM lane = twiddle row within the half
     const int r_tw = h * 128 + m;          // global twiddle row (k1 or k2)
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    int prev = -1, gi = -1;
-    long long it = 0;
-    for (long long u = u0; u < u1; ++u, ++it) {
-      const int limb = (int)(u / a.C);
+    uint8_t* my_stg = stg + m * kStgRow;
+    int prev = -1;
+    for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
+      const int limb = w.limb;
       const int prime = a.map.prime[limb];
       if (limb != prev) {
         // load this (limb, half)'s twiddle planes into TMEM columns [0, K)
-        ++gi;
         prev = limb;
         const uint32_t* src = a.twa + (((size_t)prime * a.H + h) * 128 + m) * K;
 #pragma unroll 1
@@ -204,46 +280,50 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
         tc_fence_before();
         mbar_arrive(tw_full);
       }
-      const int ab = (int)(it & 1);
-      mbar_wait(&acc_full[ab], (uint32_t)((it >> 1) & 1));
+      mbar_wait(&acc_full[w.ab], w.aph);
       tc_fence_after();
       uint32_t acc[7][16];
-      const uint32_t abase = tmem + lane_off + (ab ? kAccCol1 : kAccCol0);
+      const uint32_t abase = tmem + lane_off + (w.ab ? kAccCol1 : kAccCol0);
 #pragma unroll
       for (int s = 0; s < 7; ++s) tmem_ld16(abase + 16 * s, acc[s]);
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(&acc_empty[ab]);
+      mbar_arrive(&acc_empty[w.ab]);
 
       const PrimeConst pc = a.pc[prime];
-      const int col0 = (int)(u % a.C) * kNC;
-      const int b = col0 / a.R, x0 = col0 % a.R;
+      const int b = w.b, x0 = w.x0;
       uint32_t y[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        uint64_t v = (uint64_t)acc[0][e] + ((uint64_t)acc[1][e] << 8) +
-                     ((uint64_t)acc[2][e] << 16) + ((uint64_t)acc[3][e] << 24) +
-                     (uint64_t)acc[4][e] * pc.r[0] + (uint64_t)acc[5][e] * pc.r[1] +
-                     (uint64_t)acc[6][e] * pc.r[2];
-        y[e] = reduce64(v, pc.q, pc.mu);
+        // x = sum_s C_s 2^(8s) mod-q weights (< 2^60), then one Montgomery
+        // step: y = x R^-1 mod q (R = 2^32; the twiddles carry the R back)
+        uint64_t v = (uint64_t)acc[0][e];
+        v += (uint64_t)acc[1][e] * 256u;
+        v += (uint64_t)acc[2][e] * 65536u;
+        v += (uint64_t)acc[3][e] * pc.w3;
+        v += (uint64_t)acc[4][e] * pc.r[0];
+        v += (uint64_t)acc[5][e] * pc.r[1];
+        v += (uint64_t)acc[6][e] * pc.r[2];
+        const uint32_t mq = (uint32_t)v * pc.qneg_inv;
+        const uint32_t t = (uint32_t)((v + (uint64_t)mq * pc.q) >> 32);
+        y[e] = t >= pc.q ? t - pc.q : t;
       }
+      uint32_t* dst;
       if (STAGE == 1) {
         const size_t widx = (size_t)prime * a.n + (size_t)r_tw * a.n2 + x0;
-        uint32_t* dst = a.out + ((size_t)limb * a.batch + b) * a.n + (size_t)r_tw * a.n2 + x0;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          uint4 w = __ldg(reinterpret_cast<const uint4*>(a.w2 + widx + 4 * q4));
+          uint4 wv = __ldg(reinterpret_cast<const uint4*>(a.w2 + widx + 4 * q4));
           uint4 ws = __ldg(reinterpret_cast<const uint4*>(a.w2s + widx + 4 * q4));
-          uint4 o;
-          o.x = mul_shoup(y[4 * q4 + 0], w.x, ws.x, pc.q);
-          o.y = mul_shoup(y[4 * q4 + 1], w.y, ws.y, pc.q);
-          o.z = mul_shoup(y[4 * q4 + 2], w.z, ws.z, pc.q);
-          o.w = mul_shoup(y[4 * q4 + 3], w.w, ws.w, pc.q);
-          *reinterpret_cast<uint4*>(dst + 4 * q4) = o;
+          y[4 * q4 + 0] = mul_shoup(y[4 * q4 + 0], wv.x, ws.x, pc.q);
+          y[4 * q4 + 1] = mul_shoup(y[4 * q4 + 1], wv.y, ws.y, pc.q);
+          y[4 * q4 + 2] = mul_shoup(y[4 * q4 + 2], wv.z, ws.z, pc.q);
+          y[4 * q4 + 3] = mul_shoup(y[4 * q4 + 3], wv.w, ws.w, pc.q);
         }
+        dst = a.out + ((size_t)limb * a.batch + b) * a.n + (size_t)r_tw * a.n2 + x0;
       } else {
         const size_t pos = (size_t)r_tw * a.n1 + x0;  // out[n1*k2 + k1], k1 = x0 + e
-        uint32_t* dst = a.out + ((size_t)a.map.out_row[limb] * a.batch + b) * a.n + pos;
+        dst = a.out + ((size_t)a.map.out_row[limb] * a.batch + b) * a.n + pos;
         if (a.epi.mode == EPI_SUB_SCALE) {
           const uint32_t* xs = a.epi.x + ((size_t)a.epi.x_row[limb] * a.batch + b) * a.n + pos;
           const uint32_t s = a.epi.s[limb], sp = a.epi.s_shoup[limb];
@@ -256,42 +336,45 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
             y[e] = bs ? add_mod(__ldg(bs + e), t, pc.q) : t;
           }
         }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          *reinterpret_cast<uint4*>(dst + 4 * q4) =
-              make_uint4(y[4 * q4], y[4 * q4 + 1], y[4 * q4 + 2], y[4 * q4 + 3]);
       }
+      // 64 contiguous output bytes per thread
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4)
+        *reinterpret_cast<uint4*>(dst + 4 * q4) =
+            make_uint4(y[4 * q4], y[4 * q4 + 1], y[4 * q4 + 2], y[4 * q4 + 3]);
     }
+    (void)my_stg;
   } else if (lane == 0) {
     // ---------------------------------------------------------------- MMA issuer
-    constexpr uint32_t id64 = idesc_i8(128, 64), id48 = idesc_i8(128, 48),
-                       id16 = idesc_i8(128, 16);
-    int prev = -1, gi = -1;
-    long long it = 0;
-    for (long long u = u0; u < u1; ++u, ++it) {
-      const int limb = (int)(u / a.C);
-      if (limb != prev) {
-        ++gi;
-        prev = limb;
-        mbar_wait(tw_full, (uint32_t)(gi & 1));
+    // stage 1 streams B' MN-major (b_major bit 16), stage 2 K-major
+    constexpr uint32_t bmaj = STAGE == 1 ? (1u << 16) : 0u;
+    constexpr uint32_t id64 = idesc_i8(128, 64) | bmaj, id48 = idesc_i8(128, 48) | bmaj,
+                       id16 = idesc_i8(128, 16) | bmaj;
+    constexpr uint32_t kLbo = STAGE == 1 ? 128 : 1024, kSbo = STAGE == 1 ? 512 : 128;
+    constexpr uint32_t kPlane3 = STAGE == 1 ? 3 * 512 : 6 * 128;  // start of B' plane 3
+    int prev = -1;
+    uint32_t twph = 0;
+    for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
+      if (w.limb != prev) {
+        if (prev >= 0) twph ^= 1;
+        prev = w.limb;
+        mbar_wait(tw_full, twph);
       }
-      const int s = (int)(it % kRing);
-      mbar_wait(&b_full[s], (uint32_t)((it / kRing) & 1));
-      const int ab = (int)(it & 1);
-      if (it >= 2) mbar_wait(&acc_empty[ab], (uint32_t)(((it >> 1) & 1) ^ 1));
+      mbar_wait(&b_full[w.s], w.rph);
+      if (i >= 2) mbar_wait(&acc_empty[w.ab], w.aph ^ 1);
       tc_fence_after();
-      const uint32_t d = tmem + (ab ? kAccCol1 : kAccCol0);
-      const uint32_t sb = smem_u32(smem + s * kStageBytes);
+      const uint32_t d = tmem + (w.ab ? kAccCol1 : kAccCol0);
+      const uint32_t sb = smem_u32(smem + w.s * kStageBytes);
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) {
         const uint32_t bt = sb + kc * 2048;
-        const uint64_t bd = smem_desc_kmajor(bt, 1024, 128);
+        const uint64_t bd = smem_desc_kmajor(bt, kLbo, kSbo);
         const uint32_t a0 = tmem + 0 * (K / 4) + kc * 8, a1 = tmem + 1 * (K / 4) + kc * 8;
         const uint32_t a2 = tmem + 2 * (K / 4) + kc * 8, a3 = tmem + 3 * (K / 4) + kc * 8;
         if (kc == 0) {
           mma_i8_ts(d + 48, a3, bd, id64, 0);   // blocks 3..6 = T_3 X_0..3 (init)
           mma_i8_ts(d + 0, a0, bd, id48, 0);    // blocks 0..2 = T_0 X_0..2 (init)
-          mma_i8_ts(d + 48, a0, smem_desc_kmajor(bt + 768, 1024, 128), id16, 1);  // + T_0 X_3
+          mma_i8_ts(d + 48, a0, smem_desc_kmajor(bt + kPlane3, kLbo, kSbo), id16, 1);  // + T_0 X_3
           mma_i8_ts(d + 16, a1, bd, id64, 1);
           mma_i8_ts(d + 32, a2, bd, id64, 1);
         } else {
@@ -301,8 +384,8 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
           mma_i8_ts(d + 48, a3, bd, id64, 1);
         }
       }
-      mma_commit(&b_empty[s]);
-      mma_commit(&acc_full[ab]);
+      mma_commit(&b_empty[w.s]);
+      mma_commit(&acc_full[w.ab]);
     }
   }
 
@@ -316,7 +399,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
 
 template <int STAGE, int K>
 int launch_ts(const Ctx& c, TsArgs& a, cudaStream_t st) {
-  const int smem = kRing * ring_stage_bytes<K>() + (2 * kRing + 5) * 8 + 16;
+  const int smem = kRing * ring_stage_bytes<K>() + 2 * kStgBytes + (2 * kRing + 5) * 8 + 16;
   auto kern = ntt_ts_kernel<STAGE, K>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const long long U = (long long)a.n_limbs * a.C;
@@ -382,6 +465,8 @@ int build_ts_tables(Ctx& c) {
                 ex = inv ? (uint64_t)n1 * (2ull * k * r + r) : (uint64_t)n1 * (2ull * k * r);
               uint32_t v = pw[ex % two_n];
               if (s == 1 && inv) v = mulmod_h(v, n_inv, q);
+              // stage 2 twiddles carry R = 2^32: the Montgomery epilogue divides it out
+              if (s == 1) v = (uint32_t)(((uint64_t)v << 32) % q);
               for (int i = 0; i < 4; ++i) words[i] |= ((v >> (8 * i)) & 0xFFu) << (8 * e);
             }
             for (int i = 0; i < 4; ++i) row[i * (K / 4) + kq] = words[i];
@@ -395,6 +480,30 @@ int build_ts_tables(Ctx& c) {
         return 3;
       }
     }
+  // W2 * R mod q (+ Shoup): stage 1's Montgomery result carries R^-1
+  for (int inv = 0; inv < 2; ++inv) {
+    std::vector<uint32_t> w2((size_t)np * n), w2s((size_t)np * n);
+    if (cudaMemcpy(w2.data(), c.d_w2[inv], w2.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      set_error("w2 readback failed");
+      return 3;
+    }
+    for (int p = 0; p < np; ++p) {
+      const uint32_t q = c.primes[p];
+      for (size_t i = 0; i < (size_t)n; ++i) {
+        uint32_t& v = w2[(size_t)p * n + i];
+        v = (uint32_t)(((uint64_t)v << 32) % q);
+        w2s[(size_t)p * n + i] = (uint32_t)(((uint64_t)v << 32) / q);
+      }
+    }
+    const size_t bytes = w2.size() * 4;
+    if (cudaMalloc(&c.d_w2r[inv], bytes) != cudaSuccess ||
+        cudaMalloc(&c.d_w2rs[inv], bytes) != cudaSuccess ||
+        cudaMemcpy(c.d_w2r[inv], w2.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c.d_w2rs[inv], w2s.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+      set_error("w2r upload failed");
+      return 3;
+    }
+  }
   return 0;
 }
 
@@ -416,8 +525,8 @@ int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap
   a.in = in;
   a.out = P;
   a.twa = c.d_twa[inverse][0];
-  a.w2 = c.d_w2[inverse];
-  a.w2s = c.d_w2s[inverse];
+  a.w2 = c.d_w2r[inverse];
+  a.w2s = c.d_w2rs[inverse];
   a.R = c.n2;
   a.H = c.n1 / 128;
   a.C = batch * c.n2 / kNC;

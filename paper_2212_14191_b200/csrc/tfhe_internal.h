@@ -18,6 +18,9 @@ struct PrimeConst {
   uint64_t mu;          // floor(2^64 / q)
   uint32_t n_inv_shoup;
   uint32_t r[3];        // 2^32, 2^40, 2^48 mod q (byte weights 4..6 of the TS kernel)
+  uint32_t w3;          // 2^24 mod q
+  uint32_t qneg_inv;    // -q^-1 mod 2^32 (Montgomery, R = 2^32)
+  uint32_t pad[2];
 };
 
 // Per-launch limb map: output row l uses prime `prime[l]`, reads input row
@@ -60,6 +63,9 @@ struct Ctx {
   // twiddle-resident (TS) kernel: per [inverse][stage] words
   // [prime][half][row 128][plane 4][K/4], used when n1 >= 128
   uint32_t* d_twa[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  // stage-1 hadamard twiddles pre-scaled by R = 2^32 (Montgomery epilogue), + Shoup
+  uint32_t* d_w2r[2] = {nullptr, nullptr};
+  uint32_t* d_w2rs[2] = {nullptr, nullptr};
   bool use_ts = false;
   int sms = 148;
   std::vector<PrimeConst> h_pc;
