@@ -352,6 +352,8 @@ void tfhe_ctx_destroy(TfheCtx* h) {
     }
     cudaFree(c.d_w2[i]);
     cudaFree(c.d_w2s[i]);
+    cudaFree(c.d_w2r[i]);
+    cudaFree(c.d_w2rs[i]);
   }
   delete h;
 }

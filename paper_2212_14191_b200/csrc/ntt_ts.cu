@@ -122,16 +122,26 @@ TFHE_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "me
 TFHE_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 TFHE_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-constexpr int kStgRow = 80;                       // padded staging row (bank-conflict free)
-constexpr int kStgBytes = 128 * kStgRow;          // one staging buffer
+constexpr int kWarpStg = 3 * 2048;                // per epilogue warp: x | base | y rows
+constexpr int kStgBytes = 4 * kWarpStg;           // all 4 epilogue warps
+
+// 32 rows x 64 B staging, 16-byte chunks XOR-swizzled so both the row-wise
+// and the 4-lanes-per-row accesses are bank-conflict free
+TFHE_DEV uint32_t stg_off(int row, int q) { return (uint32_t)(row * 64 + 16 * (q ^ ((row >> 1) & 3))); }
+
+TFHE_DEV uint32_t mont_reduce(uint64_t v, const PrimeConst& pc) {
+  const uint32_t mq = (uint32_t)v * pc.qneg_inv;
+  const uint32_t t = (uint32_t)((v + (uint64_t)mq * pc.q) >> 32);
+  return t >= pc.q ? t - pc.q : t;
+}
 
 template <int STAGE, int K>
 __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_constant__ TsArgs a) {
   constexpr int kStageBytes = ring_stage_bytes<K>();
   constexpr int KC = K / 32;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* stg = smem + kRing * kStageBytes;  // 2 epilogue staging buffers
-  uint64_t* b_full = reinterpret_cast<uint64_t*>(stg + 2 * kStgBytes);
+  uint8_t* stg = smem + kRing * kStageBytes;  // epilogue staging
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(stg + kStgBytes);
   uint64_t* b_empty = b_full + kRing;
   uint64_t* acc_full = b_empty + kRing;
   uint64_t* acc_empty = acc_full + 2;
@@ -199,13 +209,15 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
           v[4 * m] = x.x; v[4 * m + 1] = x.y; v[4 * m + 2] = x.z; v[4 * m + 3] = x.w;
         }
       } else {
-        const uint32_t* src =
-            a.in + ((size_t)it.limb * a.batch + it.b) * a.n + (size_t)(it.x0 + col) * a.n2;
+        // blocked P [limb][b][i2/16][k1][16]: row k1's k-block = 64 contiguous bytes
+        const uint32_t* src = a.in + ((size_t)it.limb * a.batch + it.b) * a.n +
+                              (size_t)(it.x0 + col) * kNC;
 #pragma unroll
         for (int t = 0; t < K / 128; ++t)
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            uint4 x = __ldg(reinterpret_cast<const uint4*>(src + (kb0 + 8 * t) * 16 + 4 * q4));
+            uint4 x = __ldg(reinterpret_cast<const uint4*>(
+                src + (size_t)(kb0 + 8 * t) * kNC * a.n1 + 4 * q4));
             v[16 * t + 4 * q4] = x.x; v[16 * t + 4 * q4 + 1] = x.y;
             v[16 * t + 4 * q4 + 2] = x.z; v[16 * t + 4 * q4 + 3] = x.w;
           }
@@ -257,7 +269,39 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     const int m = wq * 32 + lane;          // TMEM lane = twiddle row within the half
     const int r_tw = h * 128 + m;          // global twiddle row (k1 or k2)
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    uint8_t* my_stg = stg + m * kStgRow;
+    uint8_t* wstg = stg + wq * kWarpStg;   // this warp's staging (x | base | y)
+    // Operands that do not depend on the accumulators (W2 for stage 1; the
+    // x / base rows of the fused epilogue for stage 2) are prefetched one
+    // chunk ahead so their global latency overlaps the previous chunk.
+    const bool sub_scale = STAGE == 2 && a.epi.mode == EPI_SUB_SCALE;
+    uint32_t pf_w[16];
+    uint4 pf_x[4], pf_b[4];
+    bool pf_has_base = false;
+    auto prefetch = [&](const UnitIter& it) {
+      const int pr = a.map.prime[it.limb];
+      if (STAGE == 1) {
+        // W2 * R^2 in [prime][i2/16][e][k1] layout: 16 warp-coalesced loads
+        const uint32_t* wp =
+            a.w2 + ((size_t)pr * (a.n2 / kNC) + it.x0 / kNC) * kNC * a.n1 + r_tw;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pf_w[e] = __ldg(wp + (size_t)e * a.n1);
+      } else if (sub_scale) {
+        // this warp's 32 output rows of x (and base), 4 lanes per 64-byte row
+        const int br = a.epi.base_row[it.limb];
+        pf_has_base = br >= 0;
+        const uint32_t* xb = a.epi.x + ((size_t)a.epi.x_row[it.limb] * a.batch + it.b) * a.n + it.x0;
+        const uint32_t* bb =
+            pf_has_base ? a.epi.base + ((size_t)br * a.batch + it.b) * a.n + it.x0 : xb;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const size_t off = (size_t)(h * 128 + wq * 32 + 8 * q + (lane >> 2)) * a.n1 + 4 * (lane & 3);
+          pf_x[q] = __ldg(reinterpret_cast<const uint4*>(xb + off));
+          pf_b[q] = __ldg(reinterpret_cast<const uint4*>(bb + off));
+        }
+      }
+    };
+    UnitIter ahead = w;
+    if (cnt > 0) prefetch(ahead);
     int prev = -1;
     for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
       const int limb = w.limb;
@@ -280,6 +324,34 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
         tc_fence_before();
         mbar_arrive(tw_full);
       }
+      const PrimeConst pc = a.pc[prime];
+      const int b = w.b;
+      uint32_t w2v[16], xrow[16], brow[16];
+      const bool has_base = pf_has_base;
+      if (STAGE == 1) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) w2v[e] = pf_w[e];
+      } else if (sub_scale) {
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = 8 * q + (lane >> 2), p = lane & 3;
+          *reinterpret_cast<uint4*>(wstg + stg_off(r, p)) = pf_x[q];
+          *reinterpret_cast<uint4*>(wstg + 2048 + stg_off(r, p)) = pf_b[q];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 v = *reinterpret_cast<const uint4*>(wstg + stg_off(lane, q));
+          xrow[4 * q] = v.x; xrow[4 * q + 1] = v.y; xrow[4 * q + 2] = v.z; xrow[4 * q + 3] = v.w;
+          uint4 u = *reinterpret_cast<const uint4*>(wstg + 2048 + stg_off(lane, q));
+          brow[4 * q] = u.x; brow[4 * q + 1] = u.y; brow[4 * q + 2] = u.z; brow[4 * q + 3] = u.w;
+        }
+      }
+      if (i + 1 < cnt) {
+        ahead.next(C, logR, R);
+        prefetch(ahead);
+      }
       mbar_wait(&acc_full[w.ab], w.aph);
       tc_fence_after();
       uint32_t acc[7][16];
@@ -290,8 +362,6 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       tc_fence_before();
       mbar_arrive(&acc_empty[w.ab]);
 
-      const PrimeConst pc = a.pc[prime];
-      const int b = w.b, x0 = w.x0;
       uint32_t y[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
@@ -304,46 +374,46 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
         v += (uint64_t)acc[4][e] * pc.r[0];
         v += (uint64_t)acc[5][e] * pc.r[1];
         v += (uint64_t)acc[6][e] * pc.r[2];
-        const uint32_t mq = (uint32_t)v * pc.qneg_inv;
-        const uint32_t t = (uint32_t)((v + (uint64_t)mq * pc.q) >> 32);
-        y[e] = t >= pc.q ? t - pc.q : t;
+        y[e] = mont_reduce(v, pc);
       }
-      uint32_t* dst;
       if (STAGE == 1) {
-        const size_t widx = (size_t)prime * a.n + (size_t)r_tw * a.n2 + x0;
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          uint4 wv = __ldg(reinterpret_cast<const uint4*>(a.w2 + widx + 4 * q4));
-          uint4 ws = __ldg(reinterpret_cast<const uint4*>(a.w2s + widx + 4 * q4));
-          y[4 * q4 + 0] = mul_shoup(y[4 * q4 + 0], wv.x, ws.x, pc.q);
-          y[4 * q4 + 1] = mul_shoup(y[4 * q4 + 1], wv.y, ws.y, pc.q);
-          y[4 * q4 + 2] = mul_shoup(y[4 * q4 + 2], wv.z, ws.z, pc.q);
-          y[4 * q4 + 3] = mul_shoup(y[4 * q4 + 3], wv.w, ws.w, pc.q);
-        }
-        dst = a.out + ((size_t)limb * a.batch + b) * a.n + (size_t)r_tw * a.n2 + x0;
-      } else {
-        const size_t pos = (size_t)r_tw * a.n1 + x0;  // out[n1*k2 + k1], k1 = x0 + e
-        dst = a.out + ((size_t)a.map.out_row[limb] * a.batch + b) * a.n + pos;
-        if (a.epi.mode == EPI_SUB_SCALE) {
-          const uint32_t* xs = a.epi.x + ((size_t)a.epi.x_row[limb] * a.batch + b) * a.n + pos;
-          const uint32_t s = a.epi.s[limb], sp = a.epi.s_shoup[limb];
-          const int br = a.epi.base_row[limb];
-          const uint32_t* bs =
-              br >= 0 ? a.epi.base + ((size_t)br * a.batch + b) * a.n + pos : nullptr;
+        for (int e = 0; e < 16; ++e) y[e] = mont_reduce((uint64_t)y[e] * w2v[e], pc);
+      } else if (sub_scale) {
+        const uint32_t s = a.epi.s[limb], sp = a.epi.s_shoup[limb];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            uint32_t t = mul_shoup(sub_mod(__ldg(xs + e), y[e], pc.q), s, sp, pc.q);
-            y[e] = bs ? add_mod(__ldg(bs + e), t, pc.q) : t;
-          }
+        for (int e = 0; e < 16; ++e) {
+          uint32_t t = mul_shoup(sub_mod(xrow[e], y[e], pc.q), s, sp, pc.q);
+          y[e] = has_base ? add_mod(brow[e], t, pc.q) : t;
         }
       }
-      // 64 contiguous output bytes per thread
+      // ---- store: transpose the warp's 32 x 64-byte rows through smem so
+      // every global store instruction writes 4 lanes per 64-byte row
+      __syncwarp();
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4)
-        *reinterpret_cast<uint4*>(dst + 4 * q4) =
-            make_uint4(y[4 * q4], y[4 * q4 + 1], y[4 * q4 + 2], y[4 * q4 + 3]);
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(wstg + 4096 + stg_off(lane, q)) =
+            make_uint4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+      __syncwarp();
+      uint32_t* dst;
+      size_t row_stride;
+      if (STAGE == 1) {
+        // blocked P layout [limb][b][i2/16][k1][16]: the warp's rows are 2 KB contiguous
+        dst = a.out + (((size_t)limb * a.batch + b) * (a.n2 / kNC) + w.x0 / kNC) * kNC * a.n1 +
+              (size_t)(h * 128 + wq * 32) * kNC;
+        row_stride = kNC;
+      } else {
+        dst = a.out + ((size_t)a.map.out_row[limb] * a.batch + b) * a.n +
+              (size_t)(h * 128 + wq * 32) * a.n1 + w.x0;
+        row_stride = a.n1;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = 8 * q + (lane >> 2), p = lane & 3;
+        *reinterpret_cast<uint4*>(dst + (size_t)r * row_stride + 4 * p) =
+            *reinterpret_cast<const uint4*>(wstg + 4096 + stg_off(r, p));
+      }
     }
-    (void)my_stg;
   } else if (lane == 0) {
     // ---------------------------------------------------------------- MMA issuer
     // stage 1 streams B' MN-major (b_major bit 16), stage 2 K-major
@@ -399,7 +469,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
 
 template <int STAGE, int K>
 int launch_ts(const Ctx& c, TsArgs& a, cudaStream_t st) {
-  const int smem = kRing * ring_stage_bytes<K>() + 2 * kStgBytes + (2 * kRing + 5) * 8 + 16;
+  const int smem = kRing * ring_stage_bytes<K>() + kStgBytes + (2 * kRing + 5) * 8 + 16;
   auto kern = ntt_ts_kernel<STAGE, K>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const long long U = (long long)a.n_limbs * a.C;
@@ -480,26 +550,27 @@ int build_ts_tables(Ctx& c) {
         return 3;
       }
     }
-  // W2 * R mod q (+ Shoup): stage 1's Montgomery result carries R^-1
+  // W2 * R^2 mod q in [prime][i2/16][e][k1] layout: stage 1 multiplies its
+  // Montgomery result (S R^-1) by this with another Montgomery step -> S * W2;
+  // the layout makes the epilogue's per-row loads warp-coalesced
   for (int inv = 0; inv < 2; ++inv) {
-    std::vector<uint32_t> w2((size_t)np * n), w2s((size_t)np * n);
+    std::vector<uint32_t> w2((size_t)np * n), w2t((size_t)np * n);
     if (cudaMemcpy(w2.data(), c.d_w2[inv], w2.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
       set_error("w2 readback failed");
       return 3;
     }
     for (int p = 0; p < np; ++p) {
       const uint32_t q = c.primes[p];
-      for (size_t i = 0; i < (size_t)n; ++i) {
-        uint32_t& v = w2[(size_t)p * n + i];
-        v = (uint32_t)(((uint64_t)v << 32) % q);
-        w2s[(size_t)p * n + i] = (uint32_t)(((uint64_t)v << 32) / q);
-      }
+      const uint64_t r2 = ((uint64_t)1 << 32) % q * (((uint64_t)1 << 32) % q) % q;
+      for (int k1 = 0; k1 < n1; ++k1)
+        for (int i2 = 0; i2 < n2; ++i2) {
+          const uint64_t v = (uint64_t)w2[(size_t)p * n + (size_t)k1 * n2 + i2] * r2 % q;
+          w2t[(size_t)p * n + ((size_t)(i2 / 16) * 16 + (i2 % 16)) * n1 + k1] = (uint32_t)v;
+        }
     }
-    const size_t bytes = w2.size() * 4;
+    const size_t bytes = w2t.size() * 4;
     if (cudaMalloc(&c.d_w2r[inv], bytes) != cudaSuccess ||
-        cudaMalloc(&c.d_w2rs[inv], bytes) != cudaSuccess ||
-        cudaMemcpy(c.d_w2r[inv], w2.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(c.d_w2rs[inv], w2s.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaMemcpy(c.d_w2r[inv], w2t.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
       set_error("w2r upload failed");
       return 3;
     }
@@ -526,7 +597,7 @@ int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap
   a.out = P;
   a.twa = c.d_twa[inverse][0];
   a.w2 = c.d_w2r[inverse];
-  a.w2s = c.d_w2rs[inverse];
+  a.w2s = nullptr;
   a.R = c.n2;
   a.H = c.n1 / 128;
   a.C = batch * c.n2 / kNC;

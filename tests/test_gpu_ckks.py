@@ -1,0 +1,104 @@
+"""GPU parity of the CKKS evaluation operators against the reference.
+
+Golden outputs were produced by running the reference (`rnsckks`) itself on
+the seeded synthetic inputs of tests/golden/synth.py (make_golden.py); the
+GPU path must reproduce them bit for bit (integer arithmetic, zero tolerance).
+Large (N=2^14, 2^16) cases are pinned by sha256 of the reference outputs.
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+import synth
+
+pytestmark = pytest.mark.gpu
+
+SMALL = [("small_full", "small", 5, 11), ("small_l4", "small", 4, 12),
+         ("small_l2", "small", 2, 13), ("default_full", "default", 5, 14),
+         ("set_a_full", "set_a", 1, 15), ("set_b_full", "set_b", 2, 16)]
+LARGE = [("n16_l3", "n16", 3, 21), ("resnet20_l3", "resnet20", 3, 22),
+         ("set_c_full", "set_c", 7, 23)]
+
+
+def _params(kind):
+    from paper_2212_14191_b200.params import CkksParams
+    if kind == "small":
+        return CkksParams.generate(n=256, l_max=5, k=3, dnum=3, bit_size=30)
+    if kind == "n16":
+        return CkksParams.generate(n=1 << 16, l_max=3, k=1, dnum=4, bit_size=28)
+    return CkksParams.from_preset(kind)
+
+
+_CTX = {}
+
+
+def _ctx(kind):
+    from paper_2212_14191_b200.ckks import CkksContext
+    if kind not in _CTX:
+        _CTX[kind] = CkksContext(_params(kind))
+    return _CTX[kind]
+
+
+def _run(kind, level, seed):
+    """Run every op on the product path; return {name: (2, l, n) array}."""
+    from paper_2212_14191_b200.ckks import Ciphertext
+    from paper_2212_14191_b200.rns import NTT, RnsPolynomial
+    ctx = _ctx(kind)
+    p = ctx.params
+    ins = synth.ckks_inputs(p.chain.q, p.chain.p, p.n, p.dnum, level, seed)
+    basis = tuple(p.chain.q[:level + 1])
+
+    def poly(rows):
+        return RnsPolynomial(rows=rows, basis=basis, domain=NTT)
+
+    c0 = Ciphertext(b=poly(ins["b0"]), a=poly(ins["a0"]), scale=1, level=level)
+    c1 = Ciphertext(b=poly(ins["b1"]), a=poly(ins["a1"]), scale=1, level=level)
+    rlk, rk = ins["rlk"], ins["rotk"]
+    out = {}
+    m = ctx.hmult(c0, c1, rlk)
+    out["hmult"] = np.stack([m.b.rows, m.a.rows])
+    ksb, ksa = ctx.key_switch(poly(ins["a0"]), rlk)
+    out["keyswitch"] = np.stack([ksb.rows, ksa.rows])
+    if level >= 1:
+        r = ctx.rescale(m)
+        out["hmult_rescale"] = np.stack([r.b.rows, r.a.rows])
+        r0 = ctx.rescale(c0)
+        out["rescale"] = np.stack([r0.b.rows, r0.a.rows])
+    h = ctx.hrotate(c0, 1, rk)
+    out["hrotate_1"] = np.stack([h.b.rows, h.a.rows])
+    hc = ctx.hconjugate(c0, rk)
+    out["hconjugate"] = np.stack([hc.b.rows, hc.a.rows])
+    s = ctx.hadd(c0, c1)
+    out["hadd"] = np.stack([s.b.rows, s.a.rows])
+    s = ctx.hsub(c0, c1)
+    out["hsub"] = np.stack([s.b.rows, s.a.rows])
+    return out
+
+
+@pytest.fixture(scope="module")
+def ckks_small():
+    return np.load(os.path.join(GOLDEN, "ckks_small.npz"))
+
+
+@pytest.mark.parametrize("case,kind,level,seed", SMALL)
+def test_ckks_ops_golden_small(case, kind, level, seed, ckks_small):
+    got = _run(kind, level, seed)
+    for op, arr in got.items():
+        want = ckks_small[f"{case}/{op}"]
+        assert np.array_equal(arr, want), (case, op)
+
+
+@pytest.mark.parametrize("case,kind,level,seed", LARGE)
+def test_ckks_ops_golden_large(case, kind, level, seed):
+    with open(os.path.join(GOLDEN, "ckks_large.json")) as fh:
+        rec = json.load(fh)[case]
+    got = _run(kind, level, seed)
+    for op, arr in got.items():
+        h = hashlib.sha256(np.ascontiguousarray(arr, dtype=np.uint32).tobytes()).hexdigest()
+        assert arr.reshape(-1)[:8].tolist() == rec[op]["head"], (case, op)
+        assert h == rec[op]["sha256"], (case, op)
