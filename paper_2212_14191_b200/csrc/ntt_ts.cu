@@ -414,8 +414,10 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
             *reinterpret_cast<const uint4*>(wstg + 4096 + stg_off(r, p));
       }
     }
-  } else if (lane == 0) {
+  } else {
     // ---------------------------------------------------------------- MMA issuer
+    // The whole warp walks the loop (so descriptors stay warp-uniform and live
+    // in uniform registers); one elected lane issues the tcgen05 ops.
     // stage 1 streams B' MN-major (b_major bit 16), stage 2 K-major
     constexpr uint32_t bmaj = STAGE == 1 ? (1u << 16) : 0u;
     constexpr uint32_t id64 = idesc_i8(128, 64) | bmaj, id48 = idesc_i8(128, 48) | bmaj,
@@ -435,6 +437,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       tc_fence_after();
       const uint32_t d = tmem + (w.ab ? kAccCol1 : kAccCol0);
       const uint32_t sb = smem_u32(smem + w.s * kStageBytes);
+      if (elect_one()) {
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) {
         const uint32_t bt = sb + kc * 2048;
@@ -456,6 +459,8 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       }
       mma_commit(&b_empty[w.s]);
       mma_commit(&acc_full[w.ab]);
+      }
+      __syncwarp();
     }
   }
 
