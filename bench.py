@@ -1,0 +1,399 @@
+"""Benchmark of the batched CKKS hot path on B200 (driver contract, one JSON line).
+
+Headline (BASELINE.json metric "NTT KOPS and HMULT KOPS (N=2^16, batched)"):
+
+* `value`  = limb-NTT KOPS: N = 2^16 negacyclic transforms of one residue row
+  (forward and inverse each count 1) over the paper-Default RNS chain
+  (`p_default`: 45 chain primes) and a batch of B ciphertext
+  polynomials -- BASELINE configs[1].  One step = batched forward NTT +
+  batched inverse NTT of the whole (45, B, 65536) buffer (2*45*B limb-NTTs).
+  Inputs (1.47 GB at B=128) are larger than L2, so no flush is needed.
+* `hmult_kops` = HMULT+relinearisation+rescale per second / 1e3 at N=2^16
+  P-Default (configs[2]), measured with the same protocol.
+
+Multi-GPU (torchrun, one rank per GPU): every rank transforms its own batch
+(independent ciphertexts shard with no collective; "scaling": "weak");
+timing is device time, barrier-bracketed, max over ranks.
+
+`--impl reference` times the CPU oracle port (oracle/, plain C + OpenMP, the
+reference's algorithm) on a bounded sample of the same workload on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PRESET = "p_default"
+N = 1 << 16
+METRIC = "NTT KOPS and HMULT KOPS (N=2^16, batched)"
+UNIT = "K limb-NTT/s"
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([s.strip() for s in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 5 + i and s[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg and --impl reference)
+# ----------------------------------------------------------------------------
+
+def cpu_oracle_rate(primes, members, reps=1):
+    """limb-NTT/s of the C oracle (fwd + inv over len(primes) limbs x members)."""
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    O.THREADS = threads
+    rng = np.random.default_rng(7)
+    x = O.uniform_rows(rng, primes, (members, N))
+    O.ntt(x[:1, :1], primes[:1])           # build tables / warm the library
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        f = O.ntt(x, primes)
+        O.intt(f, primes)
+    dt = time.perf_counter() - t0
+    return 2 * len(primes) * members * reps / dt, dt, threads
+
+
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    from paper_2212_14191_b200.params import CkksParams
+    primes = list(CkksParams.from_preset(PRESET).chain.q)
+    members = args.cpu_members
+    for _ in range(args.warmup):
+        cpu_oracle_rate(primes, 1)
+    rates, total = [], 0.0
+    for _ in range(args.steps):
+        r, dt, threads = cpu_oracle_rate(primes, members)
+        rates.append(r)
+        total += dt
+    value = float(np.median(rates)) / 1e3
+    sample = (f"fwd+inv NTT N=2^16 over the {len(primes)} p_default chain primes x "
+              f"{members} members per step ({2 * len(primes) * members} limb-NTTs)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"batched NTT/INTT N=2^16, {PRESET} ({len(primes)} limbs)",
+                   "sample_members": members},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# B200 arm
+# ----------------------------------------------------------------------------
+
+def int8_peak_tops(torch):
+    """Dense int8 tensor throughput of this GPU (torch._int_mm 8192^3, best of 10)."""
+    try:
+        a = torch.randint(-128, 127, (8192, 8192), dtype=torch.int8, device="cuda")
+        b = torch.randint(-128, 127, (8192, 8192), dtype=torch.int8, device="cuda")
+        for _ in range(3):
+            torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(10):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            torch._int_mm(a, b)
+            e.record()
+            torch.cuda.synchronize()
+            best = min(best, s.elapsed_time(e))
+        del a, b
+        return 2 * 8192 ** 3 / (best / 1e3) / 1e12
+    except Exception:
+        return None
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    from paper_2212_14191_b200.batch import BatchBuffer, batched_apply
+    from paper_2212_14191_b200.ckks import CiphertextBatch, CkksContext
+    from paper_2212_14191_b200.device import DeviceContext
+    from paper_2212_14191_b200.ntt import TwiddleTable
+    from paper_2212_14191_b200.params import CkksParams
+
+    params = CkksParams.from_preset(PRESET)
+    primes = list(params.chain.q)
+    L, B = len(primes), args.batch
+    ext = tuple(params.chain.q) + tuple(params.chain.p)
+    ctx = DeviceContext.get(N, ext, n_chain=L, n_special=len(params.chain.p), device=dev)
+
+    # synthetic uniform residues per limb (cli._random_batch, cli.py:59-64), on device
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    x = torch.empty((L, B, N), dtype=torch.int32, device=dev)
+    for i, q in enumerate(primes):
+        x[i] = torch.randint(0, q, (B, N), generator=g, device=dev, dtype=torch.int64).to(torch.int32)
+    f = torch.empty_like(x)
+    y = torch.empty_like(x)
+
+    def step():
+        ctx.ntt(x, primes, out=f)
+        ctx.ntt(f, primes, inverse=True, out=y)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    # parity spot check of the timed path against the CPU oracle (rank 0)
+    parity = None
+    if rank == 0:
+        from oracle import oracle as O
+        xs = x[:2, :1].cpu().numpy().view(np.uint32)
+        fs = f[:2, :1].cpu().numpy().view(np.uint32)
+        parity = bool(np.array_equal(fs, O.ntt(xs, primes[:2])) and
+                      np.array_equal(y[:2, :1].cpu().numpy().view(np.uint32), xs))
+
+    stream = torch.cuda.current_stream(dev)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(args.steps):
+            step()
+        e.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = max_over_ranks(s.elapsed_time(e))
+    limb_ntts = 2 * L * B * args.steps * world
+    value = limb_ntts / (ms / 1e3) / 1e3
+
+    # roofline of the dominant kernel (the tensor-core NTT stage kernel):
+    # algorithmic int8 ops per limb-NTT = 2 stages x 16 byte products x 2 ops
+    # x N x n1 (n1 = n2 = 256) = 32 N (n1 + n2)
+    n1, n2 = ctx.plan
+    ops_per_limb = 32 * N * (n1 + n2)
+    ntt_call_ms = ms / (2 * args.steps)             # one batched NTT = 2 kernel launches
+    achieved_tops = L * B * ops_per_limb / (ntt_call_ms / 1e3) / 1e12
+
+    # HMULT + relin + rescale (configs[2]), same protocol
+    hm = None
+    if args.hmult_batch > 0:
+        ck = CkksContext(params, device=dev)
+        Bh, l1, E = args.hmult_batch, L, L + len(params.chain.p)
+        key = torch.empty((params.dnum, 2, E, N), dtype=torch.int32, device=dev)
+        for i, q in enumerate(ext):
+            key[:, :, i] = torch.randint(0, q, (params.dnum, 2, N), generator=g, device=dev,
+                                         dtype=torch.int64).to(torch.int32)
+        cts = []
+        for _ in range(2):
+            d = torch.empty((2, l1, Bh, N), dtype=torch.int32, device=dev)
+            for i, q in enumerate(primes):
+                d[:, i] = torch.randint(0, q, (2, Bh, N), generator=g, device=dev,
+                                        dtype=torch.int64).to(torch.int32)
+            cts.append(CiphertextBatch(d, params.l_max))
+
+        def hstep():
+            ck.rescale_batch(ck.hmult_batch(cts[0], cts[1], key))
+
+        for _ in range(max(args.warmup, 1)):
+            hstep()
+        torch.cuda.synchronize()
+        barrier()
+        hs, he = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        hsteps = max(1, min(args.steps, 5))
+        hs.record(stream)
+        for _ in range(hsteps):
+            hstep()
+        he.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        hms = max_over_ranks(hs.elapsed_time(he))
+        hm = {"hmult_kops": Bh * hsteps * world / (hms / 1e3) / 1e3,
+              "ms_per_batch": hms / hsteps, "batch_per_gpu": Bh}
+        del ck, key, cts
+
+    # end to end through the reference-facing API (batched_apply) with pinned host buffers
+    table = TwiddleTable(N, primes, device=dev)
+    table._ctx = ctx
+    host_in = torch.empty((L, B, N), dtype=torch.int32, pin_memory=True)
+    host_in.copy_(x)
+    e2e_steps = max(1, min(args.steps, 3))
+    buf = BatchBuffer(data=host_in, basis=primes, domain="coeff")
+    batched_apply(batched_apply(buf, "ntt", table=table), "intt", table=table)  # warm
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        out = batched_apply(buf, "ntt", table=table)        # H2D + NTT + D2H
+        back = batched_apply(out, "intt", table=table)       # H2D + INTT + D2H
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_ok = bool(torch.equal(back.data, host_in))
+    e2e_value = 2 * L * B * e2e_steps * world / e2e_s / 1e3
+    bytes_per_call = L * B * N * 4
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peak = int8_peak_tops(torch)
+    peak_src = "measured: torch._int_mm int8 8192^3 best of 10 on this GPU"
+    if peak is None:
+        peak = 2 * 1617.8
+        peak_src = "derived: 2 x MEASURED_PEAKS.json bf16_tflops (int8 dense = 2x bf16)"
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ntt_dram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as fh:
+                t = json.load(fh)
+            if t.get("batch") == B and t.get("limbs") == L:
+                traffic = t.get("bytes_per_launch_pair")
+        except Exception:
+            traffic = None
+    rates = cpu_oracle_rate(primes, args.cpu_members) if world == 1 and args.cpu_members > 0 \
+        else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"batched forward+inverse NTT, N=2^16, {PRESET} chain "
+                               f"({L} RNS limbs), batch {B} per GPU (BASELINE configs[1])",
+                   "N": N, "limbs": L, "batch_per_gpu": B, "plan": [n1, n2],
+                   "l2": f"inputs larger than L2 ({L * B * N * 4 / 2**30:.2f} GiB per buffer)",
+                   "parallelism": f"batch-sharded x{world}, no collective"},
+        "poly_ntt_kops": value / L,
+        "parity_spot_check": parity,
+        "roofline": {"bound": "tensor", "achieved": achieved_tops, "peak": peak,
+                     "unit": "TOPS (int8)", "frac": achieved_tops / peak, "traffic": traffic,
+                     "kernel": "ntt_ts_kernel (stage 1 + stage 2 per NTT call)",
+                     "algorithmic": f"32*N*(n1+n2) = {ops_per_limb/1e9:.3f} G int8-ops per "
+                                    f"limb-NTT x {L*B} limbs per call",
+                     "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * bytes_per_call,
+                "d2h_bytes_per_step": 2 * bytes_per_call, "steps": e2e_steps,
+                "api": "batched_apply(BatchBuffer(pinned host), 'ntt'/'intt')",
+                "roundtrip_exact": e2e_ok},
+        "gpu_launches": 4 * args.steps,
+        "clocks": clk.summary(),
+    }
+    if hm:
+        line["hmult_kops"] = hm["hmult_kops"]
+        line["hmult"] = {"workload": f"HMULT+relin (keyswitch ModUp/ModDown)+rescale, N=2^16, "
+                                     f"{PRESET} (L=44, K=1, dnum=45), batch {hm['batch_per_gpu']}"
+                                     " per GPU (BASELINE configs[2])",
+                         "ms_per_batch": hm["ms_per_batch"],
+                         "ops_per_s": hm["hmult_kops"] * 1e3}
+    if rates:
+        r, dt, threads = rates
+        line["cpu_baseline"] = {
+            "value": r / 1e3, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"C oracle (oracle/tfhe_oracle.c), fwd+inv over {L} limbs x "
+                      f"{args.cpu_members} members ({2 * L * args.cpu_members} limb-NTTs) "
+                      f"in {dt:.1f}s"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--hmult-batch", type=int, default=32)
+    ap.add_argument("--cpu-members", type=int, default=32)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -39,27 +39,47 @@ def _stream(device):
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+#: residency tags returned by to_device (host tags are truthy)
+ON_DEVICE, HOST_NUMPY, HOST_TORCH = "", "numpy", "torch"
+
+
 def to_device(x, device=None):
-    """numpy / torch (u32 or i32) -> contiguous int32 CUDA tensor; (tensor, was_host)."""
+    """numpy / torch (u32 or i32) -> (contiguous int32 CUDA tensor, residency tag).
+
+    Host torch tensors in pinned memory are copied asynchronously on the
+    current stream; numpy arrays go through a staging copy.
+    """
     device = device or default_device()
     if isinstance(x, torch.Tensor):
         if x.dtype == torch.uint32:
             x = x.view(torch.int32)
         elif x.dtype != torch.int32:
             x = x.to(torch.int64).to(torch.int32)
-        was_host = x.device.type != "cuda"
-        x = x.to(device, non_blocking=True).contiguous()
-        return x, was_host
-    a = np.ascontiguousarray(np.asarray(x).astype(np.uint32, copy=False))
-    return torch.from_numpy(a.view(np.int32)).to(device), True
+        tag = ON_DEVICE if x.device.type == "cuda" else HOST_TORCH
+        return x.to(device, non_blocking=True).contiguous(), tag
+    a = np.asarray(x)
+    if a.dtype != np.uint32:
+        a = a.astype(np.uint32)
+    a = np.ascontiguousarray(a)
+    if not a.flags.writeable:
+        a = a.copy()
+    return torch.from_numpy(a.view(np.int32)).to(device), HOST_NUMPY
 
 
 def to_host(t) -> np.ndarray:
     return t.detach().cpu().numpy().view(np.uint32)
 
 
-def like_input(t, was_host):
-    return to_host(t) if was_host else t
+def like_input(t, tag):
+    """Return a device result with the residency of the caller's input."""
+    if tag == HOST_NUMPY:
+        return to_host(t)
+    if tag == HOST_TORCH:
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t, non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        return out
+    return t
 
 
 class DeviceContext:

@@ -25,7 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import params as par
-from .device import DeviceContext, like_input, to_device
+from .device import HOST_NUMPY, DeviceContext, like_input, to_device
 from .errors import DomainError, ParameterError
 from .rns import COEFF, NTT, RnsPolynomial
 
@@ -102,9 +102,9 @@ def transform_rows(x, q, table, backend="segmented", inverse=False, workers=None
         raise ParameterError(f"row length {n} does not match table degree {table.n}")
     rows = t.reshape(1, -1, n)
     out = ctx.ntt(rows, [int(q)], inverse=inverse).reshape(shape)
-    if host:
+    if host == HOST_NUMPY:  # reference returns uint64 rows (ntt.py:351)
         return out.cpu().numpy().view(np.uint32).astype(np.uint64)
-    return out
+    return like_input(out, host)
 
 
 def _poly_transform(poly, table, inverse):
