@@ -75,7 +75,7 @@ inline int ext_prime(const CkksGeom& g, int r) { return r < g.l1 ? r : g.Lc + (r
 
 size_t ks_bytes(const CkksGeom& g, int batch, int n) {
   const size_t U = (size_t)batch * n * 4;
-  size_t rows = g.l1 /*y*/ + g.E /*raised*/ + 2 * g.E /*acc*/ +
+  size_t rows = g.l1 /*y*/ + 2 * g.E /*acc*/ +
                 std::max({g.E, 2 * g.l1, 2 * g.K}) /*ntt ws*/ + 2 * g.K /*ysp*/ +
                 (g.need_conv ? std::max(g.E, 2 * g.l1) : 0);
   return rows * U + 16 * 256;
@@ -123,7 +123,6 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
   const CkksGeom g = geom(h, level, dnum);
   const size_t U = (size_t)batch * c.n;  // elements per limb row
   uint32_t* y = cv.take<uint32_t>(g.l1 * U * 4);
-  uint32_t* raised = cv.take<uint32_t>(g.E * U * 4);
   uint32_t* acc = cv.take<uint32_t>(2 * g.E * U * 4);
   const int ntt_rows = std::max({g.E, 2 * g.l1, 2 * g.K});
   const size_t ntt_ws_bytes = ntt_rows * U * 4;
@@ -176,18 +175,25 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
     }
     // alpha = 1: fast_basis_conv is the identity on the slice's coefficients
     // (Q = q_lo, Q/q = 1), so the NTT reads y's row directly and reduces it
-    // mod each target prime inside the byte-sliced GEMM.
-    if ((rc = launch_ntt(c, ntt_in, raised, mu, batch, 0, nullptr, ntt_ws, ntt_ws_bytes, st)))
-      return rc;
-    // slice rows are reused unchanged (ckks.py:361-364)
-    if (cudaMemcpyAsync(raised + (size_t)lo * U, d + (size_t)lo * U, (hi - lo) * U * 4,
-                        cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
-      set_error("slice copy failed");
-      return TFHE_ECUDA;
-    }
+    // mod each target prime inside the byte-sliced GEMM.  The inner product
+    // acc += raised * key_j (ckks.py:345-351) is fused into the NTT's output
+    // epilogue: the raised limbs never touch HBM.
     const uint32_t* kb = key + (size_t)j * key_pair;
     const uint32_t* ka = kb + (size_t)(g.Lc + g.K) * c.n;
-    if ((rc = launch_ks_mac(c, raised, kb, ka, acc, acc + g.E * U, row_prime, key_row, g.E, batch,
+    EpiArgs ek;
+    memset(&ek, 0, sizeof(ek));
+    ek.mode = EPI_KS_MAC;
+    ek.kb = kb;
+    ek.ka = ka;
+    ek.acc_b = acc;
+    ek.acc_a = acc + g.E * U;
+    ek.first = first;
+    for (int l = 0; l < mu.n; ++l) ek.key_row[l] = (int16_t)key_row[mu.out_row[l]];
+    if ((rc = launch_ntt(c, ntt_in, nullptr, mu, batch, 0, &ek, ntt_ws, ntt_ws_bytes, st)))
+      return rc;
+    // slice rows are reused unchanged (ckks.py:361-364): MAC them straight from d
+    if ((rc = launch_ks_mac(c, d + (size_t)lo * U, kb, ka, acc + (size_t)lo * U,
+                            acc + (g.E + lo) * U, row_prime + lo, key_row + lo, hi - lo, batch,
                             first, st)))
       return rc;
     first = 0;
@@ -349,6 +355,7 @@ void tfhe_ctx_destroy(TfheCtx* h) {
     for (int s = 0; s < 2; ++s) {
       cudaFree(c.d_tw[i][s]);
       cudaFree(c.d_twa[i][s]);
+      if (i == 0 && s == 0) cudaFree(c.d_twa_ks);
     }
     cudaFree(c.d_w2[i]);
     cudaFree(c.d_w2s[i]);

@@ -189,6 +189,16 @@ __global__ void __launch_bounds__(kThreads, 1) ntt_stage_kernel(const __grid_con
           // out[n1*k2 + k1], k2 = col, k1 = x
           const size_t pos = (size_t)col * a.n1 + x;
           const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n;
+          if (a.epi.mode == EPI_KS_MAC) {
+            const size_t kr = (size_t)a.epi.key_row[limb] * a.n + pos;
+            const uint32_t tb = mul_mod(y, __ldg(a.epi.kb + kr), pc.q, pc.mu);
+            const uint32_t ta = mul_mod(y, __ldg(a.epi.ka + kr), pc.q, pc.mu);
+            uint32_t* ob = a.epi.acc_b + orow + pos;
+            uint32_t* oa = a.epi.acc_a + orow + pos;
+            *ob = a.epi.first ? tb : add_mod(*ob, tb, pc.q);
+            *oa = a.epi.first ? ta : add_mod(*oa, ta, pc.q);
+            continue;
+          }
           if (a.epi.mode == EPI_SUB_SCALE) {
             const uint32_t xv = a.epi.x[((size_t)a.epi.x_row[limb] * a.batch + b) * a.n + pos];
             y = mul_shoup(sub_mod(xv, y, pc.q), a.epi.s[limb], a.epi.s_shoup[limb], pc.q);

@@ -122,12 +122,20 @@ TFHE_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "me
 TFHE_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 TFHE_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-constexpr int kWarpStg = 3 * 2048;                // per epilogue warp: x | base | y rows
+constexpr int kWarpStg = 10 * 2048;               // per epilogue warp: in[2][4] | out[2] tiles
 constexpr int kStgBytes = 4 * kWarpStg;           // all 4 epilogue warps
 
 // 32 rows x 64 B staging, 16-byte chunks XOR-swizzled so both the row-wise
 // and the 4-lanes-per-row accesses are bank-conflict free
 TFHE_DEV uint32_t stg_off(int row, int q) { return (uint32_t)(row * 64 + 16 * (q ^ ((row >> 1) & 3))); }
+
+TFHE_DEV void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc)
+               : "memory");
+}
+TFHE_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+TFHE_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+TFHE_DEV void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 TFHE_DEV uint32_t mont_reduce(uint64_t v, const PrimeConst& pc) {
   const uint32_t mq = (uint32_t)v * pc.qneg_inv;
@@ -269,43 +277,79 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     const int m = wq * 32 + lane;          // TMEM lane = twiddle row within the half
     const int r_tw = h * 128 + m;          // global twiddle row (k1 or k2)
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    uint8_t* wstg = stg + wq * kWarpStg;   // this warp's staging (x | base | y)
-    // Operands that do not depend on the accumulators (W2 for stage 1; the
-    // x / base rows of the fused epilogue for stage 2) are prefetched one
-    // chunk ahead so their global latency overlaps the previous chunk.
-    const bool sub_scale = STAGE == 2 && a.epi.mode == EPI_SUB_SCALE;
+    uint8_t* wstg = stg + wq * kWarpStg;   // in[2][4] tiles | out[2] tiles (2 KB each)
+    const int mode = STAGE == 2 ? a.epi.mode : EPI_STORE;
+    // Stage-2 epilogue operands (x/base rows, key rows, accumulators) are
+    // fetched one chunk ahead with cp.async into a double-buffered staging
+    // area (4 lanes per 64-byte row = coalesced), stage 1's W2 with 16
+    // warp-coalesced loads into registers.
     uint32_t pf_w[16];
-    uint4 pf_x[4], pf_b[4];
-    bool pf_has_base = false;
-    auto prefetch = [&](const UnitIter& it) {
-      const int pr = a.map.prime[it.limb];
+    auto prefetch = [&](const UnitIter& it, int buf) {
       if (STAGE == 1) {
-        // W2 * R^2 in [prime][i2/16][e][k1] layout: 16 warp-coalesced loads
+        const int pr = a.map.prime[it.limb];
         const uint32_t* wp =
             a.w2 + ((size_t)pr * (a.n2 / kNC) + it.x0 / kNC) * kNC * a.n1 + r_tw;
 #pragma unroll
         for (int e = 0; e < 16; ++e) pf_w[e] = __ldg(wp + (size_t)e * a.n1);
-      } else if (sub_scale) {
-        // this warp's 32 output rows of x (and base), 4 lanes per 64-byte row
+        return;
+      }
+      const size_t wrow = (size_t)(h * 128 + wq * 32) * a.n1 + it.x0;  // warp's first row
+      const uint32_t* src[4] = {nullptr, nullptr, nullptr, nullptr};
+      if (mode == EPI_SUB_SCALE) {
+        src[0] = a.epi.x + ((size_t)a.epi.x_row[it.limb] * a.batch + it.b) * a.n + wrow;
         const int br = a.epi.base_row[it.limb];
-        pf_has_base = br >= 0;
-        const uint32_t* xb = a.epi.x + ((size_t)a.epi.x_row[it.limb] * a.batch + it.b) * a.n + it.x0;
-        const uint32_t* bb =
-            pf_has_base ? a.epi.base + ((size_t)br * a.batch + it.b) * a.n + it.x0 : xb;
+        if (br >= 0) src[1] = a.epi.base + ((size_t)br * a.batch + it.b) * a.n + wrow;
+      } else if (mode == EPI_KS_MAC) {
+        src[0] = a.epi.kb + (size_t)a.epi.key_row[it.limb] * a.n + wrow;
+        src[1] = a.epi.ka + (size_t)a.epi.key_row[it.limb] * a.n + wrow;
+        if (!a.epi.first) {
+          const size_t ar = ((size_t)a.map.out_row[it.limb] * a.batch + it.b) * a.n + wrow;
+          src[2] = a.epi.acc_b + ar;
+          src[3] = a.epi.acc_a + ar;
+        }
+      }
+      uint8_t* dstb = wstg + buf * 8192;
+#pragma unroll
+      for (int tI = 0; tI < 4; ++tI) {
+        if (!src[tI]) continue;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const size_t off = (size_t)(h * 128 + wq * 32 + 8 * q + (lane >> 2)) * a.n1 + 4 * (lane & 3);
-          pf_x[q] = __ldg(reinterpret_cast<const uint4*>(xb + off));
-          pf_b[q] = __ldg(reinterpret_cast<const uint4*>(bb + off));
+          const int r = 8 * q + (lane >> 2), p = lane & 3;
+          cp_async16(dstb + tI * 2048 + stg_off(r, p), src[tI] + (size_t)r * a.n1 + 4 * p);
         }
       }
     };
+    auto read_row = [&](int buf, int tI, uint32_t (&v)[16]) {
+      const uint8_t* t = wstg + buf * 8192 + tI * 2048;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u = *reinterpret_cast<const uint4*>(t + stg_off(lane, q));
+        v[4 * q] = u.x; v[4 * q + 1] = u.y; v[4 * q + 2] = u.z; v[4 * q + 3] = u.w;
+      }
+    };
+    // coalesced store of this warp's 32 rows x 16 values (row stride in elements)
+    auto store_tile = [&](int oI, const uint32_t (&v)[16], uint32_t* dst, size_t row_stride) {
+      uint8_t* t = wstg + 16384 + oI * 2048;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(t + stg_off(lane, q)) =
+            make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = 8 * q + (lane >> 2), p = lane & 3;
+        *reinterpret_cast<uint4*>(dst + (size_t)r * row_stride + 4 * p) =
+            *reinterpret_cast<const uint4*>(t + stg_off(r, p));
+      }
+    };
     UnitIter ahead = w;
-    if (cnt > 0) prefetch(ahead);
+    if (cnt > 0) prefetch(ahead, 0);
+    cp_async_commit();
     int prev = -1;
     for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
       const int limb = w.limb;
       const int prime = a.map.prime[limb];
+      const int buf = i & 1;
       if (limb != prev) {
         // load this (limb, half)'s twiddle planes into TMEM columns [0, K)
         prev = limb;
@@ -326,32 +370,17 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       }
       const PrimeConst pc = a.pc[prime];
       const int b = w.b;
-      uint32_t w2v[16], xrow[16], brow[16];
-      const bool has_base = pf_has_base;
+      uint32_t w2v[16];
       if (STAGE == 1) {
 #pragma unroll
         for (int e = 0; e < 16; ++e) w2v[e] = pf_w[e];
-      } else if (sub_scale) {
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int r = 8 * q + (lane >> 2), p = lane & 3;
-          *reinterpret_cast<uint4*>(wstg + stg_off(r, p)) = pf_x[q];
-          *reinterpret_cast<uint4*>(wstg + 2048 + stg_off(r, p)) = pf_b[q];
-        }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 v = *reinterpret_cast<const uint4*>(wstg + stg_off(lane, q));
-          xrow[4 * q] = v.x; xrow[4 * q + 1] = v.y; xrow[4 * q + 2] = v.z; xrow[4 * q + 3] = v.w;
-          uint4 u = *reinterpret_cast<const uint4*>(wstg + 2048 + stg_off(lane, q));
-          brow[4 * q] = u.x; brow[4 * q + 1] = u.y; brow[4 * q + 2] = u.z; brow[4 * q + 3] = u.w;
-        }
       }
+      __syncwarp();  // every lane is done with the staging buffer about to be refilled
       if (i + 1 < cnt) {
         ahead.next(C, logR, R);
-        prefetch(ahead);
+        prefetch(ahead, buf ^ 1);
       }
+      cp_async_commit();
       mbar_wait(&acc_full[w.ab], w.aph);
       tc_fence_after();
       uint32_t acc[7][16];
@@ -379,7 +408,42 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       if (STAGE == 1) {
 #pragma unroll
         for (int e = 0; e < 16; ++e) y[e] = mont_reduce((uint64_t)y[e] * w2v[e], pc);
-      } else if (sub_scale) {
+        // blocked P layout [limb][b][i2/16][k1][16]: the warp's rows are 2 KB contiguous
+        uint32_t* dst = a.out + (((size_t)limb * a.batch + b) * (a.n2 / kNC) + w.x0 / kNC) * kNC * a.n1 +
+                        (size_t)(h * 128 + wq * 32) * kNC;
+        store_tile(0, y, dst, kNC);
+        continue;
+      }
+      cp_async_wait1();   // this chunk's operand tiles have landed (own copies)
+      __syncwarp();       // ... and every lane's copies are visible
+      const size_t wrow = (size_t)(h * 128 + wq * 32) * a.n1 + w.x0;
+      if (mode == EPI_KS_MAC) {
+        // y is in Montgomery form (y R: twiddles carry R^2), so one Montgomery
+        // product per key gives y * k exactly
+        uint32_t kb[16], ka[16], ob[16], oa[16];
+        read_row(buf, 0, kb);
+        read_row(buf, 1, ka);
+        if (!a.epi.first) {
+          read_row(buf, 2, ob);
+          read_row(buf, 3, oa);
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const uint32_t tb = mont_reduce((uint64_t)y[e] * kb[e], pc);
+          const uint32_t ta = mont_reduce((uint64_t)y[e] * ka[e], pc);
+          ob[e] = a.epi.first ? tb : add_mod(ob[e], tb, pc.q);
+          oa[e] = a.epi.first ? ta : add_mod(oa[e], ta, pc.q);
+        }
+        const size_t ar = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n + wrow;
+        store_tile(0, ob, a.epi.acc_b + ar, a.n1);
+        store_tile(1, oa, a.epi.acc_a + ar, a.n1);
+        continue;
+      }
+      if (mode == EPI_SUB_SCALE) {
+        uint32_t xrow[16], brow[16];
+        read_row(buf, 0, xrow);
+        const bool has_base = a.epi.base_row[limb] >= 0;
+        if (has_base) read_row(buf, 1, brow);
         const uint32_t s = a.epi.s[limb], sp = a.epi.s_shoup[limb];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
@@ -387,33 +451,9 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
           y[e] = has_base ? add_mod(brow[e], t, pc.q) : t;
         }
       }
-      // ---- store: transpose the warp's 32 x 64-byte rows through smem so
-      // every global store instruction writes 4 lanes per 64-byte row
-      __syncwarp();
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<uint4*>(wstg + 4096 + stg_off(lane, q)) =
-            make_uint4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
-      __syncwarp();
-      uint32_t* dst;
-      size_t row_stride;
-      if (STAGE == 1) {
-        // blocked P layout [limb][b][i2/16][k1][16]: the warp's rows are 2 KB contiguous
-        dst = a.out + (((size_t)limb * a.batch + b) * (a.n2 / kNC) + w.x0 / kNC) * kNC * a.n1 +
-              (size_t)(h * 128 + wq * 32) * kNC;
-        row_stride = kNC;
-      } else {
-        dst = a.out + ((size_t)a.map.out_row[limb] * a.batch + b) * a.n +
-              (size_t)(h * 128 + wq * 32) * a.n1 + w.x0;
-        row_stride = a.n1;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = 8 * q + (lane >> 2), p = lane & 3;
-        *reinterpret_cast<uint4*>(dst + (size_t)r * row_stride + 4 * p) =
-            *reinterpret_cast<const uint4*>(wstg + 4096 + stg_off(r, p));
-      }
+      store_tile(0, y, a.out + ((size_t)a.map.out_row[limb] * a.batch + b) * a.n + wrow, a.n1);
     }
+    cp_async_wait0();
   } else {
     // ---------------------------------------------------------------- MMA issuer
     // The whole warp walks the loop (so descriptors stay warp-uniform and live
@@ -516,8 +556,11 @@ int build_ts_tables(Ctx& c) {
   const int n = c.n, n1 = c.n1, n2 = c.n2, np = c.n_primes;
   const uint64_t two_n = 2ull * n;
   std::vector<uint32_t> pw(two_n);
-  for (int inv = 0; inv < 2; ++inv)
-    for (int s = 0; s < 2; ++s) {
+  // variants 0..3: (inv, stage) = (v>>1, v&1); variant 4: forward stage 2
+  // scaled by R^2 for the fused key-switch MAC epilogue
+  for (int var = 0; var < 5; ++var) {
+      const int inv = var < 4 ? var >> 1 : 0, s = var < 4 ? var & 1 : 1;
+      const bool ks = var == 4;
       const int ntw = s == 0 ? n1 : n2, K = ntw, H = ntw / 128;
       std::vector<uint32_t> tw((size_t)np * ntw * K);  // K words per row (4 planes x K/4)
       for (int p = 0; p < np; ++p) {
@@ -542,6 +585,7 @@ int build_ts_tables(Ctx& c) {
               if (s == 1 && inv) v = mulmod_h(v, n_inv, q);
               // stage 2 twiddles carry R = 2^32: the Montgomery epilogue divides it out
               if (s == 1) v = (uint32_t)(((uint64_t)v << 32) % q);
+              if (ks) v = (uint32_t)(((uint64_t)v << 32) % q);
               for (int i = 0; i < 4; ++i) words[i] |= ((v >> (8 * i)) & 0xFFu) << (8 * e);
             }
             for (int i = 0; i < 4; ++i) row[i * (K / 4) + kq] = words[i];
@@ -549,12 +593,13 @@ int build_ts_tables(Ctx& c) {
         }
       }
       const size_t bytes = tw.size() * 4;
-      if (cudaMalloc(&c.d_twa[inv][s], bytes) != cudaSuccess ||
-          cudaMemcpy(c.d_twa[inv][s], tw.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+      uint32_t** dst = ks ? &c.d_twa_ks : &c.d_twa[inv][s];
+      if (cudaMalloc(dst, bytes) != cudaSuccess ||
+          cudaMemcpy(*dst, tw.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
         set_error("ts twiddle upload failed");
         return 3;
       }
-    }
+  }
   // W2 * R^2 mod q in [prime][i2/16][e][k1] layout: stage 1 multiplies its
   // Montgomery result (S R^-1) by this with another Montgomery step -> S * W2;
   // the layout makes the epilogue's per-row loads warp-coalesced
@@ -611,7 +656,11 @@ int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap
   // stage 2: rows k2 (n2 twiddle rows), data columns (b, k1)
   a.in = P;
   a.out = out;
-  a.twa = c.d_twa[inverse][1];
+  a.twa = (epi && epi->mode == EPI_KS_MAC) ? c.d_twa_ks : c.d_twa[inverse][1];
+  if (epi && epi->mode == EPI_KS_MAC && inverse) {
+    set_error("fused key-switch MAC needs a forward transform");
+    return 2;
+  }
   a.R = c.n1;
   a.H = c.n2 / 128;
   a.C = batch * c.n1 / kNC;

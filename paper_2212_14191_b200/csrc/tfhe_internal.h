@@ -36,6 +36,9 @@ struct LimbMap {
 enum EpiMode : int {
   EPI_STORE = 0,       // out = NTT(in)
   EPI_SUB_SCALE = 1,   // out = (x - NTT(in)) * s  [+ base]   (ModDown, rescale)
+  EPI_KS_MAC = 2,      // acc_b (+)= NTT(in) * kb[key_row], acc_a (+)= NTT(in) * ka[key_row]
+                       // (key-switch inner product fused into ModUp, ckks.py:345-351);
+                       // acc rows = out_row[l]; `first` overwrites instead of adding
 };
 
 struct EpiArgs {
@@ -46,6 +49,13 @@ struct EpiArgs {
   int16_t base_row[kMaxLimbs];
   uint32_t s[kMaxLimbs];        // per-limb scale
   uint32_t s_shoup[kMaxLimbs];
+  // EPI_KS_MAC
+  const uint32_t* kb;     // (key_rows, n) NTT-domain key rows, shared by the batch
+  const uint32_t* ka;
+  uint32_t* acc_b;        // (acc_rows, batch, n)
+  uint32_t* acc_a;
+  int16_t key_row[kMaxLimbs];
+  int first;
 };
 
 struct Ctx {
@@ -66,6 +76,9 @@ struct Ctx {
   // stage-1 hadamard twiddles pre-scaled by R = 2^32 (Montgomery epilogue), + Shoup
   uint32_t* d_w2r[2] = {nullptr, nullptr};
   uint32_t* d_w2rs[2] = {nullptr, nullptr};
+  // forward stage-2 twiddle planes scaled by R^2 (not R): the stage-2 result
+  // is then y*R, the Montgomery form the fused key-switch MAC multiplies with
+  uint32_t* d_twa_ks = nullptr;
   bool use_ts = false;
   int sms = 148;
   std::vector<PrimeConst> h_pc;
