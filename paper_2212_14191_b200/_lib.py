@@ -14,7 +14,9 @@ import subprocess
 from .errors import DeviceError, ParameterError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtfhe_b200.so")
+#: in-tree build; TFHE_B200_LIB may point at another build of the same ABI
+#: (A/B performance experiments)
+LIB_PATH = os.environ.get("TFHE_B200_LIB") or os.path.join(_HERE, "libtfhe_b200.so")
 ABI_VERSION = 1
 
 EINVAL = 2

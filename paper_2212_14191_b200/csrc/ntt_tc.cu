@@ -399,7 +399,9 @@ int build_ntt_tables(Ctx& c) {
   cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
   if (c.sms <= 0) c.sms = 148;
   // twiddle-resident tensor-core path for n1, n2 in {128, 256}
-  c.use_ts = c.n1 >= 128 && c.n2 <= 256;
+  // (its single-correction Montgomery epilogue needs q > 2^20; see ntt_ts.cu)
+  c.use_ts = c.n1 >= 128 && c.n2 <= 256 &&
+             *std::min_element(c.primes.begin(), c.primes.end()) > (1u << 20);
   if (c.use_ts) return build_ts_tables(c);
   return 0;
 }

@@ -27,6 +27,7 @@
 // (one CTA per SM); with two 128-row halves the CTAs run in pairs over the
 // same data range so the second read of each data chunk hits L2.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -39,8 +40,19 @@ namespace {
 
 constexpr int kNC = 16;                  // data columns per chunk
 constexpr int kRing = 6;                 // smem ring depth (chunks)
-constexpr int kThreadsTS = 288;          // 4 producer + 4 epilogue + 1 MMA warp
+// 3 warpgroups: producers (warps 0-3), epilogue (4-7), MMA issuer (warp 8;
+// warps 9-11 idle).  Registers are rebalanced with setmaxnreg: each SMSP
+// holds one warp of every warpgroup, so 144 + 256 + 88 <= 512 per lane.
+constexpr int kThreadsTS = 384;
+constexpr int kRegsProducer = 144, kRegsEpilogue = 256, kRegsMma = 88;
 constexpr uint32_t kAccCol0 = 256, kAccCol1 = 384;
+// Performance-experiment knobs (env TFHE_DBG) exist only in builds with
+// -DTFHE_TS_DBG; normal builds compile them away.
+#ifdef TFHE_TS_DBG
+#define kDbg (a.dbg)
+#else
+#define kDbg 0
+#endif
 
 struct TsArgs {
   const uint32_t* in;
@@ -54,6 +66,8 @@ struct TsArgs {
   int H;      // 128-row twiddle halves
   int C;      // chunks per limb
   int n_limbs;
+  int dbg;    // perf experiments only (env TFHE_DBG): 1 = producers skip global loads,
+              // 2 = epilogue skips math/stores; results are garbage when set
   LimbMap map;
   EpiArgs epi;
 };
@@ -143,7 +157,7 @@ TFHE_DEV uint32_t mont_reduce(uint64_t v, const PrimeConst& pc) {
   return t >= pc.q ? t - pc.q : t;
 }
 
-template <int STAGE, int K>
+template <int STAGE, int K, int MODE>
 __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_constant__ TsArgs a) {
   constexpr int kStageBytes = ring_stage_bytes<K>();
   constexpr int KC = K / 32;
@@ -192,8 +206,11 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
   const uint32_t tmem = *tmem_slot;
   UnitIter w;
   w.init(u0, C, logR, R);
-
+  // Each role's register budget is set at the top of its own branch so that
+  // ptxas allocates every role's code under the matching setmaxnreg limit.
   if (warp < 4) {
+    reg_dealloc<kRegsProducer>();
+    if (kDbg & 4) goto role_done;
     // ---------------------------------------------------------------- producers
     // Stage 1 (X_b[k][x0 + c], columns contiguous): B' is stored MN-major --
     // each thread loads 16 B (4 columns of one k row) and writes one 4-byte
@@ -239,11 +256,13 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       for (int e = 0; e < kVals; ++e) cur[e] = nxt[e];
       if (i + 1 < cnt) {
         ahead.next(C, logR, R);
-        load_chunk(ahead, nxt);
+        if (!(kDbg & 1)) load_chunk(ahead, nxt);
       }
       if (i >= kRing) mbar_wait(&b_empty[w.s], w.rph ^ 1);
       uint8_t* st = smem + w.s * kStageBytes;
-      if (STAGE == 1) {
+      if (kDbg & 16) {
+        // handshake-only experiment
+      } else if (STAGE == 1) {
 #pragma unroll
         for (int m = 0; m < K / 32; ++m) {
           const int k = krow0 + 32 * m;
@@ -268,29 +287,36 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
                 make_uint4(pw[0][j], pw[1][j], pw[2][j], pw[3][j]);
         }
       }
-      fence_proxy_async_smem();
+      if (!(kDbg & 32)) fence_proxy_async_smem();
       mbar_arrive(&b_full[w.s]);
     }
   } else if (warp < 8) {
+    reg_alloc<kRegsEpilogue>();
+    if (kDbg & 4) goto role_done;
     // ---------------------------------------------------------------- epilogue
     const int wq = warp & 3;
     const int m = wq * 32 + lane;          // TMEM lane = twiddle row within the half
     const int r_tw = h * 128 + m;          // global twiddle row (k1 or k2)
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     uint8_t* wstg = stg + wq * kWarpStg;   // in[2][4] tiles | out[2] tiles (2 KB each)
-    const int mode = STAGE == 2 ? a.epi.mode : EPI_STORE;
+    constexpr int mode = STAGE == 2 ? MODE : EPI_STORE;
     // Stage-2 epilogue operands (x/base rows, key rows, accumulators) are
     // fetched one chunk ahead with cp.async into a double-buffered staging
     // area (4 lanes per 64-byte row = coalesced), stage 1's W2 with 16
     // warp-coalesced loads into registers.
-    uint32_t pf_w[16];
     auto prefetch = [&](const UnitIter& it, int buf) {
       if (STAGE == 1) {
+        // W2 * R^2 in [prime][i2][k1] layout: for each of the chunk's 16 i2
+        // columns the warp's 32 k1 rows are 128 contiguous bytes -> staged as
+        // [16][32] words (one 16-byte cp.async per lane per 512 bytes)
         const int pr = a.map.prime[it.limb];
-        const uint32_t* wp =
-            a.w2 + ((size_t)pr * (a.n2 / kNC) + it.x0 / kNC) * kNC * a.n1 + r_tw;
+        const uint32_t* wp = a.w2 + (size_t)pr * a.n + (size_t)it.x0 * a.n1 + h * 128 + wq * 32;
+        uint8_t* dstb = wstg + buf * 8192;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) pf_w[e] = __ldg(wp + (size_t)e * a.n1);
+        for (int q = 0; q < 4; ++q) {
+          const int idx = q * 32 + lane, e = idx >> 3, part = idx & 7;
+          cp_async16(dstb + e * 128 + part * 16, wp + (size_t)e * a.n1 + part * 4);
+        }
         return;
       }
       const size_t wrow = (size_t)(h * 128 + wq * 32) * a.n1 + it.x0;  // warp's first row
@@ -370,11 +396,6 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       }
       const PrimeConst pc = a.pc[prime];
       const int b = w.b;
-      uint32_t w2v[16];
-      if (STAGE == 1) {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) w2v[e] = pf_w[e];
-      }
       __syncwarp();  // every lane is done with the staging buffer about to be refilled
       if (i + 1 < cnt) {
         ahead.next(C, logR, R);
@@ -383,39 +404,52 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       cp_async_commit();
       mbar_wait(&acc_full[w.ab], w.aph);
       tc_fence_after();
-      uint32_t acc[7][16];
+      // all 7 x 16 accumulators are read back-to-back and the TMEM buffer is
+      // released before any math (the MMA of chunk i+2 waits on it)
       const uint32_t abase = tmem + lane_off + (w.ab ? kAccCol1 : kAccCol0);
+      uint32_t acc[7][16];
+      if (!(kDbg & 8)) {
 #pragma unroll
-      for (int s = 0; s < 7; ++s) tmem_ld16(abase + 16 * s, acc[s]);
-      tmem_ld_wait();
+        for (int s = 0; s < 7; ++s) tmem_ld16(abase + 16 * s, acc[s]);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int s = 0; s < 7; ++s)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) acc[s][e] = s + e;
+      }
       tc_fence_before();
       mbar_arrive(&acc_empty[w.ab]);
-
       uint32_t y[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        // x = sum_s C_s 2^(8s) mod-q weights (< 2^60), then one Montgomery
-        // step: y = x R^-1 mod q (R = 2^32; the twiddles carry the R back)
-        uint64_t v = (uint64_t)acc[0][e];
-        v += (uint64_t)acc[1][e] * 256u;
-        v += (uint64_t)acc[2][e] * 65536u;
-        v += (uint64_t)acc[3][e] * pc.w3;
+        // x = sum_s C_s 2^(8s) (powers of two up to 2^24 as shifts, 2^(8s)
+        // mod q for s >= 4) < 2^60, then one Montgomery step:
+        // y = x R^-1 mod q (R = 2^32; the twiddles carry the R back)
+        uint64_t v = (uint64_t)acc[0][e] + ((uint64_t)acc[1][e] << 8) +
+                     ((uint64_t)acc[2][e] << 16) + ((uint64_t)acc[3][e] << 24);
         v += (uint64_t)acc[4][e] * pc.r[0];
         v += (uint64_t)acc[5][e] * pc.r[1];
         v += (uint64_t)acc[6][e] * pc.r[2];
         y[e] = mont_reduce(v, pc);
       }
+      if (kDbg & 2) {
+        if (y[0] == 0x7fffffff && y[15] == 1) a.out[0] = 0;  // keep the work live
+        continue;
+      }
+      cp_async_wait1();   // this chunk's operand tiles have landed (own copies)
+      __syncwarp();       // ... and every lane's copies are visible
       if (STAGE == 1) {
+        const uint8_t* wt = wstg + buf * 8192;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) y[e] = mont_reduce((uint64_t)y[e] * w2v[e], pc);
+        for (int e = 0; e < 16; ++e)
+          y[e] = mont_reduce((uint64_t)y[e] * *reinterpret_cast<const uint32_t*>(wt + e * 128 + lane * 4), pc);
         // blocked P layout [limb][b][i2/16][k1][16]: the warp's rows are 2 KB contiguous
         uint32_t* dst = a.out + (((size_t)limb * a.batch + b) * (a.n2 / kNC) + w.x0 / kNC) * kNC * a.n1 +
                         (size_t)(h * 128 + wq * 32) * kNC;
         store_tile(0, y, dst, kNC);
         continue;
       }
-      cp_async_wait1();   // this chunk's operand tiles have landed (own copies)
-      __syncwarp();       // ... and every lane's copies are visible
       const size_t wrow = (size_t)(h * 128 + wq * 32) * a.n1 + w.x0;
       if (mode == EPI_KS_MAC) {
         // y is in Montgomery form (y R: twiddles carry R^2), so one Montgomery
@@ -455,6 +489,8 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     }
     cp_async_wait0();
   } else {
+    reg_dealloc<kRegsMma>();
+    if (warp != 8) goto role_done;
     // ---------------------------------------------------------------- MMA issuer
     // The whole warp walks the loop (so descriptors stay warp-uniform and live
     // in uniform registers); one elected lane issues the tcgen05 ops.
@@ -464,22 +500,15 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
                        id16 = idesc_i8(128, 16) | bmaj;
     constexpr uint32_t kLbo = STAGE == 1 ? 128 : 1024, kSbo = STAGE == 1 ? 512 : 128;
     constexpr uint32_t kPlane3 = STAGE == 1 ? 3 * 512 : 6 * 128;  // start of B' plane 3
-    int prev = -1;
-    uint32_t twph = 0;
-    for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
-      if (w.limb != prev) {
-        if (prev >= 0) twph ^= 1;
-        prev = w.limb;
-        mbar_wait(tw_full, twph);
-      }
-      mbar_wait(&b_full[w.s], w.rph);
-      if (i >= 2) mbar_wait(&acc_empty[w.ab], w.aph ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem + (w.ab ? kAccCol1 : kAccCol0);
-      const uint32_t sb = smem_u32(smem + w.s * kStageBytes);
-      if (elect_one()) {
+    // The epilogue may only overwrite the twiddle (limb change) once every
+    // MMA of the previous limb has completed: tw_full is waited per limb.
+    const bool handshake = !(kDbg & 4);
+    auto issue = [&](const UnitIter& it, int kc0, int kc1) {
+      const uint32_t d = tmem + (it.ab ? kAccCol1 : kAccCol0);
+      const uint32_t sb = smem_u32(smem + it.s * kStageBytes);
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) {
+        if (kc < kc0 || kc >= kc1) continue;
         const uint32_t bt = sb + kc * 2048;
         const uint64_t bd = smem_desc_kmajor(bt, kLbo, kSbo);
         const uint32_t a0 = tmem + 0 * (K / 4) + kc * 8, a1 = tmem + 1 * (K / 4) + kc * 8;
@@ -497,13 +526,35 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
           mma_i8_ts(d + 48, a3, bd, id64, 1);
         }
       }
-      mma_commit(&b_empty[w.s]);
-      mma_commit(&acc_full[w.ab]);
+    };
+    // data / accumulator readiness of chunk `it` (index i)
+    auto wait_ready = [&](const UnitIter& it, int i) {
+      if (!handshake) return;
+      mbar_wait(&b_full[it.s], it.rph);
+      if (i >= 2) mbar_wait(&acc_empty[it.ab], it.aph ^ 1);
+    };
+    int prev = -1;
+    uint32_t twph = 0;
+    for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
+      if (w.limb != prev) {
+        if (handshake) {
+          if (prev >= 0) twph ^= 1;
+          mbar_wait(tw_full, twph);
+        }
+        prev = w.limb;
+      }
+      wait_ready(w, i);
+      tc_fence_after();
+      if (elect_one()) {
+        issue(w, 0, KC);
+        mma_commit(&b_empty[w.s]);
+        mma_commit(&acc_full[w.ab]);
       }
       __syncwarp();
     }
   }
 
+role_done:
   tc_fence_before();
   __syncthreads();
   if (warp == 8) {
@@ -512,10 +563,10 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
   }
 }
 
-template <int STAGE, int K>
+template <int STAGE, int K, int MODE>
 int launch_ts(const Ctx& c, TsArgs& a, cudaStream_t st) {
   const int smem = kRing * ring_stage_bytes<K>() + kStgBytes + (2 * kRing + 5) * 8 + 16;
-  auto kern = ntt_ts_kernel<STAGE, K>;
+  auto kern = ntt_ts_kernel<STAGE, K, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const long long U = (long long)a.n_limbs * a.C;
   int grid;
@@ -533,8 +584,18 @@ int launch_ts(const Ctx& c, TsArgs& a, cudaStream_t st) {
 
 template <int STAGE>
 int launch_ts_k(const Ctx& c, int K, TsArgs& a, cudaStream_t st) {
-  if (K == 256) return launch_ts<STAGE, 256>(c, a, st);
-  if (K == 128) return launch_ts<STAGE, 128>(c, a, st);
+  const int mode = STAGE == 2 ? a.epi.mode : EPI_STORE;
+#define TFHE_TS_CASE(KK, MM) \
+  if (K == KK && mode == MM) return launch_ts<STAGE, KK, (STAGE == 2 ? MM : EPI_STORE)>(c, a, st);
+  TFHE_TS_CASE(256, EPI_STORE)
+  TFHE_TS_CASE(128, EPI_STORE)
+  if (STAGE == 2) {
+    TFHE_TS_CASE(256, EPI_SUB_SCALE)
+    TFHE_TS_CASE(128, EPI_SUB_SCALE)
+    TFHE_TS_CASE(256, EPI_KS_MAC)
+    TFHE_TS_CASE(128, EPI_KS_MAC)
+  }
+#undef TFHE_TS_CASE
   set_error("ts kernel: unsupported contraction length");
   return 2;
 }
@@ -638,6 +699,8 @@ int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap
   a.n2 = c.n2;
   a.batch = batch;
   a.n_limbs = map.n;
+  static const int dbg = getenv("TFHE_DBG") ? atoi(getenv("TFHE_DBG")) : 0;
+  a.dbg = dbg;  // (only read when built with -DTFHE_TS_DBG)
   a.map = map;
   if (epi) a.epi = *epi;
   else a.epi.mode = EPI_STORE;
