@@ -57,6 +57,8 @@ struct Carve {
 struct CkksGeom {
   int Lc, K, alpha, l1, E;
   bool need_conv;
+  int nslices;   // non-empty GKS slices at this level
+  int S;         // slices per fused key-switch group (TS path), 1 otherwise
 };
 
 CkksGeom geom(const TfheCtx* h, int level, int dnum) {
@@ -67,17 +69,34 @@ CkksGeom geom(const TfheCtx* h, int level, int dnum) {
   g.l1 = level + 1;
   g.E = g.l1 + g.K;
   g.need_conv = g.alpha > 1 || g.K > 1;
+  g.nslices = (g.l1 + g.alpha - 1) / g.alpha;
+  g.S = 1;
   return g;
+}
+
+// slices per key-switch group: bounded by the launch limb map and by an
+// 8 GiB cap on the (S * E, batch, n) stage-1 workspace
+void set_group(CkksGeom& g, const Ctx& c, int batch) {
+  if (!c.use_ts) {
+    g.S = 1;
+    return;
+  }
+  const size_t row_bytes = (size_t)batch * c.n * 4;
+  const size_t cap = (size_t)8 << 30;
+  int s_mem = (int)std::max<size_t>(1, cap / (row_bytes * g.E));
+  g.S = std::max(1, std::min({g.nslices, kMaxLimbs / g.E, s_mem}));
 }
 
 // prime index of extended-basis position r at level (chain 0..level, then specials)
 inline int ext_prime(const CkksGeom& g, int r) { return r < g.l1 ? r : g.Lc + (r - g.l1); }
 
+int ks_ntt_rows(const CkksGeom& g) { return std::max({g.S * g.E, g.E, 2 * g.l1, 2 * g.K}); }
+int ks_conv_rows(const CkksGeom& g) { return std::max({g.S * g.E, g.E, 2 * g.l1}); }
+
 size_t ks_bytes(const CkksGeom& g, int batch, int n) {
   const size_t U = (size_t)batch * n * 4;
-  size_t rows = g.l1 /*y*/ + 2 * g.E /*acc*/ +
-                std::max({g.E, 2 * g.l1, 2 * g.K}) /*ntt ws*/ + 2 * g.K /*ysp*/ +
-                (g.need_conv ? std::max(g.E, 2 * g.l1) : 0);
+  size_t rows = g.l1 /*y*/ + 2 * g.E /*acc*/ + ks_ntt_rows(g) /*ntt ws*/ + 2 * g.K /*ysp*/ +
+                (g.need_conv ? ks_conv_rows(g) : 0);
   return rows * U + 16 * 256;
 }
 
@@ -120,15 +139,15 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
                    int dnum, uint32_t* out, const uint32_t* base, const int16_t* base_rows,
                    Carve& cv, cudaStream_t st) {
   const Ctx& c = h->c;
-  const CkksGeom g = geom(h, level, dnum);
+  CkksGeom g = geom(h, level, dnum);
+  set_group(g, c, batch);
   const size_t U = (size_t)batch * c.n;  // elements per limb row
   uint32_t* y = cv.take<uint32_t>(g.l1 * U * 4);
   uint32_t* acc = cv.take<uint32_t>(2 * g.E * U * 4);
-  const int ntt_rows = std::max({g.E, 2 * g.l1, 2 * g.K});
-  const size_t ntt_ws_bytes = ntt_rows * U * 4;
+  const size_t ntt_ws_bytes = ks_ntt_rows(g) * U * 4;
   uint32_t* ntt_ws = cv.take<uint32_t>(ntt_ws_bytes);
   uint32_t* ysp = cv.take<uint32_t>(2 * g.K * U * 4);
-  uint32_t* conv = g.need_conv ? cv.take<uint32_t>(std::max(g.E, 2 * g.l1) * U * 4) : nullptr;
+  uint32_t* conv = g.need_conv ? cv.take<uint32_t>(ks_conv_rows(g) * U * 4) : nullptr;
   if (!cv.ok) {
     set_error("ckks workspace too small");
     return TFHE_EINVAL;
@@ -142,61 +161,126 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
   for (int r = 0; r < g.l1; ++r) m.prime[r] = m.in_row[r] = m.out_row[r] = (int16_t)r;
   if ((rc = launch_ntt(c, d, y, m, batch, 1, nullptr, ntt_ws, ntt_ws_bytes, st))) return rc;
 
-  // 2. per GKS slice: ModUp + inner product  (ckks.py:337-351)
+  // 2. ModUp + inner product  (ckks.py:337-351)
   int16_t row_prime[kMaxRows];
   int32_t key_row[kMaxRows];
   for (int r = 0; r < g.E; ++r) {
     row_prime[r] = (int16_t)ext_prime(g, r);
     key_row[r] = ext_prime(g, r);  // key rows are over the full ext basis
   }
-  int first = 1;
-  for (int j = 0; j < dnum; ++j) {
-    const int lo = j * g.alpha;
-    if (lo > level) break;
-    const int hi = std::min((j + 1) * g.alpha, g.l1);
-    LimbMap mu;
-    mu.n = 0;
-    std::vector<int> src, dst;
-    for (int s = lo; s < hi; ++s) src.push_back(s);
-    for (int r = 0; r < g.E; ++r) {
-      if (r >= lo && r < hi) continue;
-      mu.prime[mu.n] = (int16_t)ext_prime(g, r);
-      mu.out_row[mu.n] = (int16_t)r;
-      mu.in_row[mu.n] = (int16_t)(hi - lo == 1 ? lo : mu.n);
-      dst.push_back(ext_prime(g, r));
-      ++mu.n;
-    }
-    const uint32_t* ntt_in = y;
-    if (hi - lo > 1) {
-      BconvArgs ba;
-      if ((rc = fill_bconv(c, src, dst, ba))) return rc;
-      if ((rc = launch_bconv(c, y + (size_t)lo * U, conv, ba, batch, st))) return rc;
-      ntt_in = conv;
-    }
-    // alpha = 1: fast_basis_conv is the identity on the slice's coefficients
-    // (Q = q_lo, Q/q = 1), so the NTT reads y's row directly and reduces it
-    // mod each target prime inside the byte-sliced GEMM.  The inner product
-    // acc += raised * key_j (ckks.py:345-351) is fused into the NTT's output
-    // epilogue: the raised limbs never touch HBM.
-    const uint32_t* kb = key + (size_t)j * key_pair;
-    const uint32_t* ka = kb + (size_t)(g.Lc + g.K) * c.n;
+  if (c.use_ts) {
+    // 2a. slice rows are reused unchanged (ckks.py:361-364): acc[r] = d_r * k_{slice(r)}[r]
+    int64_t key_off[kMaxRows];
+    for (int r = 0; r < g.l1; ++r) key_off[r] = (int64_t)(r / g.alpha) * key_pair + (int64_t)r * c.n;
+    if ((rc = launch_ks_mac(c, d, key, key + key_pair / 2, acc, acc + g.E * U, row_prime, key_off,
+                            g.l1, batch, 1, st)))
+      return rc;
+    // 2b. groups of S slices: stage 1 for every (slice, target) pair, stage 2
+    // accumulates the S slices of each target on chip (EPI_KS_ACC).  Targets
+    // are all E extended rows; a slice's own rows are skipped in the sum.
+    LimbMap tmap;
+    tmap.n = g.E;
     EpiArgs ek;
     memset(&ek, 0, sizeof(ek));
-    ek.mode = EPI_KS_MAC;
-    ek.kb = kb;
-    ek.ka = ka;
+    ek.mode = EPI_KS_ACC;
+    ek.key = key;
+    ek.key_pair = (long long)key_pair;
     ek.acc_b = acc;
     ek.acc_a = acc + g.E * U;
-    ek.first = first;
-    for (int l = 0; l < mu.n; ++l) ek.key_row[l] = (int16_t)key_row[mu.out_row[l]];
-    if ((rc = launch_ntt(c, ntt_in, nullptr, mu, batch, 0, &ek, ntt_ws, ntt_ws_bytes, st)))
-      return rc;
-    // slice rows are reused unchanged (ckks.py:361-364): MAC them straight from d
-    if ((rc = launch_ks_mac(c, d + (size_t)lo * U, kb, ka, acc + (size_t)lo * U,
-                            acc + (g.E + lo) * U, row_prime + lo, key_row + lo, hi - lo, batch,
-                            first, st)))
-      return rc;
-    first = 0;
+    for (int t = 0; t < g.E; ++t) {
+      tmap.prime[t] = (int16_t)ext_prime(g, t);
+      tmap.in_row[t] = (int16_t)t;
+      tmap.out_row[t] = (int16_t)t;
+      ek.key_row[t] = (int16_t)key_row[t];
+      ek.js[t] = (int16_t)(t < g.l1 ? t / g.alpha : -1);
+      ek.init_acc[t] = (int16_t)(t < g.l1);  // specials start from zero
+    }
+    for (int j0 = 0; j0 < g.nslices; j0 += g.S) {
+      const int S = std::min(g.S, g.nslices - j0);
+      LimbMap s1;
+      s1.n = S * g.E;
+      const uint32_t* ntt_in = y;
+      for (int sl = 0; sl < S; ++sl) {
+        const int j = j0 + sl, lo = j * g.alpha, hi = std::min(lo + g.alpha, g.l1);
+        if (hi - lo > 1) {
+          // alpha > 1: fast_basis_conv of the slice to every extended prime
+          // (slice primes are copied through) into conv rows [sl*E, sl*E+E)
+          std::vector<int> src, dst;
+          for (int q = lo; q < hi; ++q) src.push_back(q);
+          for (int t = 0; t < g.E; ++t) dst.push_back(ext_prime(g, t));
+          BconvArgs ba;
+          if ((rc = fill_bconv(c, src, dst, ba))) return rc;
+          if ((rc = launch_bconv(c, y + (size_t)lo * U, conv + (size_t)sl * g.E * U, ba, batch,
+                                 st)))
+            return rc;
+          ntt_in = conv;
+        }
+        for (int t = 0; t < g.E; ++t) {
+          const int l = sl * g.E + t;
+          s1.prime[l] = (int16_t)ext_prime(g, t);
+          // alpha = 1: fast_basis_conv is the identity on the slice's
+          // coefficients (Q = q_lo, Q/q = 1): the NTT reads y's row directly
+          // and reduces it mod each target prime inside the byte-sliced GEMM
+          s1.in_row[l] = (int16_t)(hi - lo > 1 ? l : lo);
+          s1.out_row[l] = (int16_t)l;
+        }
+      }
+      ek.j0 = j0;
+      if ((rc = launch_ntt_ts_ks_group(c, ntt_in, ntt_ws, s1, tmap, S, batch, ek, st))) return rc;
+      for (int t = 0; t < g.E; ++t) ek.init_acc[t] = 1;
+    }
+  } else {
+    int first = 1;
+    for (int j = 0; j < dnum; ++j) {
+      const int lo = j * g.alpha;
+      if (lo > level) break;
+      const int hi = std::min((j + 1) * g.alpha, g.l1);
+      LimbMap mu;
+      mu.n = 0;
+      std::vector<int> src, dst;
+      for (int s = lo; s < hi; ++s) src.push_back(s);
+      for (int r = 0; r < g.E; ++r) {
+        if (r >= lo && r < hi) continue;
+        mu.prime[mu.n] = (int16_t)ext_prime(g, r);
+        mu.out_row[mu.n] = (int16_t)r;
+        mu.in_row[mu.n] = (int16_t)(hi - lo == 1 ? lo : mu.n);
+        dst.push_back(ext_prime(g, r));
+        ++mu.n;
+      }
+      const uint32_t* ntt_in = y;
+      if (hi - lo > 1) {
+        BconvArgs ba;
+        if ((rc = fill_bconv(c, src, dst, ba))) return rc;
+        if ((rc = launch_bconv(c, y + (size_t)lo * U, conv, ba, batch, st))) return rc;
+        ntt_in = conv;
+      }
+      // alpha = 1: fast_basis_conv is the identity on the slice's coefficients
+      // (Q = q_lo, Q/q = 1), so the NTT reads y's row directly and reduces it
+      // mod each target prime inside the byte-sliced GEMM.  The inner product
+      // acc += raised * key_j (ckks.py:345-351) is fused into the NTT's output
+      // epilogue: the raised limbs never touch HBM.
+      const uint32_t* kb = key + (size_t)j * key_pair;
+      const uint32_t* ka = kb + (size_t)(g.Lc + g.K) * c.n;
+      EpiArgs ek;
+      memset(&ek, 0, sizeof(ek));
+      ek.mode = EPI_KS_MAC;
+      ek.kb = kb;
+      ek.ka = ka;
+      ek.acc_b = acc;
+      ek.acc_a = acc + g.E * U;
+      ek.first = first;
+      for (int l = 0; l < mu.n; ++l) ek.key_row[l] = (int16_t)key_row[mu.out_row[l]];
+      if ((rc = launch_ntt(c, ntt_in, nullptr, mu, batch, 0, &ek, ntt_ws, ntt_ws_bytes, st)))
+        return rc;
+      // slice rows are reused unchanged (ckks.py:361-364): MAC them straight from d
+      int64_t key_off[kMaxRows];
+      for (int r = lo; r < hi; ++r) key_off[r - lo] = (int64_t)key_row[r] * c.n;
+      if ((rc = launch_ks_mac(c, d + (size_t)lo * U, kb, ka, acc + (size_t)lo * U,
+                              acc + (g.E + lo) * U, row_prime + lo, key_off, hi - lo, batch,
+                              first, st)))
+        return rc;
+      first = 0;
+    }
   }
 
   // 3. ModDown of acc_b and acc_a  (ckks.py:367-381)
@@ -465,7 +549,10 @@ int tfhe_bconv(TfheCtx* h, const uint32_t* in, uint32_t* out, const int32_t* src
 size_t tfhe_ckks_workspace_bytes(const TfheCtx* h, int level, int batch) {
   if (!h) return 0;
   // worst case over dnum: general base conversion buffers included
-  CkksGeom g = geom(h, level, 1);
+  // worst case over dnum: alpha = 1 maximises the key-switch group size,
+  // general base-conversion buffers included
+  CkksGeom g = geom(h, level, h->n_chain);
+  set_group(g, h->c, batch);
   g.need_conv = true;
   const size_t U = (size_t)batch * h->c.n * 4;
   return ks_bytes(g, batch, h->c.n) + 3 * (size_t)g.l1 * U + 256;

@@ -66,6 +66,8 @@ struct TsArgs {
   int H;      // 128-row twiddle halves
   int C;      // chunks per limb
   int n_limbs;
+  int S;      // stage-2 input slices per (limb, chunk) group (EPI_KS_ACC), else 1;
+              // the stage-2 input row of (slice s, limb l) is s * n_limbs + l
   int dbg;    // perf experiments only (env TFHE_DBG): 1 = producers skip global loads,
               // 2 = epilogue skips math/stores; results are garbage when set
   LimbMap map;
@@ -95,14 +97,17 @@ TFHE_DEV uint32_t ring_off(int row, int k) {
 // sequence (limb, chunk) and the same ring / accumulator phases
 struct UnitIter {
   int limb, c, b, x0;
+  int sl;         // slice within the (limb, chunk) group (EPI_KS_ACC)
+  int S;          // slices per group
   int s;          // ring slot
   uint32_t rph;   // ring phase parity of slot s
   int ab;         // accumulator buffer
   uint32_t aph;   // accumulator phase parity
-  TFHE_DEV void init(long long u0, int C, int logR, int R) {
-    limb = (int)(u0 / C);
-    c = (int)(u0 % C);
+  TFHE_DEV void init(long long g0, int C, int logR, int R, int S_) {
+    limb = (int)(g0 / C);
+    c = (int)(g0 % C);
     set_col(logR, R);
+    sl = 0; S = S_;
     s = 0; rph = 0; ab = 0; aph = 0;
   }
   TFHE_DEV void set_col(int logR, int R) {
@@ -111,7 +116,10 @@ struct UnitIter {
     x0 = col0 & (R - 1);
   }
   TFHE_DEV void next(int C, int logR, int R) {
-    if (++c == C) { c = 0; ++limb; }
+    if (++sl == S) {
+      sl = 0;
+      if (++c == C) { c = 0; ++limb; }
+    }
     set_col(logR, R);
     if (++s == kRing) { s = 0; rph ^= 1; }
     ab ^= 1;
@@ -182,9 +190,10 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     grp = blockIdx.x;
     groups = gridDim.x;
   }
-  const long long U = (long long)a.n_limbs * a.C;
-  const long long u0 = U * grp / groups;
-  const int cnt = (int)(U * (grp + 1) / groups - u0);
+  // groups = (limb, chunk); each group is S consecutive units (one per slice)
+  const long long G = (long long)a.n_limbs * a.C;
+  const long long g0 = G * grp / groups;
+  const int cnt = (int)(G * (grp + 1) / groups - g0) * a.S;
   const int C = a.C, R = a.R, logR = 31 - __clz(a.R);
 
   if (tid == 0) {
@@ -205,7 +214,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   UnitIter w;
-  w.init(u0, C, logR, R);
+  w.init(g0, C, logR, R, a.S);
   // Each role's register budget is set at the top of its own branch so that
   // ptxas allocates every role's code under the matching setmaxnreg limit.
   if (warp < 4) {
@@ -235,8 +244,9 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
         }
       } else {
         // blocked P [limb][b][i2/16][k1][16]: row k1's k-block = 64 contiguous bytes
-        const uint32_t* src = a.in + ((size_t)it.limb * a.batch + it.b) * a.n +
-                              (size_t)(it.x0 + col) * kNC;
+        const uint32_t* src =
+            a.in + ((size_t)(it.sl * a.n_limbs + it.limb) * a.batch + it.b) * a.n +
+            (size_t)(it.x0 + col) * kNC;
 #pragma unroll
         for (int t = 0; t < K / 128; ++t)
 #pragma unroll
@@ -333,6 +343,17 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
           src[2] = a.epi.acc_b + ar;
           src[3] = a.epi.acc_a + ar;
         }
+      } else if (mode == EPI_KS_ACC) {
+        // key rows of slice j0 + sl for this target; accumulators at group start
+        const uint32_t* kbj = a.epi.key + (size_t)(a.epi.j0 + it.sl) * a.epi.key_pair +
+                              (size_t)a.epi.key_row[it.limb] * a.n + wrow;
+        src[0] = kbj;
+        src[1] = kbj + a.epi.key_pair / 2;
+        if (it.sl == 0 && a.epi.init_acc[it.limb]) {
+          const size_t ar = ((size_t)a.map.out_row[it.limb] * a.batch + it.b) * a.n + wrow;
+          src[2] = a.epi.acc_b + ar;
+          src[3] = a.epi.acc_a + ar;
+        }
       }
       uint8_t* dstb = wstg + buf * 8192;
 #pragma unroll
@@ -370,6 +391,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     };
     UnitIter ahead = w;
     if (cnt > 0) prefetch(ahead, 0);
+    uint32_t regb[16], rega[16];   // EPI_KS_ACC group accumulators
     cp_async_commit();
     int prev = -1;
     for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
@@ -451,6 +473,35 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
         continue;
       }
       const size_t wrow = (size_t)(h * 128 + wq * 32) * a.n1 + w.x0;
+      if (mode == EPI_KS_ACC) {
+        // y is in Montgomery form (twiddles carry R^2); the S slices of this
+        // (target, chunk) group accumulate in registers, acc touches HBM once
+        if (w.sl == 0) {
+          if (a.epi.init_acc[limb]) {
+            read_row(buf, 2, regb);
+            read_row(buf, 3, rega);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) regb[e] = rega[e] = 0;
+          }
+        }
+        if (a.epi.j0 + w.sl != a.epi.js[limb]) {
+          uint32_t kb[16], ka[16];
+          read_row(buf, 0, kb);
+          read_row(buf, 1, ka);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            regb[e] = add_mod(regb[e], mont_reduce((uint64_t)y[e] * kb[e], pc), pc.q);
+            rega[e] = add_mod(rega[e], mont_reduce((uint64_t)y[e] * ka[e], pc), pc.q);
+          }
+        }
+        if (w.sl == w.S - 1) {
+          const size_t ar = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n + wrow;
+          store_tile(0, regb, a.epi.acc_b + ar, a.n1);
+          store_tile(1, rega, a.epi.acc_a + ar, a.n1);
+        }
+        continue;
+      }
       if (mode == EPI_KS_MAC) {
         // y is in Montgomery form (y R: twiddles carry R^2), so one Montgomery
         // product per key gives y * k exactly
@@ -594,6 +645,8 @@ int launch_ts_k(const Ctx& c, int K, TsArgs& a, cudaStream_t st) {
     TFHE_TS_CASE(128, EPI_SUB_SCALE)
     TFHE_TS_CASE(256, EPI_KS_MAC)
     TFHE_TS_CASE(128, EPI_KS_MAC)
+    TFHE_TS_CASE(256, EPI_KS_ACC)
+    TFHE_TS_CASE(128, EPI_KS_ACC)
   }
 #undef TFHE_TS_CASE
   set_error("ts kernel: unsupported contraction length");
@@ -689,6 +742,29 @@ int build_ts_tables(Ctx& c) {
   return 0;
 }
 
+int launch_ntt_ts_stage1(const Ctx& c, const uint32_t* in, uint32_t* P, const LimbMap& map,
+                         int batch, int inverse, cudaStream_t st) {
+  TsArgs a;
+  memset(&a, 0, sizeof(a));
+  a.pc = c.d_pc;
+  a.n = c.n;
+  a.n1 = c.n1;
+  a.n2 = c.n2;
+  a.batch = batch;
+  a.n_limbs = map.n;
+  a.S = 1;
+  a.map = map;
+  a.epi.mode = EPI_STORE;
+  a.in = in;
+  a.out = P;
+  a.twa = c.d_twa[inverse][0];
+  a.w2 = c.d_w2r[inverse];
+  a.R = c.n2;
+  a.H = c.n1 / 128;
+  a.C = batch * c.n2 / kNC;
+  return launch_ts_k<1>(c, c.n1, a, st);
+}
+
 int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& map, int batch,
                   int inverse, const EpiArgs* epi, void* ws, cudaStream_t st) {
   TsArgs a;
@@ -699,6 +775,7 @@ int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap
   a.n2 = c.n2;
   a.batch = batch;
   a.n_limbs = map.n;
+  a.S = 1;
   static const int dbg = getenv("TFHE_DBG") ? atoi(getenv("TFHE_DBG")) : 0;
   a.dbg = dbg;  // (only read when built with -DTFHE_TS_DBG)
   a.map = map;
@@ -724,6 +801,37 @@ int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap
     set_error("fused key-switch MAC needs a forward transform");
     return 2;
   }
+  a.R = c.n1;
+  a.H = c.n2 / 128;
+  a.C = batch * c.n1 / kNC;
+  return launch_ts_k<2>(c, c.n2, a, st);
+}
+
+int launch_ntt_ts_ks_group(const Ctx& c, const uint32_t* in, void* ws, const LimbMap& s1map,
+                           const LimbMap& tmap, int S, int batch, const EpiArgs& epi,
+                           cudaStream_t st) {
+  if (s1map.n != S * tmap.n) {
+    set_error("key-switch group: stage-1 map must hold S * T limbs");
+    return 2;
+  }
+  // stage 1 (forward) over every (slice, target) limb into the workspace
+  int rc = launch_ntt_ts_stage1(c, in, static_cast<uint32_t*>(ws), s1map, batch, 0, st);
+  if (rc) return rc;
+  TsArgs a;
+  memset(&a, 0, sizeof(a));
+  a.pc = c.d_pc;
+  a.n = c.n;
+  a.n1 = c.n1;
+  a.n2 = c.n2;
+  a.batch = batch;
+  a.n_limbs = tmap.n;
+  a.S = S;
+  a.map = tmap;
+  a.epi = epi;
+  a.epi.mode = EPI_KS_ACC;
+  a.in = static_cast<const uint32_t*>(ws);
+  a.out = nullptr;
+  a.twa = c.d_twa_ks;
   a.R = c.n1;
   a.H = c.n2 / 128;
   a.C = batch * c.n1 / kNC;

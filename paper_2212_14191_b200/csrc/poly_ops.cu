@@ -115,7 +115,7 @@ __global__ void tensor_kernel(const uint32_t* __restrict__ b0, const uint32_t* _
 
 struct MacArgs {
   int16_t prime[kMaxRows];
-  int32_t key_row[kMaxRows];  // row of the (rows_key, n) key matrices
+  int64_t key_off[kMaxRows];  // element offset of this row's key row (from kb / ka)
 };
 
 // acc_b[r] (+)= x[r] * kb[key_row[r]], acc_a[r] (+)= x[r] * ka[key_row[r]];
@@ -128,8 +128,8 @@ __global__ void ks_mac_kernel(const uint32_t* __restrict__ x, const uint32_t* __
   const PrimeConst pc = pcs[ma.prime[row]];
   const int64_t per_row = (int64_t)batch * n;
   const int64_t base = (int64_t)row * per_row;
-  const uint32_t* kbr = kb + (int64_t)ma.key_row[row] * n;
-  const uint32_t* kar = ka + (int64_t)ma.key_row[row] * n;
+  const uint32_t* kbr = kb + ma.key_off[row];
+  const uint32_t* kar = ka + ma.key_off[row];
   for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
        i += (int64_t)gridDim.x * blockDim.x * 4) {
     const int64_t o = base + i;
@@ -294,12 +294,12 @@ int launch_tensor(const Ctx& c, const uint32_t* b0, const uint32_t* a0, const ui
 
 int launch_ks_mac(const Ctx& c, const uint32_t* x, const uint32_t* kb, const uint32_t* ka,
                   uint32_t* acc_b, uint32_t* acc_a, const int16_t* row_prime,
-                  const int32_t* key_row, int rows, int batch, int first, cudaStream_t st) {
+                  const int64_t* key_off, int rows, int batch, int first, cudaStream_t st) {
   if (rows <= 0) return 0;
   MacArgs ma;
   for (int r = 0; r < rows; ++r) {
     ma.prime[r] = row_prime[r];
-    ma.key_row[r] = key_row[r];
+    ma.key_off[r] = key_off[r];
   }
   dim3 g = grid_rows((int64_t)batch * c.n, rows, 256);
   ks_mac_kernel<<<g, 256, 0, st>>>(x, kb, ka, acc_b, acc_a, c.d_pc, ma, batch, c.n, first);

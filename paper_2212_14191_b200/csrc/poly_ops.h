@@ -28,7 +28,7 @@ int launch_tensor(const Ctx& c, const uint32_t* b0, const uint32_t* a0, const ui
                   const int16_t* row_prime, int rows, int64_t per_row, cudaStream_t st);
 int launch_ks_mac(const Ctx& c, const uint32_t* x, const uint32_t* kb, const uint32_t* ka,
                   uint32_t* acc_b, uint32_t* acc_a, const int16_t* row_prime,
-                  const int32_t* key_row, int rows, int batch, int first, cudaStream_t st);
+                  const int64_t* key_off, int rows, int batch, int first, cudaStream_t st);
 int launch_automorph(const Ctx& c, const uint32_t* in, uint32_t* out, uint32_t t, int ntt_domain,
                      const int16_t* row_prime, int rows, int batch, cudaStream_t st);
 int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,

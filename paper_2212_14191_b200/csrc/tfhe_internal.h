@@ -10,7 +10,7 @@
 
 namespace tfhe {
 
-constexpr int kMaxLimbs = 128;  // rows one launch may address
+constexpr int kMaxLimbs = 512;  // rows one launch may address (kernel params <= 32 KB)
 
 struct PrimeConst {
   uint32_t q;
@@ -39,6 +39,9 @@ enum EpiMode : int {
   EPI_KS_MAC = 2,      // acc_b (+)= NTT(in) * kb[key_row], acc_a (+)= NTT(in) * ka[key_row]
                        // (key-switch inner product fused into ModUp, ckks.py:345-351);
                        // acc rows = out_row[l]; `first` overwrites instead of adding
+  EPI_KS_ACC = 3,      // TS stage 2 over a group of S key-switch slices per target:
+                       // acc (=|+=) sum_s NTT(P_s) * k_{j0+s}[key_row], accumulated on
+                       // chip, one acc read/write per group (ckks.py:337-351)
 };
 
 struct EpiArgs {
@@ -56,6 +59,12 @@ struct EpiArgs {
   uint32_t* acc_a;
   int16_t key_row[kMaxLimbs];
   int first;
+  // EPI_KS_ACC
+  const uint32_t* key;      // (dnum, 2, key_rows, n) switching key
+  long long key_pair;       // elements per (b_j, a_j) pair
+  int j0;                   // first slice of the group
+  int16_t js[kMaxLimbs];    // slice that owns target row l (-1: none) -> skipped
+  int16_t init_acc[kMaxLimbs];  // 1: start from acc, 0: start from zero
 };
 
 struct Ctx {
@@ -86,6 +95,15 @@ struct Ctx {
 
 // twiddle-resident tensor-core stages (ntt_ts.cu)
 int build_ts_tables(Ctx& c);
+// Key-switch group: stage 1 over the S*T limbs of `s1map` (limb s*T + t =
+// slice s, target t) into ws, then stage 2 over the T targets of `tmap`
+// (prime, out_row = accumulator row) accumulating the S slices per target on
+// chip into epi.acc_b / epi.acc_a (EPI_KS_ACC).  ws >= S*T*batch*n words.
+int launch_ntt_ts_ks_group(const Ctx& c, const uint32_t* in, void* ws, const LimbMap& s1map,
+                           const LimbMap& tmap, int S, int batch, const EpiArgs& epi,
+                           cudaStream_t st);
+int launch_ntt_ts_stage1(const Ctx& c, const uint32_t* in, uint32_t* P, const LimbMap& map,
+                         int batch, int inverse, cudaStream_t st);
 int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& map, int batch,
                   int inverse, const EpiArgs* epi, void* ws, cudaStream_t st);
 
