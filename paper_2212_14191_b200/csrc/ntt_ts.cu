@@ -31,6 +31,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "tfhe_internal.h"
 
@@ -39,7 +41,8 @@ namespace tfhe {
 namespace {
 
 constexpr int kNC = 16;                  // data columns per chunk
-constexpr int kRing = 6;                 // smem ring depth (chunks)
+constexpr int kRing = 4;                 // smem operand ring depth (chunks)
+constexpr int kRaw = 4;                  // TMA raw-data ring depth (chunks in flight)
 // 3 warpgroups: producers (warps 0-3), epilogue (4-7), MMA issuer (warp 8;
 // warps 9-11 idle).  Registers are rebalanced with setmaxnreg: each SMSP
 // holds one warp of every warpgroup, so 144 + 256 + 88 <= 512 per lane.
@@ -50,6 +53,8 @@ constexpr uint32_t kAccCol0 = 256, kAccCol1 = 384;
 // -DTFHE_TS_DBG; normal builds compile them away.
 #ifdef TFHE_TS_DBG
 #define kDbg (a.dbg)
+#elif defined(TFHE_TS_DBG_VAL)
+#define kDbg (TFHE_TS_DBG_VAL)
 #else
 #define kDbg 0
 #endif
@@ -70,6 +75,8 @@ struct TsArgs {
               // the stage-2 input row of (slice s, limb l) is s * n_limbs + l
   int dbg;    // perf experiments only (env TFHE_DBG): 1 = producers skip global loads,
               // 2 = epilogue skips math/stores; results are garbage when set
+  CUtensorMap tmap;  // TMA view of the input (stage 1: [rows*B][n1][n2]; stage 2:
+                     // blocked P [rows*B][n2/16][n1][16], 64-byte swizzle)
   LimbMap map;
   EpiArgs epi;
 };
@@ -170,13 +177,16 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
   constexpr int kStageBytes = ring_stage_bytes<K>();
   constexpr int KC = K / 32;
   extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int kRawBytes = K * 64;            // one raw data chunk (16 u32 x K)
   uint8_t* stg = smem + kRing * kStageBytes;  // epilogue staging
-  uint64_t* b_full = reinterpret_cast<uint64_t*>(stg + kStgBytes);
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(stg + kStgBytes + kRaw * kRawBytes);
   uint64_t* b_empty = b_full + kRing;
   uint64_t* acc_full = b_empty + kRing;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* tw_full = acc_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tw_full + 1);
+  uint64_t* raw_full = tw_full + 1;
+  uint64_t* raw_empty = raw_full + kRaw;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + kRaw);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // work split: units u = limb * C + chunk over this CTA's half
@@ -206,6 +216,10 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       mbar_init(&acc_empty[s], 128);
     }
     mbar_init(tw_full, 128);
+    for (int s = 0; s < kRaw; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], 128);
+    }
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc<512>(tmem_slot);
@@ -221,63 +235,48 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     reg_dealloc<kRegsProducer>();
     if (kDbg & 4) goto role_done;
     // ---------------------------------------------------------------- producers
-    // Stage 1 (X_b[k][x0 + c], columns contiguous): B' is stored MN-major --
-    // each thread loads 16 B (4 columns of one k row) and writes one 4-byte
-    // word per byte plane; a warp covers 8 k rows x 64 B = one conflict-free
-    // 128-byte span per plane.
-    // Stage 2 (P_b[x0 + r][k], k contiguous): B' is stored K-major -- each
-    // thread loads 16 consecutive k of one row and writes one 16-byte vector
-    // per plane; a quarter warp covers 8 rows = 8 distinct 16-byte slots.
-    // Software-pipelined: the next chunk's global loads are issued before the
-    // current chunk is split and stored, so load latency overlaps the ring.
-    constexpr int kVals = K / 8;   // u32 values per thread per chunk
+    // Raw data chunks arrive by TMA (one elected thread, kRaw chunks in
+    // flight) in a staging ring; the 4 producer warps byte-split them into the
+    // MMA operand ring.
+    // Stage 1 (X_b[k][x0 + c], columns contiguous): raw [K rows][16 u32];
+    // B' is stored MN-major -- each thread reads 16 B (4 columns of one k
+    // row) and writes one 4-byte word per byte plane; a warp covers 8 k rows
+    // x 64 B = one conflict-free 128-byte span per plane.
+    // Stage 2 (blocked P, k contiguous): raw [K/16][16 rows][16 u32] with the
+    // TMA 64-byte swizzle; B' is stored K-major -- each thread reads 16
+    // consecutive k of one row and writes one 16-byte vector per plane; a
+    // quarter warp covers 8 rows = 8 distinct 16-byte slots on both sides.
     const int c4 = (tid & 3) * 4, krow0 = tid >> 2;   // stage 1 mapping
     const int col = tid & 15, kb0 = tid >> 4;         // stage 2 mapping
-    auto load_chunk = [&](const UnitIter& it, uint32_t (&v)[kVals]) {
-      if (STAGE == 1) {
-        const uint32_t* src =
-            a.in + ((size_t)a.map.in_row[it.limb] * a.batch + it.b) * a.n + it.x0 + c4;
-#pragma unroll
-        for (int m = 0; m < K / 32; ++m) {
-          uint4 x = __ldg(reinterpret_cast<const uint4*>(src + (size_t)(krow0 + 32 * m) * a.n2));
-          v[4 * m] = x.x; v[4 * m + 1] = x.y; v[4 * m + 2] = x.z; v[4 * m + 3] = x.w;
-        }
-      } else {
-        // blocked P [limb][b][i2/16][k1][16]: row k1's k-block = 64 contiguous bytes
-        const uint32_t* src =
-            a.in + ((size_t)(it.sl * a.n_limbs + it.limb) * a.batch + it.b) * a.n +
-            (size_t)(it.x0 + col) * kNC;
-#pragma unroll
-        for (int t = 0; t < K / 128; ++t)
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            uint4 x = __ldg(reinterpret_cast<const uint4*>(
-                src + (size_t)(kb0 + 8 * t) * kNC * a.n1 + 4 * q4));
-            v[16 * t + 4 * q4] = x.x; v[16 * t + 4 * q4 + 1] = x.y;
-            v[16 * t + 4 * q4 + 2] = x.z; v[16 * t + 4 * q4 + 3] = x.w;
-          }
-      }
+    uint8_t* raw = smem + kRing * kStageBytes + kStgBytes;
+    auto issue_raw = [&](const UnitIter& it, int slot) {
+      uint8_t* dst = raw + slot * kRawBytes;
+      mbar_arrive_expect_tx(&raw_full[slot], kRawBytes);
+      if (STAGE == 1)
+        tma_load_3d(dst, &a.tmap, it.x0, 0, a.map.in_row[it.limb] * a.batch + it.b,
+                    &raw_full[slot]);
+      else
+        tma_load_4d(dst, &a.tmap, 0, it.x0, 0,
+                    (it.sl * a.n_limbs + it.limb) * a.batch + it.b, &raw_full[slot]);
     };
-    uint32_t cur[kVals], nxt[kVals];
     UnitIter ahead = w;
-    if (cnt > 0) load_chunk(ahead, nxt);
+    if (tid == 0) {
+      for (int i = 0; i < kRaw && i < cnt; ++i, ahead.next(C, logR, R)) issue_raw(ahead, i);
+    }
     for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
-#pragma unroll
-      for (int e = 0; e < kVals; ++e) cur[e] = nxt[e];
-      if (i + 1 < cnt) {
-        ahead.next(C, logR, R);
-        if (!(kDbg & 1)) load_chunk(ahead, nxt);
-      }
+      const int rs = i % kRaw;
+      const uint32_t rph = (uint32_t)((i / kRaw) & 1);
+      mbar_wait(&raw_full[rs], rph);
+      const uint8_t* rw = raw + rs * kRawBytes;
       if (i >= kRing) mbar_wait(&b_empty[w.s], w.rph ^ 1);
       uint8_t* st = smem + w.s * kStageBytes;
-      if (kDbg & 16) {
-        // handshake-only experiment
-      } else if (STAGE == 1) {
+      if (STAGE == 1) {
 #pragma unroll
         for (int m = 0; m < K / 32; ++m) {
           const int k = krow0 + 32 * m;
+          const uint4 x = *reinterpret_cast<const uint4*>(rw + k * 64 + c4 * 4);
           uint32_t pw[4];
-          planes4(cur[4 * m], cur[4 * m + 1], cur[4 * m + 2], cur[4 * m + 3], pw);
+          planes4(x.x, x.y, x.z, x.w, pw);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<uint32_t*>(st + ring_off_mn(j, c4, k)) = pw[j];
@@ -285,20 +284,31 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       } else {
 #pragma unroll
         for (int t = 0; t < K / 128; ++t) {
-          const int k0 = (kb0 + 8 * t) * 16;
+          const int kb = kb0 + 8 * t, k0 = kb * 16;
+          uint32_t v[16];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 x = *reinterpret_cast<const uint4*>(rw + kb * 1024 + stg_off(col, q));
+            v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+          }
           uint32_t pw[4][4];  // [group][plane]
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
-            planes4(cur[16 * t + 4 * g], cur[16 * t + 4 * g + 1], cur[16 * t + 4 * g + 2],
-                    cur[16 * t + 4 * g + 3], pw[g]);
+          for (int g = 0; g < 4; ++g) planes4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3], pw[g]);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<uint4*>(st + ring_off(j * 16 + col, k0)) =
                 make_uint4(pw[0][j], pw[1][j], pw[2][j], pw[3][j]);
         }
       }
-      if (!(kDbg & 32)) fence_proxy_async_smem();
+      fence_proxy_async_smem();
       mbar_arrive(&b_full[w.s]);
+      mbar_arrive(&raw_empty[rs]);
+      if (tid == 0 && i + kRaw < cnt) {
+        // refill this raw slot once every producer thread has read it
+        mbar_wait(&raw_empty[rs], rph);
+        issue_raw(ahead, rs);
+        ahead.next(C, logR, R);
+      }
     }
   } else if (warp < 8) {
     reg_alloc<kRegsEpilogue>();
@@ -616,7 +626,8 @@ role_done:
 
 template <int STAGE, int K, int MODE>
 int launch_ts(const Ctx& c, TsArgs& a, cudaStream_t st) {
-  const int smem = kRing * ring_stage_bytes<K>() + kStgBytes + (2 * kRing + 5) * 8 + 16;
+  const int smem = kRing * ring_stage_bytes<K>() + kStgBytes + kRaw * K * 64 +
+                   (2 * kRing + 5 + 2 * kRaw) * 8 + 16;
   auto kern = ntt_ts_kernel<STAGE, K, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const long long U = (long long)a.n_limbs * a.C;
@@ -664,6 +675,72 @@ uint32_t powmod_h(uint64_t b, uint64_t e, uint32_t q) {
   return (uint32_t)r;
 }
 
+
+// ---- TMA tensor maps (driver entry point fetched once through the runtime)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// stage-1 input: (rows*B, n1, n2) u32, box {16, K, 1}
+int make_tmap_stage1(const Ctx& c, CUtensorMap* m, const uint32_t* in, int rows, int batch) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return 3;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)c.n2, (cuuint64_t)c.n1, (cuuint64_t)rows * batch};
+  cuuint64_t strides[2] = {(cuuint64_t)c.n2 * 4, (cuuint64_t)c.n * 4};
+  cuuint32_t box[3] = {16, (cuuint32_t)c.n1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(in), dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    set_error("stage-1 tensor map encode failed");
+    return 3;
+  }
+  return 0;
+}
+
+// stage-2 input: blocked P (rows*B, n2/16, n1, 16) u32, box {16, 16, K/16, 1},
+// 64-byte swizzle (conflict-free converter reads)
+int make_tmap_stage2(const Ctx& c, CUtensorMap* m, const uint32_t* P, int rows, int batch) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return 3;
+  }
+  cuuint64_t dims[4] = {16, (cuuint64_t)c.n1, (cuuint64_t)c.n2 / 16, (cuuint64_t)rows * batch};
+  cuuint64_t strides[3] = {64, (cuuint64_t)c.n1 * 64, (cuuint64_t)c.n * 4};
+  cuuint32_t box[4] = {16, 16, (cuuint32_t)c.n2 / 16, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  if (fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t*>(P), dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    set_error("stage-2 tensor map encode failed");
+    return 3;
+  }
+  return 0;
+}
+
+int max_in_row(const LimbMap& m) {
+  int r = 0;
+  for (int l = 0; l < m.n; ++l) r = std::max(r, (int)m.in_row[l]);
+  return r + 1;
+}
 }  // namespace
 
 int build_ts_tables(Ctx& c) {
@@ -762,6 +839,8 @@ int launch_ntt_ts_stage1(const Ctx& c, const uint32_t* in, uint32_t* P, const Li
   a.R = c.n2;
   a.H = c.n1 / 128;
   a.C = batch * c.n2 / kNC;
+  int rc = make_tmap_stage1(c, &a.tmap, in, max_in_row(map), batch);
+  if (rc) return rc;
   return launch_ts_k<1>(c, c.n1, a, st);
 }
 
@@ -791,11 +870,14 @@ int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap
   a.R = c.n2;
   a.H = c.n1 / 128;
   a.C = batch * c.n2 / kNC;
-  int rc = launch_ts_k<1>(c, c.n1, a, st);
+  int rc = make_tmap_stage1(c, &a.tmap, in, max_in_row(map), batch);
+  if (rc) return rc;
+  rc = launch_ts_k<1>(c, c.n1, a, st);
   if (rc) return rc;
   // stage 2: rows k2 (n2 twiddle rows), data columns (b, k1)
   a.in = P;
   a.out = out;
+  if ((rc = make_tmap_stage2(c, &a.tmap, P, map.n, batch))) return rc;
   a.twa = (epi && epi->mode == EPI_KS_MAC) ? c.d_twa_ks : c.d_twa[inverse][1];
   if (epi && epi->mode == EPI_KS_MAC && inverse) {
     set_error("fused key-switch MAC needs a forward transform");
@@ -832,6 +914,7 @@ int launch_ntt_ts_ks_group(const Ctx& c, const uint32_t* in, void* ws, const Lim
   a.in = static_cast<const uint32_t*>(ws);
   a.out = nullptr;
   a.twa = c.d_twa_ks;
+  if ((rc = make_tmap_stage2(c, &a.tmap, a.in, S * tmap.n, batch))) return rc;
   a.R = c.n1;
   a.H = c.n2 / 128;
   a.C = batch * c.n1 / kNC;
