@@ -64,9 +64,15 @@ TFHE_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n"
       "WAIT_%=:\n\t"
+#ifdef TFHE_MBAR_HINT
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(TFHE_MBAR_HINT)
+#else
       "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
       "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
+#endif
       : "memory");
 }
 // 1-D bulk copy global -> shared through the TMA engine; completes tx bytes

@@ -20,13 +20,15 @@
 //   (7 x 16 TMEM columns, double-buffered).  C_s < 4 * 256 * 255^2 < 2^26.
 // * Epilogue warps fold sum C_s 2^(8s) (2^(8s) mod q for s >= 4) in 64 bits,
 //   Barrett-reduce, apply W2 (stage 1) or the fused output epilogue
-//   (stage 2) and store 64 contiguous bytes per thread.
+//   (stage 2) and store through a smem transpose (full 32-byte sectors).
 //
-// Roles: warps 0-3 data producers, warps 4-7 epilogue (+ twiddle -> TMEM
-// loads), warp 8 TMEM allocation + single-thread MMA issue.  Persistent grid
+// Roles: warps 0-3 data producers, warps 4-11 epilogue (+ twiddle -> TMEM
+// loads; two warps per TMEM lane quarter, 8 columns each), warp 12 TMEM
+// allocation + single-thread MMA issue.  Persistent grid
 // (one CTA per SM); with two 128-row halves the CTAs run in pairs over the
 // same data range so the second read of each data chunk hits L2.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -43,11 +45,20 @@ namespace {
 constexpr int kNC = 16;                  // data columns per chunk
 constexpr int kRing = 4;                 // smem operand ring depth (chunks)
 constexpr int kRaw = 4;                  // TMA raw-data ring depth (chunks in flight)
-// 3 warpgroups: producers (warps 0-3), epilogue (4-7), MMA issuer (warp 8;
-// warps 9-11 idle).  Registers are rebalanced with setmaxnreg: each SMSP
-// holds one warp of every warpgroup, so 144 + 256 + 88 <= 512 per lane.
-constexpr int kThreadsTS = 384;
-constexpr int kRegsProducer = 144, kRegsEpilogue = 256, kRegsMma = 88;
+// 4 warpgroups: producers (warps 0-3), epilogue (4-11), MMA issuer (warp 12;
+// warps 13-15 idle).  Registers are rebalanced with setmaxnreg: each SMSP
+// holds one warp of every warpgroup, so 96 + 2 * 176 + 64 <= 512 per lane.
+constexpr int kEpiWarps = 8;              // two epilogue warps per TMEM lane quarter
+constexpr int kCW = kNC / (kEpiWarps / 4);  // chunk columns per epilogue warp
+constexpr int kMmaWarp = 4 + kEpiWarps;
+// MMA-issuing warps (chunks round-robin): while one issuer waits on its
+// barriers / steps its bookkeeping the other keeps the tensor queue fed
+#ifndef TFHE_MMA_ISSUERS
+#define TFHE_MMA_ISSUERS 2
+#endif
+constexpr int kMmaIssuers = TFHE_MMA_ISSUERS;
+constexpr int kThreadsTS = 512;
+constexpr int kRegsProducer = 96, kRegsEpilogue = 176, kRegsMma = 64;
 constexpr uint32_t kAccCol0 = 256, kAccCol1 = 384;
 // Performance-experiment knobs (env TFHE_DBG) exist only in builds with
 // -DTFHE_TS_DBG; normal builds compile them away.
@@ -73,6 +84,7 @@ struct TsArgs {
   int n_limbs;
   int S;      // stage-2 input slices per (limb, chunk) group (EPI_KS_ACC), else 1;
               // the stage-2 input row of (slice s, limb l) is s * n_limbs + l
+  unsigned long long* trace;  // TFHE_TS_TRACE builds: per-chunk event clocks of CTA 0
   int dbg;    // perf experiments only (env TFHE_DBG): 1 = producers skip global loads,
               // 2 = epilogue skips math/stores; results are garbage when set
   CUtensorMap tmap;  // TMA view of the input (stage 1: [rows*B][n1][n2]; stage 2:
@@ -80,6 +92,17 @@ struct TsArgs {
   LimbMap map;
   EpiArgs epi;
 };
+
+#ifdef TFHE_TS_TRACE
+constexpr int kTraceN = 512;
+#define TS_TRACE(ev, i)                                                        \
+  do {                                                                         \
+    if (blockIdx.x == 0 && lane == 0 && (i) < kTraceN)                         \
+      a.trace[(ev) * kTraceN + (i)] = clock64();                               \
+  } while (0)
+#else
+#define TS_TRACE(ev, i) do { } while (0)
+#endif
 
 template <int K>
 __host__ __device__ constexpr int ring_stage_bytes() { return (K / 32) * 2048; }
@@ -142,21 +165,16 @@ TFHE_DEV uint32_t ring_off_mn(int j, int c, int k) {
   return (uint32_t)(kc * 2048 + j * 512 + (kk >> 3) * 128 + (kk & 7) * 16 + c);
 }
 
-TFHE_DEV void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
-               "r"(smem_u32(ssrc)), "r"(bytes)
-               : "memory");
-}
-TFHE_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-TFHE_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
-TFHE_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-constexpr int kWarpStg = 10 * 2048;               // per epilogue warp: in[2][4] | out[2] tiles
-constexpr int kStgBytes = 4 * kWarpStg;           // all 4 epilogue warps
+constexpr int kWarpStg = 10 * 1024;               // per epilogue warp: in[2][4] | out[2] tiles
+constexpr int kStgBytes = kEpiWarps * kWarpStg;   // all epilogue warps
 
 // 32 rows x 64 B staging, 16-byte chunks XOR-swizzled so both the row-wise
 // and the 4-lanes-per-row accesses are bank-conflict free
 TFHE_DEV uint32_t stg_off(int row, int q) { return (uint32_t)(row * 64 + 16 * (q ^ ((row >> 1) & 3))); }
+// 32 rows x 32 B epilogue tile: row-wise (1 lane per row) and 2-lanes-per-row
+// 16-byte accesses are both conflict free
+TFHE_DEV uint32_t stg8_off(int row, int q) { return (uint32_t)(row * 32 + 16 * (q ^ ((row >> 2) & 1))); }
 
 TFHE_DEV void cp_async16(void* sdst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc)
@@ -170,6 +188,30 @@ TFHE_DEV uint32_t mont_reduce(uint64_t v, const PrimeConst& pc) {
   const uint32_t mq = (uint32_t)v * pc.qneg_inv;
   const uint32_t t = (uint32_t)((v + (uint64_t)mq * pc.q) >> 32);
   return t >= pc.q ? t - pc.q : t;
+}
+
+// x = sum_{s=0..6} C_s 2^(8s) (C_s < 2^26, x < 2^76) -> x * 2^-64 mod q, by two
+// Montgomery rounds: A = C_0..C_3 part (< 2^51), t = A 2^-32 (< 2^30), then
+// u = t + C_4 + C_5 2^8 + C_6 2^16 (< 2^44, built on the ALU pipe) and
+// y = u 2^-32 < q + 2^12.  Four multiplies instead of seven 64-bit ones: the
+// epilogue is bound by the integer-multiply pipe.
+TFHE_DEV uint32_t fold_redc(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t c4,
+                            uint32_t c5, uint32_t c6, const PrimeConst& pc) {
+  const uint64_t A = (uint64_t)c0 + ((uint64_t)c1 << 8) + ((uint64_t)c2 << 16) + ((uint64_t)c3 << 24);
+  const uint32_t m0 = (uint32_t)A * pc.qneg_inv;
+  const uint32_t t = (uint32_t)((A + (uint64_t)m0 * pc.q) >> 32);
+  uint32_t lo, hi;
+  asm("{\n\t.reg .u32 s5, h5, s6, h6;\n\t"
+      "shl.b32 s5, %3, 8;\n\tshr.b32 h5, %3, 24;\n\t"
+      "shl.b32 s6, %4, 16;\n\tshr.b32 h6, %4, 16;\n\t"
+      "add.u32 %0, %2, %5;\n\t"
+      "add.cc.u32 %0, %0, s5;\n\taddc.u32 %1, h5, h6;\n\t"
+      "add.cc.u32 %0, %0, s6;\n\taddc.u32 %1, %1, 0;\n\t}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(c4), "r"(c5), "r"(c6), "r"(t));
+  const uint32_t m1 = lo * pc.qneg_inv;
+  const uint32_t y = (uint32_t)(((((uint64_t)hi << 32) | lo) + (uint64_t)m1 * pc.q) >> 32);
+  return y >= pc.q ? y - pc.q : y;
 }
 
 template <int STAGE, int K, int MODE>
@@ -213,16 +255,16 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], 128);
+      mbar_init(&acc_empty[s], 32 * kEpiWarps);
     }
-    mbar_init(tw_full, 128);
+    mbar_init(tw_full, 32 * kEpiWarps);
     for (int s = 0; s < kRaw; ++s) {
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], 128);
     }
     fence_mbar_init();
   }
-  if (warp == 8) tmem_alloc<512>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -233,7 +275,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
   // ptxas allocates every role's code under the matching setmaxnreg limit.
   if (warp < 4) {
     reg_dealloc<kRegsProducer>();
-    if (kDbg & 4) goto role_done;
+    if (kDbg & (4 | 512)) goto role_done;
     // ---------------------------------------------------------------- producers
     // Raw data chunks arrive by TMA (one elected thread, kRaw chunks in
     // flight) in a staging ring; the 4 producer warps byte-split them into the
@@ -260,17 +302,21 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
                     (it.sl * a.n_limbs + it.limb) * a.batch + it.b, &raw_full[slot]);
     };
     UnitIter ahead = w;
-    if (tid == 0) {
+    if (tid == 0 && !(kDbg & 32)) {
       for (int i = 0; i < kRaw && i < cnt; ++i, ahead.next(C, logR, R)) issue_raw(ahead, i);
     }
     for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
       const int rs = i % kRaw;
       const uint32_t rph = (uint32_t)((i / kRaw) & 1);
-      mbar_wait(&raw_full[rs], rph);
+      if (warp == 0) TS_TRACE(7, i);
+      if (!(kDbg & 32)) mbar_wait(&raw_full[rs], rph);
+      if (warp == 0) TS_TRACE(8, i);
       const uint8_t* rw = raw + rs * kRawBytes;
       if (i >= kRing) mbar_wait(&b_empty[w.s], w.rph ^ 1);
+      if (warp == 0) TS_TRACE(9, i);
       uint8_t* st = smem + w.s * kStageBytes;
-      if (STAGE == 1) {
+      if (kDbg & 16) {
+      } else if (STAGE == 1) {
 #pragma unroll
         for (int m = 0; m < K / 32; ++m) {
           const int k = krow0 + 32 * m;
@@ -303,43 +349,46 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       fence_proxy_async_smem();
       mbar_arrive(&b_full[w.s]);
       mbar_arrive(&raw_empty[rs]);
-      if (tid == 0 && i + kRaw < cnt) {
+      if (warp == 0) TS_TRACE(10, i);
+      if (tid == 0 && i + kRaw < cnt && !(kDbg & 32)) {
         // refill this raw slot once every producer thread has read it
         mbar_wait(&raw_empty[rs], rph);
         issue_raw(ahead, rs);
         ahead.next(C, logR, R);
       }
     }
-  } else if (warp < 8) {
+  } else if (warp < 4 + kEpiWarps) {
     reg_alloc<kRegsEpilogue>();
-    if (kDbg & 4) goto role_done;
+    if (kDbg & (4 | 1024)) goto role_done;
     // ---------------------------------------------------------------- epilogue
-    const int wq = warp & 3;
+    // Two warps per TMEM lane quarter (one per SMSP pair of the two epilogue
+    // warpgroups): warp 4 + 4 hf + wq owns rows wq*32..+31 and chunk columns
+    // [8 hf, 8 hf + 8).  Two independent warps per SMSP hide the latency of the
+    // 64-bit fold / Montgomery chains that one warp alone stalls on.
+    const int wq = warp & 3, hf = (warp - 4) >> 2, cb = hf * kCW;
     const int m = wq * 32 + lane;          // TMEM lane = twiddle row within the half
-    const int r_tw = h * 128 + m;          // global twiddle row (k1 or k2)
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    uint8_t* wstg = stg + wq * kWarpStg;   // in[2][4] tiles | out[2] tiles (2 KB each)
+    uint8_t* wstg = stg + (warp - 4) * kWarpStg;   // in[2][4] tiles | out[2] tiles (1 KB each)
     constexpr int mode = STAGE == 2 ? MODE : EPI_STORE;
-    // Stage-2 epilogue operands (x/base rows, key rows, accumulators) are
+    // Epilogue operands (W2 tile, x/base rows, key rows, accumulators) are
     // fetched one chunk ahead with cp.async into a double-buffered staging
-    // area (4 lanes per 64-byte row = coalesced), stage 1's W2 with 16
-    // warp-coalesced loads into registers.
+    // area: 32 rows x 32 bytes per tile, 2 lanes per row (full sectors).
     auto prefetch = [&](const UnitIter& it, int buf) {
+      uint8_t* dstb = wstg + buf * 4096;
       if (STAGE == 1) {
-        // W2 * R^2 in [prime][i2][k1] layout: for each of the chunk's 16 i2
+        // W2 * 2^96 in [prime][i2][k1] layout: for each of this warp's 8 i2
         // columns the warp's 32 k1 rows are 128 contiguous bytes -> staged as
-        // [16][32] words (one 16-byte cp.async per lane per 512 bytes)
+        // [8][32] words
         const int pr = a.map.prime[it.limb];
-        const uint32_t* wp = a.w2 + (size_t)pr * a.n + (size_t)it.x0 * a.n1 + h * 128 + wq * 32;
-        uint8_t* dstb = wstg + buf * 8192;
+        const uint32_t* wp = a.w2 + (size_t)pr * a.n + (size_t)(it.x0 + cb) * a.n1 + h * 128 + wq * 32;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 2; ++q) {
           const int idx = q * 32 + lane, e = idx >> 3, part = idx & 7;
           cp_async16(dstb + e * 128 + part * 16, wp + (size_t)e * a.n1 + part * 4);
         }
         return;
       }
-      const size_t wrow = (size_t)(h * 128 + wq * 32) * a.n1 + it.x0;  // warp's first row
+      const size_t wrow = (size_t)(h * 128 + wq * 32) * a.n1 + it.x0 + cb;  // warp's first row
       const uint32_t* src[4] = {nullptr, nullptr, nullptr, nullptr};
       if (mode == EPI_SUB_SCALE) {
         src[0] = a.epi.x + ((size_t)a.epi.x_row[it.limb] * a.batch + it.b) * a.n + wrow;
@@ -365,55 +414,60 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
           src[3] = a.epi.acc_a + ar;
         }
       }
-      uint8_t* dstb = wstg + buf * 8192;
 #pragma unroll
       for (int tI = 0; tI < 4; ++tI) {
         if (!src[tI]) continue;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int r = 8 * q + (lane >> 2), p = lane & 3;
-          cp_async16(dstb + tI * 2048 + stg_off(r, p), src[tI] + (size_t)r * a.n1 + 4 * p);
+        for (int q = 0; q < 2; ++q) {
+          const int r = 16 * q + (lane >> 1), p = lane & 1;
+          cp_async16(dstb + tI * 1024 + stg8_off(r, p), src[tI] + (size_t)r * a.n1 + 4 * p);
         }
       }
     };
-    auto read_row = [&](int buf, int tI, uint32_t (&v)[16]) {
-      const uint8_t* t = wstg + buf * 8192 + tI * 2048;
+    auto read_row = [&](int buf, int tI, uint32_t (&v)[kCW]) {
+      const uint8_t* t = wstg + buf * 4096 + tI * 1024;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 u = *reinterpret_cast<const uint4*>(t + stg_off(lane, q));
+      for (int q = 0; q < 2; ++q) {
+        uint4 u = *reinterpret_cast<const uint4*>(t + stg8_off(lane, q));
         v[4 * q] = u.x; v[4 * q + 1] = u.y; v[4 * q + 2] = u.z; v[4 * q + 3] = u.w;
       }
     };
-    // coalesced store of this warp's 32 rows x 16 values (row stride in elements)
-    auto store_tile = [&](int oI, const uint32_t (&v)[16], uint32_t* dst, size_t row_stride) {
-      uint8_t* t = wstg + 16384 + oI * 2048;
+    // coalesced store of this warp's 32 rows x 8 values (row stride in elements):
+    // transposed through smem so each store instruction writes 16 full sectors
+    auto store_tile = [&](int oI, const uint32_t (&v)[kCW], uint32_t* dst, size_t row_stride) {
+      uint8_t* t = wstg + 8192 + oI * 1024;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<uint4*>(t + stg_off(lane, q)) =
+      for (int q = 0; q < 2; ++q)
+        *reinterpret_cast<uint4*>(t + stg8_off(lane, q)) =
             make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       __syncwarp();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = 8 * q + (lane >> 2), p = lane & 3;
+      for (int q = 0; q < 2; ++q) {
+        const int r = 16 * q + (lane >> 1), p = lane & 1;
         *reinterpret_cast<uint4*>(dst + (size_t)r * row_stride + 4 * p) =
-            *reinterpret_cast<const uint4*>(t + stg_off(r, p));
+            *reinterpret_cast<const uint4*>(t + stg8_off(r, p));
       }
     };
     UnitIter ahead = w;
-    if (cnt > 0) prefetch(ahead, 0);
-    uint32_t regb[16], rega[16];   // EPI_KS_ACC group accumulators
+    if (cnt > 0 && !(kDbg & 64)) prefetch(ahead, 0);
+    uint32_t regb[kCW], rega[kCW];   // EPI_KS_ACC group accumulators
     cp_async_commit();
     int prev = -1;
+    PrimeConst pc;
     for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
       const int limb = w.limb;
       const int prime = a.map.prime[limb];
       const int buf = i & 1;
       if (limb != prev) {
-        // load this (limb, half)'s twiddle planes into TMEM columns [0, K)
+        // per-prime constants stay in registers for the whole limb (a
+        // per-chunk global load would sit on the fold's critical path)
+        pc = a.pc[prime];
+        // load this (limb, half)'s twiddle planes into TMEM columns [0, K):
+        // each of the quarter's two warps writes half of the columns
         prev = limb;
         const uint32_t* src = a.twa + (((size_t)prime * a.H + h) * 128 + m) * K;
 #pragma unroll 1
-        for (int w0 = 0; w0 < K; w0 += 16) {
+        for (int w0 = hf * (K / 2); w0 < (hf + 1) * (K / 2) && !(kDbg & 2048); w0 += 16) {
           uint32_t r[16];
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
@@ -426,65 +480,64 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
         tc_fence_before();
         mbar_arrive(tw_full);
       }
-      const PrimeConst pc = a.pc[prime];
       const int b = w.b;
       __syncwarp();  // every lane is done with the staging buffer about to be refilled
       if (i + 1 < cnt) {
         ahead.next(C, logR, R);
-        prefetch(ahead, buf ^ 1);
+        if (!(kDbg & 64)) prefetch(ahead, buf ^ 1);
       }
       cp_async_commit();
-      mbar_wait(&acc_full[w.ab], w.aph);
-      tc_fence_after();
-      // all 7 x 16 accumulators are read back-to-back and the TMEM buffer is
-      // released before any math (the MMA of chunk i+2 waits on it)
-      const uint32_t abase = tmem + lane_off + (w.ab ? kAccCol1 : kAccCol0);
-      uint32_t acc[7][16];
+      if (warp == 4 || warp == 8) TS_TRACE(warp == 4 ? 4 : 11, i);
+      if (!(kDbg & 4096)) mbar_wait(&acc_full[w.ab], w.aph);
+      if (warp == 4 || warp == 8) TS_TRACE(warp == 4 ? 5 : 12, i);
+      if (!(kDbg & 16384)) tc_fence_after();
+      // all 7 x 8 accumulators are read back-to-back and this warp's share of
+      // the TMEM buffer is released before any math
+      const uint32_t abase = tmem + lane_off + (w.ab ? kAccCol1 : kAccCol0) + cb;
+      uint32_t acc[7][kCW];
       if (!(kDbg & 8)) {
 #pragma unroll
-        for (int s = 0; s < 7; ++s) tmem_ld16(abase + 16 * s, acc[s]);
+        for (int s = 0; s < 7; ++s) tmem_ld8(abase + 16 * s, acc[s]);
         tmem_ld_wait();
+        if (warp == 4) TS_TRACE(6, i);
       } else {
 #pragma unroll
         for (int s = 0; s < 7; ++s)
 #pragma unroll
-          for (int e = 0; e < 16; ++e) acc[s][e] = s + e;
+          for (int e = 0; e < kCW; ++e) acc[s][e] = s + e;
       }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[w.ab]);
-      uint32_t y[16];
+      if (!(kDbg & 16384)) tc_fence_before();
+      if (!(kDbg & 32768)) mbar_arrive(&acc_empty[w.ab]);
+      if (kDbg & 8192) continue;
+      uint32_t y[kCW];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        // x = sum_s C_s 2^(8s) (powers of two up to 2^24 as shifts, 2^(8s)
-        // mod q for s >= 4) < 2^60, then one Montgomery step:
-        // y = x R^-1 mod q (R = 2^32; the twiddles carry the R back)
-        uint64_t v = (uint64_t)acc[0][e] + ((uint64_t)acc[1][e] << 8) +
-                     ((uint64_t)acc[2][e] << 16) + ((uint64_t)acc[3][e] << 24);
-        v += (uint64_t)acc[4][e] * pc.r[0];
-        v += (uint64_t)acc[5][e] * pc.r[1];
-        v += (uint64_t)acc[6][e] * pc.r[2];
-        y[e] = mont_reduce(v, pc);
+      for (int e = 0; e < kCW; ++e) {
+        // y = (sum_s C_s 2^(8s)) * 2^-64 mod q (the twiddles carry the 2^64 back)
+        y[e] = fold_redc(acc[0][e], acc[1][e], acc[2][e], acc[3][e], acc[4][e], acc[5][e],
+                         acc[6][e], pc);
       }
+      if (warp == 4) TS_TRACE(15, i);
       if (kDbg & 2) {
-        if (y[0] == 0x7fffffff && y[15] == 1) a.out[0] = 0;  // keep the work live
+        if (y[0] == 0x7fffffff && y[kCW - 1] == 1) a.out[0] = 0;  // keep the work live
         continue;
       }
       cp_async_wait1();   // this chunk's operand tiles have landed (own copies)
       __syncwarp();       // ... and every lane's copies are visible
       if (STAGE == 1) {
-        const uint8_t* wt = wstg + buf * 8192;
+        const uint8_t* wt = wstg + buf * 4096;
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
+        for (int e = 0; e < kCW; ++e)
           y[e] = mont_reduce((uint64_t)y[e] * *reinterpret_cast<const uint32_t*>(wt + e * 128 + lane * 4), pc);
-        // blocked P layout [limb][b][i2/16][k1][16]: the warp's rows are 2 KB contiguous
+        // blocked P layout [limb][b][i2/16][k1][16]: the warp's rows are 64 B apart
         uint32_t* dst = a.out + (((size_t)limb * a.batch + b) * (a.n2 / kNC) + w.x0 / kNC) * kNC * a.n1 +
-                        (size_t)(h * 128 + wq * 32) * kNC;
+                        (size_t)(h * 128 + wq * 32) * kNC + cb;
         store_tile(0, y, dst, kNC);
+        if (warp == 4 || warp == 8) TS_TRACE(warp == 4 ? 13 : 14, i);
         continue;
       }
-      const size_t wrow = (size_t)(h * 128 + wq * 32) * a.n1 + w.x0;
+      const size_t wrow = (size_t)(h * 128 + wq * 32) * a.n1 + w.x0 + cb;
       if (mode == EPI_KS_ACC) {
-        // y is in Montgomery form (twiddles carry R^2); the S slices of this
+        // y is in Montgomery form (twiddles carry 2^96); the S slices of this
         // (target, chunk) group accumulate in registers, acc touches HBM once
         if (w.sl == 0) {
           if (a.epi.init_acc[limb]) {
@@ -492,15 +545,15 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
             read_row(buf, 3, rega);
           } else {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) regb[e] = rega[e] = 0;
+            for (int e = 0; e < kCW; ++e) regb[e] = rega[e] = 0;
           }
         }
         if (a.epi.j0 + w.sl != a.epi.js[limb]) {
-          uint32_t kb[16], ka[16];
+          uint32_t kb[kCW], ka[kCW];
           read_row(buf, 0, kb);
           read_row(buf, 1, ka);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
+          for (int e = 0; e < kCW; ++e) {
             regb[e] = add_mod(regb[e], mont_reduce((uint64_t)y[e] * kb[e], pc), pc.q);
             rega[e] = add_mod(rega[e], mont_reduce((uint64_t)y[e] * ka[e], pc), pc.q);
           }
@@ -513,9 +566,9 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
         continue;
       }
       if (mode == EPI_KS_MAC) {
-        // y is in Montgomery form (y R: twiddles carry R^2), so one Montgomery
+        // y is in Montgomery form (y R: twiddles carry 2^96), so one Montgomery
         // product per key gives y * k exactly
-        uint32_t kb[16], ka[16], ob[16], oa[16];
+        uint32_t kb[kCW], ka[kCW], ob[kCW], oa[kCW];
         read_row(buf, 0, kb);
         read_row(buf, 1, ka);
         if (!a.epi.first) {
@@ -523,7 +576,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
           read_row(buf, 3, oa);
         }
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
+        for (int e = 0; e < kCW; ++e) {
           const uint32_t tb = mont_reduce((uint64_t)y[e] * kb[e], pc);
           const uint32_t ta = mont_reduce((uint64_t)y[e] * ka[e], pc);
           ob[e] = a.epi.first ? tb : add_mod(ob[e], tb, pc.q);
@@ -535,23 +588,25 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
         continue;
       }
       if (mode == EPI_SUB_SCALE) {
-        uint32_t xrow[16], brow[16];
+        uint32_t xrow[kCW], brow[kCW];
         read_row(buf, 0, xrow);
         const bool has_base = a.epi.base_row[limb] >= 0;
         if (has_base) read_row(buf, 1, brow);
         const uint32_t s = a.epi.s[limb], sp = a.epi.s_shoup[limb];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
+        for (int e = 0; e < kCW; ++e) {
           uint32_t t = mul_shoup(sub_mod(xrow[e], y[e], pc.q), s, sp, pc.q);
           y[e] = has_base ? add_mod(brow[e], t, pc.q) : t;
         }
       }
       store_tile(0, y, a.out + ((size_t)a.map.out_row[limb] * a.batch + b) * a.n + wrow, a.n1);
+      if (warp == 4) TS_TRACE(13, i);
     }
     cp_async_wait0();
   } else {
     reg_dealloc<kRegsMma>();
-    if (warp != 8) goto role_done;
+    if (warp >= kMmaWarp + kMmaIssuers) goto role_done;
+    const int mw = warp - kMmaWarp;   // this issuer owns the chunks i = mw (mod kMmaIssuers)
     // ---------------------------------------------------------------- MMA issuer
     // The whole warp walks the loop (so descriptors stay warp-uniform and live
     // in uniform registers); one elected lane issues the tcgen05 ops.
@@ -591,8 +646,8 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     // data / accumulator readiness of chunk `it` (index i)
     auto wait_ready = [&](const UnitIter& it, int i) {
       if (!handshake) return;
-      mbar_wait(&b_full[it.s], it.rph);
-      if (i >= 2) mbar_wait(&acc_empty[it.ab], it.aph ^ 1);
+      if (!(kDbg & 256)) mbar_wait(&b_full[it.s], it.rph);
+      if (i >= 2 && !(kDbg & 128)) mbar_wait(&acc_empty[it.ab], it.aph ^ 1);
     };
     int prev = -1;
     uint32_t twph = 0;
@@ -600,17 +655,21 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       if (w.limb != prev) {
         if (handshake) {
           if (prev >= 0) twph ^= 1;
-          mbar_wait(tw_full, twph);
+          if (!(kDbg & 1024)) mbar_wait(tw_full, twph);
         }
         prev = w.limb;
       }
+      if (kMmaIssuers > 1 && (i % kMmaIssuers) != mw) continue;
+      TS_TRACE(0, i);
       wait_ready(w, i);
+      TS_TRACE(1, i);
       tc_fence_after();
       if (elect_one()) {
         issue(w, 0, KC);
         mma_commit(&b_empty[w.s]);
         mma_commit(&acc_full[w.ab]);
       }
+      TS_TRACE(2, i);
       __syncwarp();
     }
   }
@@ -618,7 +677,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
 role_done:
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -635,7 +694,26 @@ int launch_ts(const Ctx& c, TsArgs& a, cudaStream_t st) {
   if (a.H == 2) grid = 2 * (int)std::min<long long>(c.sms / 2, U);
   else grid = (int)std::min<long long>(c.sms, U);
   if (grid <= 0) return 0;
+#ifdef TFHE_TS_TRACE
+  static unsigned long long* tbuf = nullptr;
+  if (!tbuf) cudaMalloc(&tbuf, 16 * kTraceN * 8);
+  cudaMemset(tbuf, 0, 16 * kTraceN * 8);
+  a.trace = tbuf;
+#endif
   kern<<<grid, kThreadsTS, smem, st>>>(a);
+#ifdef TFHE_TS_TRACE
+  {
+    std::vector<unsigned long long> h(16 * kTraceN);
+    cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost);
+    static int seq = 0;
+    char fn[256];
+    snprintf(fn, sizeof(fn), "gpurun_out/trace_s%d_%d.bin", STAGE, seq++);
+    if (FILE* f = fopen(fn, "wb")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
+#endif
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("ntt ts launch: ") + cudaGetErrorString(e));
@@ -748,7 +826,7 @@ int build_ts_tables(Ctx& c) {
   const uint64_t two_n = 2ull * n;
   std::vector<uint32_t> pw(two_n);
   // variants 0..3: (inv, stage) = (v>>1, v&1); variant 4: forward stage 2
-  // scaled by R^2 for the fused key-switch MAC epilogue
+  // scaled by 2^96 for the fused key-switch MAC epilogue
   for (int var = 0; var < 5; ++var) {
       const int inv = var < 4 ? var >> 1 : 0, s = var < 4 ? var & 1 : 1;
       const bool ks = var == 4;
@@ -774,8 +852,8 @@ int build_ts_tables(Ctx& c) {
                 ex = inv ? (uint64_t)n1 * (2ull * k * r + r) : (uint64_t)n1 * (2ull * k * r);
               uint32_t v = pw[ex % two_n];
               if (s == 1 && inv) v = mulmod_h(v, n_inv, q);
-              // stage 2 twiddles carry R = 2^32: the Montgomery epilogue divides it out
-              if (s == 1) v = (uint32_t)(((uint64_t)v << 32) % q);
+              // stage 2 twiddles carry 2^64: the two-round Montgomery fold divides it out
+              if (s == 1) v = (uint32_t)(((((uint64_t)v << 32) % q) << 32) % q);
               if (ks) v = (uint32_t)(((uint64_t)v << 32) % q);
               for (int i = 0; i < 4; ++i) words[i] |= ((v >> (8 * i)) & 0xFFu) << (8 * e);
             }
@@ -791,8 +869,8 @@ int build_ts_tables(Ctx& c) {
         return 3;
       }
   }
-  // W2 * R^2 mod q in [prime][i2/16][e][k1] layout: stage 1 multiplies its
-  // Montgomery result (S R^-1) by this with another Montgomery step -> S * W2;
+  // W2 * 2^96 mod q in [prime][i2/16][e][k1] layout: stage 1 multiplies its
+  // folded result (S 2^-64) by this with another Montgomery step -> S * W2;
   // the layout makes the epilogue's per-row loads warp-coalesced
   for (int inv = 0; inv < 2; ++inv) {
     std::vector<uint32_t> w2((size_t)np * n), w2t((size_t)np * n);
@@ -802,10 +880,10 @@ int build_ts_tables(Ctx& c) {
     }
     for (int p = 0; p < np; ++p) {
       const uint32_t q = c.primes[p];
-      const uint64_t r2 = ((uint64_t)1 << 32) % q * (((uint64_t)1 << 32) % q) % q;
+      const uint64_t r1 = ((uint64_t)1 << 32) % q, r3 = r1 * r1 % q * r1 % q;
       for (int k1 = 0; k1 < n1; ++k1)
         for (int i2 = 0; i2 < n2; ++i2) {
-          const uint64_t v = (uint64_t)w2[(size_t)p * n + (size_t)k1 * n2 + i2] * r2 % q;
+          const uint64_t v = (uint64_t)w2[(size_t)p * n + (size_t)k1 * n2 + i2] * r3 % q;
           w2t[(size_t)p * n + ((size_t)(i2 / 16) * 16 + (i2 % 16)) * n1 + k1] = (uint32_t)v;
         }
     }

@@ -82,11 +82,11 @@ struct Ctx {
   // twiddle-resident (TS) kernel: per [inverse][stage] words
   // [prime][half][row 128][plane 4][K/4], used when n1 >= 128
   uint32_t* d_twa[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  // stage-1 hadamard twiddles pre-scaled by R = 2^32 (Montgomery epilogue), + Shoup
+  // stage-1 hadamard twiddles (W2 * 2^96, transposed) for the TS epilogue
   uint32_t* d_w2r[2] = {nullptr, nullptr};
   uint32_t* d_w2rs[2] = {nullptr, nullptr};
-  // forward stage-2 twiddle planes scaled by R^2 (not R): the stage-2 result
-  // is then y*R, the Montgomery form the fused key-switch MAC multiplies with
+  // forward stage-2 twiddle planes scaled by 2^96 (not 2^64): the stage-2 result
+  // is then y*2^32, the Montgomery form the fused key-switch MAC multiplies with
   uint32_t* d_twa_ks = nullptr;
   bool use_ts = false;
   int sms = 148;
