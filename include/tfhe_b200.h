@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define TFHE_ABI_VERSION 1
+#define TFHE_ABI_VERSION 2
 #define TFHE_OK 0
 #define TFHE_EINVAL 2
 #define TFHE_ECUDA 3
@@ -123,6 +123,37 @@ int tfhe_hrotate(TfheCtx* ctx, const uint32_t* ct, int level, int batch, uint32_
                  const uint32_t* key, int dnum, uint32_t* out, void* ws, size_t ws_bytes,
                  void* stream);
 /* hadd / hsub (ckks.py:246-256) are tfhe_eltwise over the 2*(level+1) rows. */
+
+/* ---- limb-partitioned evaluation (optional multi-GPU mode) ----
+ * Each of G ranks owns the chain rows [row_lo, row_lo + n_rows) of every
+ * ciphertext.  Only the key switch needs other ranks' data: the caller
+ * INTTs its own rows of d (tfhe_ntt, inverse), all-gathers them (one NCCL
+ * all-gather per key switch) into y_full = (level+1, batch, n) coefficient
+ * rows, and every rank then raises ALL slices to its own rows plus the K
+ * specials (specials computed redundantly, no second collective) and does
+ * ModDown locally.  Concatenating the ranks' outputs equals the
+ * unpartitioned call (ckks.key_switch, ckks.py:321-381) bit for bit.
+ *
+ * tfhe_tensor_product: hmult's d0 = b0 b1, d1 = a0 b1 + a1 b0, d2 = a0 a1
+ *   (ckks.py:265-271) over local rows: ct (2, n_rows, batch, n) ->
+ *   out (3, n_rows, batch, n).
+ * tfhe_keyswitch_part: d_local (n_rows, batch, n) NTT domain, y_full as
+ *   above -> out (2, n_rows, batch, n); with `add`, its first add_components
+ *   (1: b only, as hrotate's phi(b); 2: both, as hmult's d0/d1) of
+ *   (2, n_rows, batch, n) are added.
+ * tfhe_rescale_part: ct_local (2, n_rows, batch, n) and top_coeff = the
+ *   INTT of both components' top limb (2, batch, n), broadcast by its owner
+ *   -> out (2, n_keep, batch, n), n_keep = local rows below `level`
+ *   (_rescale_poly, ckks.py:301-311). */
+int tfhe_tensor_product(TfheCtx* ctx, const uint32_t* ct0, const uint32_t* ct1, int row_lo,
+                        int n_rows, int batch, uint32_t* out, void* stream);
+int tfhe_keyswitch_part(TfheCtx* ctx, const uint32_t* d_local, const uint32_t* y_full, int level,
+                        int batch, const uint32_t* key, int dnum, int row_lo, int n_rows,
+                        uint32_t* out, const uint32_t* add, int add_components, void* ws,
+                        size_t ws_bytes, void* stream);
+int tfhe_rescale_part(TfheCtx* ctx, const uint32_t* ct_local, const uint32_t* top_coeff,
+                      int level, int batch, int row_lo, int n_rows, uint32_t* out, void* ws,
+                      size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -292,6 +292,45 @@ def key_switch(d, basis, key, chain_q, chain_p, alpha, dnum, threads=None):
             mod_down(acc_a, ext, basis, tuple(chain_p), threads))
 
 
+def key_switch_part(d_local, y_full, basis, lo, key, chain_q, chain_p, alpha, dnum,
+                    threads=None):
+    """Limb-partitioned key switch restated on the CPU: the rank
+    owning chain rows [lo, lo + len(d_local)) of `basis` raises every GKS
+    slice of the gathered coefficient rows y_full to its own primes plus the
+    specials, accumulates against the key and does ModDown to its own rows.
+    Equals key_switch(...)[:, lo:lo+n] (ckks.py:321-381)."""
+    basis = tuple(basis)
+    level = len(basis) - 1
+    n_loc = d_local.shape[0]
+    own = basis[lo:lo + n_loc]
+    tgt = own + tuple(chain_p)
+    full_ext = tuple(chain_q) + tuple(chain_p)
+    acc_b = np.zeros((len(tgt),) + d_local.shape[1:], dtype=np.uint32)
+    acc_a = np.zeros_like(acc_b)
+    for j in range(dnum):
+        s0 = j * alpha
+        if s0 > level:
+            break
+        s1 = min((j + 1) * alpha, level + 1)
+        sl_basis = basis[s0:s1]
+        raised = np.empty_like(acc_b)
+        for t, q in enumerate(tgt):
+            if q in sl_basis:          # slice rows reused unchanged (ckks.py:361-364)
+                raised[t] = d_local[own.index(q)]
+            else:
+                conv = fast_basis_conv(y_full[s0:s1], sl_basis, (q,))
+                raised[t] = ntt(conv, (q,), threads)[0]
+        kb = _key_rows(key[j][0], full_ext, tgt)
+        ka = _key_rows(key[j][1], full_ext, tgt)
+        if raised.ndim > 2:
+            kb = kb.reshape(kb.shape[:1] + (1,) * (raised.ndim - 2) + kb.shape[1:])
+            ka = ka.reshape(kb.shape)
+        acc_b = ele_add(acc_b, hada_mult(raised, kb, tgt), tgt)
+        acc_a = ele_add(acc_a, hada_mult(raised, ka, tgt), tgt)
+    return (mod_down(acc_b, tgt, own, tuple(chain_p), threads),
+            mod_down(acc_a, tgt, own, tuple(chain_p), threads))
+
+
 def hmult(b0, a0, b1, a1, basis, rlk, chain_q, chain_p, alpha, dnum, threads=None):
     """ckks.py:265-274 -> (b, a)"""
     d0 = hada_mult(b0, b1, basis)

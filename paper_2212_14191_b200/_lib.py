@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 #: in-tree build; TFHE_B200_LIB may point at another build of the same ABI
 #: (A/B performance experiments)
 LIB_PATH = os.environ.get("TFHE_B200_LIB") or os.path.join(_HERE, "libtfhe_b200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 EINVAL = 2
 ECUDA = 3
@@ -55,6 +55,13 @@ SIGNATURES = {
                                     ctypes.c_size_t, _vp]),
     "tfhe_hrotate": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint32, _vp,
                                     ctypes.c_int, _vp, _vp, ctypes.c_size_t, _vp]),
+    "tfhe_tensor_product": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int, _vp, _vp]),
+    "tfhe_keyswitch_part": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp,
+                                           ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp,
+                                           ctypes.c_int, _vp, ctypes.c_size_t, _vp]),
+    "tfhe_rescale_part": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, _vp, _vp, ctypes.c_size_t, _vp]),
 }
 
 _lib = None

@@ -54,20 +54,29 @@ struct Carve {
   }
 };
 
+// Key-switch geometry.  Targets are the extended-basis rows a call produces:
+// the local chain rows [r0, r0 + nr) then the K special rows (T = nr + K).
+// The unpartitioned key switch has r0 = 0, nr = level + 1 (T = E); the
+// limb-partitioned one gives each rank its own chain rows and
+// every rank the specials.
 struct CkksGeom {
   int Lc, K, alpha, l1, E;
+  int r0, nr, T;
   bool need_conv;
   int nslices;   // non-empty GKS slices at this level
   int S;         // slices per fused key-switch group (TS path), 1 otherwise
 };
 
-CkksGeom geom(const TfheCtx* h, int level, int dnum) {
+CkksGeom geom(const TfheCtx* h, int level, int dnum, int r0 = 0, int nr = -1) {
   CkksGeom g;
   g.Lc = h->n_chain;
   g.K = h->n_special;
   g.alpha = dnum > 0 ? g.Lc / dnum : 1;
   g.l1 = level + 1;
   g.E = g.l1 + g.K;
+  g.r0 = r0;
+  g.nr = nr < 0 ? g.l1 : nr;
+  g.T = g.nr + g.K;
   g.need_conv = g.alpha > 1 || g.K > 1;
   g.nslices = (g.l1 + g.alpha - 1) / g.alpha;
   g.S = 1;
@@ -75,7 +84,7 @@ CkksGeom geom(const TfheCtx* h, int level, int dnum) {
 }
 
 // slices per key-switch group: bounded by the launch limb map and by an
-// 8 GiB cap on the (S * E, batch, n) stage-1 workspace
+// 8 GiB cap on the (S * T, batch, n) stage-1 workspace
 void set_group(CkksGeom& g, const Ctx& c, int batch) {
   if (!c.use_ts) {
     g.S = 1;
@@ -83,19 +92,21 @@ void set_group(CkksGeom& g, const Ctx& c, int batch) {
   }
   const size_t row_bytes = (size_t)batch * c.n * 4;
   const size_t cap = (size_t)8 << 30;
-  int s_mem = (int)std::max<size_t>(1, cap / (row_bytes * g.E));
-  g.S = std::max(1, std::min({g.nslices, kMaxLimbs / g.E, s_mem}));
+  int s_mem = (int)std::max<size_t>(1, cap / (row_bytes * g.T));
+  g.S = std::max(1, std::min({g.nslices, kMaxLimbs / g.T, s_mem}));
 }
 
-// prime index of extended-basis position r at level (chain 0..level, then specials)
-inline int ext_prime(const CkksGeom& g, int r) { return r < g.l1 ? r : g.Lc + (r - g.l1); }
+// prime index of target t (local chain rows, then specials)
+inline int tprime(const CkksGeom& g, int t) { return t < g.nr ? g.r0 + t : g.Lc + (t - g.nr); }
 
-int ks_ntt_rows(const CkksGeom& g) { return std::max({g.S * g.E, g.E, 2 * g.l1, 2 * g.K}); }
-int ks_conv_rows(const CkksGeom& g) { return std::max({g.S * g.E, g.E, 2 * g.l1}); }
+int ks_ntt_rows(const CkksGeom& g) {
+  return std::max({g.S * g.T, g.T, g.l1, 2 * g.nr, 2 * g.K});
+}
+int ks_conv_rows(const CkksGeom& g) { return std::max({g.S * g.T, g.T, 2 * g.nr}); }
 
 size_t ks_bytes(const CkksGeom& g, int batch, int n) {
   const size_t U = (size_t)batch * n * 4;
-  size_t rows = g.l1 /*y*/ + 2 * g.E /*acc*/ + ks_ntt_rows(g) /*ntt ws*/ + 2 * g.K /*ysp*/ +
+  size_t rows = g.l1 /*y*/ + 2 * g.T /*acc*/ + ks_ntt_rows(g) /*ntt ws*/ + 2 * g.K /*ysp*/ +
                 (g.need_conv ? ks_conv_rows(g) : 0);
   return rows * U + 16 * 256;
 }
@@ -134,16 +145,20 @@ int fill_bconv(const Ctx& c, const std::vector<int>& src, const std::vector<int>
   return 0;
 }
 
-// key switch of d (l1, B, n) -> out (2, l1, B, n) [+ add rows base_row]
-int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const uint32_t* key,
-                   int dnum, uint32_t* out, const uint32_t* base, const int16_t* base_rows,
-                   Carve& cv, cudaStream_t st) {
+// key switch of the local rows d (nr, B, n; chain rows [r0, r0+nr), NTT
+// domain) -> out (2, nr, B, n) [+ add rows base_rows[]].  y_full is the
+// coefficient-domain d over ALL level+1 chain rows (the all-gathered INTT of
+// the limb-partitioned key switch); NULL = compute it here from d, which then
+// must hold every chain row (r0 = 0, nr = level + 1).
+int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int level, int batch,
+                   const uint32_t* key, int dnum, int r0, int nr, uint32_t* out,
+                   const uint32_t* base, const int16_t* base_rows, Carve& cv, cudaStream_t st) {
   const Ctx& c = h->c;
-  CkksGeom g = geom(h, level, dnum);
+  CkksGeom g = geom(h, level, dnum, r0, nr);
   set_group(g, c, batch);
   const size_t U = (size_t)batch * c.n;  // elements per limb row
-  uint32_t* y = cv.take<uint32_t>(g.l1 * U * 4);
-  uint32_t* acc = cv.take<uint32_t>(2 * g.E * U * 4);
+  uint32_t* y = y_full ? nullptr : cv.take<uint32_t>(g.l1 * U * 4);
+  uint32_t* acc = cv.take<uint32_t>(2 * g.T * U * 4);
   const size_t ntt_ws_bytes = ks_ntt_rows(g) * U * 4;
   uint32_t* ntt_ws = cv.take<uint32_t>(ntt_ws_bytes);
   uint32_t* ysp = cv.take<uint32_t>(2 * g.K * U * 4);
@@ -156,68 +171,74 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
   int rc;
 
   // 1. y = INTT(d), every limb of the level  (ModUp's to_coeff, ckks.py:362)
-  LimbMap m;
-  m.n = g.l1;
-  for (int r = 0; r < g.l1; ++r) m.prime[r] = m.in_row[r] = m.out_row[r] = (int16_t)r;
-  if ((rc = launch_ntt(c, d, y, m, batch, 1, nullptr, ntt_ws, ntt_ws_bytes, st))) return rc;
+  if (!y_full) {
+    if (r0 != 0 || nr != g.l1) {
+      set_error("key switch of a limb subset needs the gathered coefficient rows");
+      return TFHE_EINVAL;
+    }
+    LimbMap m;
+    m.n = g.l1;
+    for (int r = 0; r < g.l1; ++r) m.prime[r] = m.in_row[r] = m.out_row[r] = (int16_t)r;
+    if ((rc = launch_ntt(c, d, y, m, batch, 1, nullptr, ntt_ws, ntt_ws_bytes, st))) return rc;
+    y_full = y;
+  }
 
   // 2. ModUp + inner product  (ckks.py:337-351)
   int16_t row_prime[kMaxRows];
-  int32_t key_row[kMaxRows];
-  for (int r = 0; r < g.E; ++r) {
-    row_prime[r] = (int16_t)ext_prime(g, r);
-    key_row[r] = ext_prime(g, r);  // key rows are over the full ext basis
-  }
+  for (int t = 0; t < g.nr; ++t) row_prime[t] = (int16_t)(g.r0 + t);
   if (c.use_ts) {
     // 2a. slice rows are reused unchanged (ckks.py:361-364): acc[r] = d_r * k_{slice(r)}[r]
     int64_t key_off[kMaxRows];
-    for (int r = 0; r < g.l1; ++r) key_off[r] = (int64_t)(r / g.alpha) * key_pair + (int64_t)r * c.n;
-    if ((rc = launch_ks_mac(c, d, key, key + key_pair / 2, acc, acc + g.E * U, row_prime, key_off,
-                            g.l1, batch, 1, st)))
+    for (int t = 0; t < g.nr; ++t) {
+      const int r = g.r0 + t;
+      key_off[t] = (int64_t)(r / g.alpha) * key_pair + (int64_t)r * c.n;
+    }
+    if ((rc = launch_ks_mac(c, d, key, key + key_pair / 2, acc, acc + g.T * U, row_prime, key_off,
+                            g.nr, batch, 1, st)))
       return rc;
     // 2b. groups of S slices: stage 1 for every (slice, target) pair, stage 2
-    // accumulates the S slices of each target on chip (EPI_KS_ACC).  Targets
-    // are all E extended rows; a slice's own rows are skipped in the sum.
+    // accumulates the S slices of each target on chip (EPI_KS_ACC).  A
+    // slice's own rows are skipped in the sum (they were reused in 2a).
     LimbMap tmap;
-    tmap.n = g.E;
+    tmap.n = g.T;
     EpiArgs ek;
     memset(&ek, 0, sizeof(ek));
     ek.mode = EPI_KS_ACC;
     ek.key = key;
     ek.key_pair = (long long)key_pair;
     ek.acc_b = acc;
-    ek.acc_a = acc + g.E * U;
-    for (int t = 0; t < g.E; ++t) {
-      tmap.prime[t] = (int16_t)ext_prime(g, t);
+    ek.acc_a = acc + g.T * U;
+    for (int t = 0; t < g.T; ++t) {
+      tmap.prime[t] = (int16_t)tprime(g, t);
       tmap.in_row[t] = (int16_t)t;
       tmap.out_row[t] = (int16_t)t;
-      ek.key_row[t] = (int16_t)key_row[t];
-      ek.js[t] = (int16_t)(t < g.l1 ? t / g.alpha : -1);
-      ek.init_acc[t] = (int16_t)(t < g.l1);  // specials start from zero
+      ek.key_row[t] = (int16_t)tprime(g, t);  // key rows are over the full ext basis
+      ek.js[t] = (int16_t)(t < g.nr ? (g.r0 + t) / g.alpha : -1);
+      ek.init_acc[t] = (int16_t)(t < g.nr);  // specials start from zero
     }
     for (int j0 = 0; j0 < g.nslices; j0 += g.S) {
       const int S = std::min(g.S, g.nslices - j0);
       LimbMap s1;
-      s1.n = S * g.E;
-      const uint32_t* ntt_in = y;
+      s1.n = S * g.T;
+      const uint32_t* ntt_in = y_full;
       for (int sl = 0; sl < S; ++sl) {
         const int j = j0 + sl, lo = j * g.alpha, hi = std::min(lo + g.alpha, g.l1);
         if (hi - lo > 1) {
-          // alpha > 1: fast_basis_conv of the slice to every extended prime
-          // (slice primes are copied through) into conv rows [sl*E, sl*E+E)
+          // alpha > 1: fast_basis_conv of the slice to every target prime
+          // (slice primes are copied through) into conv rows [sl*T, sl*T+T)
           std::vector<int> src, dst;
           for (int q = lo; q < hi; ++q) src.push_back(q);
-          for (int t = 0; t < g.E; ++t) dst.push_back(ext_prime(g, t));
+          for (int t = 0; t < g.T; ++t) dst.push_back(tprime(g, t));
           BconvArgs ba;
           if ((rc = fill_bconv(c, src, dst, ba))) return rc;
-          if ((rc = launch_bconv(c, y + (size_t)lo * U, conv + (size_t)sl * g.E * U, ba, batch,
-                                 st)))
+          if ((rc = launch_bconv(c, y_full + (size_t)lo * U, conv + (size_t)sl * g.T * U, ba,
+                                 batch, st)))
             return rc;
           ntt_in = conv;
         }
-        for (int t = 0; t < g.E; ++t) {
-          const int l = sl * g.E + t;
-          s1.prime[l] = (int16_t)ext_prime(g, t);
+        for (int t = 0; t < g.T; ++t) {
+          const int l = sl * g.T + t;
+          s1.prime[l] = (int16_t)tprime(g, t);
           // alpha = 1: fast_basis_conv is the identity on the slice's
           // coefficients (Q = q_lo, Q/q = 1): the NTT reads y's row directly
           // and reduces it mod each target prime inside the byte-sliced GEMM
@@ -227,7 +248,7 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
       }
       ek.j0 = j0;
       if ((rc = launch_ntt_ts_ks_group(c, ntt_in, ntt_ws, s1, tmap, S, batch, ek, st))) return rc;
-      for (int t = 0; t < g.E; ++t) ek.init_acc[t] = 1;
+      for (int t = 0; t < g.T; ++t) ek.init_acc[t] = 1;
     }
   } else {
     int first = 1;
@@ -239,19 +260,19 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
       mu.n = 0;
       std::vector<int> src, dst;
       for (int s = lo; s < hi; ++s) src.push_back(s);
-      for (int r = 0; r < g.E; ++r) {
-        if (r >= lo && r < hi) continue;
-        mu.prime[mu.n] = (int16_t)ext_prime(g, r);
-        mu.out_row[mu.n] = (int16_t)r;
+      for (int t = 0; t < g.T; ++t) {
+        if (t < g.nr && g.r0 + t >= lo && g.r0 + t < hi) continue;
+        mu.prime[mu.n] = (int16_t)tprime(g, t);
+        mu.out_row[mu.n] = (int16_t)t;
         mu.in_row[mu.n] = (int16_t)(hi - lo == 1 ? lo : mu.n);
-        dst.push_back(ext_prime(g, r));
+        dst.push_back(tprime(g, t));
         ++mu.n;
       }
-      const uint32_t* ntt_in = y;
+      const uint32_t* ntt_in = y_full;
       if (hi - lo > 1) {
         BconvArgs ba;
         if ((rc = fill_bconv(c, src, dst, ba))) return rc;
-        if ((rc = launch_bconv(c, y + (size_t)lo * U, conv, ba, batch, st))) return rc;
+        if ((rc = launch_bconv(c, y_full + (size_t)lo * U, conv, ba, batch, st))) return rc;
         ntt_in = conv;
       }
       // alpha = 1: fast_basis_conv is the identity on the slice's coefficients
@@ -267,18 +288,22 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
       ek.kb = kb;
       ek.ka = ka;
       ek.acc_b = acc;
-      ek.acc_a = acc + g.E * U;
+      ek.acc_a = acc + g.T * U;
       ek.first = first;
-      for (int l = 0; l < mu.n; ++l) ek.key_row[l] = (int16_t)key_row[mu.out_row[l]];
-      if ((rc = launch_ntt(c, ntt_in, nullptr, mu, batch, 0, &ek, ntt_ws, ntt_ws_bytes, st)))
+      for (int l = 0; l < mu.n; ++l) ek.key_row[l] = mu.prime[l];
+      if (mu.n &&
+          (rc = launch_ntt(c, ntt_in, nullptr, mu, batch, 0, &ek, ntt_ws, ntt_ws_bytes, st)))
         return rc;
-      // slice rows are reused unchanged (ckks.py:361-364): MAC them straight from d
-      int64_t key_off[kMaxRows];
-      for (int r = lo; r < hi; ++r) key_off[r - lo] = (int64_t)key_row[r] * c.n;
-      if ((rc = launch_ks_mac(c, d + (size_t)lo * U, kb, ka, acc + (size_t)lo * U,
-                              acc + (g.E + lo) * U, row_prime + lo, key_off, hi - lo, batch,
-                              first, st)))
-        return rc;
+      // slice rows are reused unchanged (ckks.py:361-364): MAC the local ones straight from d
+      const int a0 = std::max(lo, g.r0), a1 = std::min(hi, g.r0 + g.nr);
+      if (a1 > a0) {
+        int64_t key_off[kMaxRows];
+        for (int r = a0; r < a1; ++r) key_off[r - a0] = (int64_t)r * c.n;
+        const size_t t0 = (size_t)(a0 - g.r0);
+        if ((rc = launch_ks_mac(c, d + t0 * U, kb, ka, acc + t0 * U, acc + (g.T + t0) * U,
+                                row_prime + t0, key_off, a1 - a0, batch, first, st)))
+          return rc;
+      }
       first = 0;
     }
   }
@@ -290,7 +315,7 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
     for (int k = 0; k < g.K; ++k) {
       const int l = cmp * g.K + k;
       ms.prime[l] = (int16_t)(g.Lc + k);
-      ms.in_row[l] = (int16_t)(cmp * g.E + g.l1 + k);
+      ms.in_row[l] = (int16_t)(cmp * g.T + g.nr + k);
       ms.out_row[l] = (int16_t)l;
     }
   if ((rc = launch_ntt(c, acc, ysp, ms, batch, 1, nullptr, ntt_ws, ntt_ws_bytes, st))) return rc;
@@ -299,20 +324,14 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
   if (g.K > 1) {
     std::vector<int> src, dst;
     for (int k = 0; k < g.K; ++k) src.push_back(g.Lc + k);
-    for (int i = 0; i < g.l1; ++i) dst.push_back(i);
+    for (int t = 0; t < g.nr; ++t) dst.push_back(g.r0 + t);
     BconvArgs ba;
     if ((rc = fill_bconv(c, src, dst, ba))) return rc;
     for (int cmp = 0; cmp < 2; ++cmp)
-      if ((rc = launch_bconv(c, ysp + (size_t)cmp * g.K * U, conv + (size_t)cmp * g.l1 * U, ba,
+      if ((rc = launch_bconv(c, ysp + (size_t)cmp * g.K * U, conv + (size_t)cmp * g.nr * U, ba,
                              batch, st)))
         return rc;
     md_in = conv;
-  }
-  uint64_t big_p_mod[kMaxLimbs];
-  for (int i = 0; i < g.l1; ++i) {
-    uint64_t pm = 1;
-    for (int k = 0; k < g.K; ++k) pm = pm * (c.primes[g.Lc + k] % c.primes[i]) % c.primes[i];
-    big_p_mod[i] = pm;
   }
   LimbMap md;
   EpiArgs ep;
@@ -320,19 +339,23 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
   ep.mode = EPI_SUB_SCALE;
   ep.x = acc;
   ep.base = base;
-  md.n = 2 * g.l1;
-  for (int cmp = 0; cmp < 2; ++cmp)
-    for (int i = 0; i < g.l1; ++i) {
-      const int l = cmp * g.l1 + i;
-      const uint32_t q = c.primes[i];
+  md.n = 2 * g.nr;
+  for (int t = 0; t < g.nr; ++t) {
+    const int i = g.r0 + t;
+    const uint32_t q = c.primes[i];
+    uint64_t pm = 1;
+    for (int k = 0; k < g.K; ++k) pm = pm * (c.primes[g.Lc + k] % q) % q;
+    for (int cmp = 0; cmp < 2; ++cmp) {
+      const int l = cmp * g.nr + t;
       md.prime[l] = (int16_t)i;
-      md.in_row[l] = (int16_t)(g.K > 1 ? cmp * g.l1 + i : cmp);
+      md.in_row[l] = (int16_t)(g.K > 1 ? cmp * g.nr + t : cmp);
       md.out_row[l] = (int16_t)l;
-      ep.x_row[l] = (int16_t)(cmp * g.E + i);
+      ep.x_row[l] = (int16_t)(cmp * g.T + t);
       ep.base_row[l] = base ? base_rows[l] : (int16_t)-1;
-      ep.s[l] = invmod(big_p_mod[i], q);
+      ep.s[l] = invmod(pm, q);
       ep.s_shoup[l] = shoup(ep.s[l], q);
     }
+  }
   return launch_ntt(c, md_in, out, md, batch, 0, &ep, ntt_ws, ntt_ws_bytes, st);
 }
 
@@ -566,7 +589,8 @@ int tfhe_keyswitch(TfheCtx* h, const uint32_t* d, int level, int batch, const ui
   Carve cv{static_cast<uint8_t*>(ws), ws_bytes};
   int16_t rows[kMaxLimbs];
   for (int l = 0; l < 2 * (level + 1); ++l) rows[l] = (int16_t)l;
-  return keyswitch_impl(h, d, level, batch, key, dnum, out, add, rows, cv, (cudaStream_t)stream);
+  return keyswitch_impl(h, d, nullptr, level, batch, key, dnum, 0, level + 1, out, add, rows, cv,
+                        (cudaStream_t)stream);
 }
 
 int tfhe_hmult(TfheCtx* h, const uint32_t* ct0, const uint32_t* ct1, int level, int batch,
@@ -590,7 +614,8 @@ int tfhe_hmult(TfheCtx* h, const uint32_t* ct0, const uint32_t* ct1, int level, 
     return rc;
   int16_t rows[kMaxLimbs];
   for (int l = 0; l < 2 * l1; ++l) rows[l] = (int16_t)l;  // (d0, d1) added to (ksb, ksa)
-  return keyswitch_impl(h, dd + 2 * P, level, batch, rlk, dnum, out, dd, rows, cv, st);
+  return keyswitch_impl(h, dd + 2 * P, nullptr, level, batch, rlk, dnum, 0, l1, out, dd, rows, cv,
+                        st);
 }
 
 int tfhe_rescale(TfheCtx* h, const uint32_t* ct, int level, int batch, uint32_t* out, void* ws,
@@ -671,7 +696,91 @@ int tfhe_hrotate(TfheCtx* h, const uint32_t* ct, int level, int batch, uint32_t 
     rows[i] = (int16_t)i;   // b' = phi(b) + ksb
     rows[l1 + i] = -1;      // a' = ksa
   }
-  return keyswitch_impl(h, phi + P, level, batch, key, dnum, out, phi, rows, cv, st);
+  return keyswitch_impl(h, phi + P, nullptr, level, batch, key, dnum, 0, l1, out, phi, rows, cv,
+                        st);
+}
+
+}  // extern "C"
+
+/* ---- limb-partitioned evaluation ----------------------------- */
+extern "C" {
+
+int tfhe_tensor_product(TfheCtx* h, const uint32_t* ct0, const uint32_t* ct1, int row_lo,
+                        int n_rows, int batch, uint32_t* out, void* stream) {
+  int rc;
+  if ((rc = check_ctx(h))) return rc;
+  if (row_lo < 0 || n_rows < 0 || n_rows > kMaxRows || row_lo + n_rows > h->n_chain ||
+      batch <= 0 || (n_rows && (!ct0 || !ct1 || !out))) {
+    set_error("tfhe_tensor_product: bad arguments");
+    return TFHE_EINVAL;
+  }
+  if (!n_rows) return 0;
+  const size_t P = (size_t)n_rows * batch * h->c.n;
+  int16_t rp[kMaxRows];
+  for (int i = 0; i < n_rows; ++i) rp[i] = (int16_t)(row_lo + i);
+  return launch_tensor(h->c, ct0, ct0 + P, ct1, ct1 + P, out, out + P, out + 2 * P, rp, n_rows,
+                       (int64_t)batch * h->c.n, (cudaStream_t)stream);
+}
+
+int tfhe_keyswitch_part(TfheCtx* h, const uint32_t* d_local, const uint32_t* y_full, int level,
+                        int batch, const uint32_t* key, int dnum, int row_lo, int n_rows,
+                        uint32_t* out, const uint32_t* add, int add_components, void* ws,
+                        size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_ctx(h)) || (rc = check_level(h, level, batch, dnum ? dnum : -1))) return rc;
+  if (!y_full || !key || !out || row_lo < 0 || n_rows < 1 || row_lo + n_rows > level + 1 ||
+      !d_local || add_components < 0 || add_components > 2) {
+    set_error("tfhe_keyswitch_part: bad arguments");
+    return TFHE_EINVAL;
+  }
+  Carve cv{static_cast<uint8_t*>(ws), ws_bytes};
+  int16_t rows[kMaxLimbs];
+  for (int l = 0; l < 2 * n_rows; ++l) rows[l] = (int16_t)(l < add_components * n_rows ? l : -1);
+  return keyswitch_impl(h, d_local, y_full, level, batch, key, dnum, row_lo, n_rows, out, add,
+                        rows, cv, (cudaStream_t)stream);
+}
+
+int tfhe_rescale_part(TfheCtx* h, const uint32_t* ct_local, const uint32_t* top_coeff, int level,
+                      int batch, int row_lo, int n_rows, uint32_t* out, void* ws, size_t ws_bytes,
+                      void* stream) {
+  int rc;
+  if ((rc = check_ctx(h)) || (rc = check_level(h, level, batch, 0))) return rc;
+  if (level < 1 || !top_coeff || row_lo < 0 || n_rows < 0 || row_lo + n_rows > level + 1 ||
+      (n_rows && (!ct_local || !out))) {
+    set_error("tfhe_rescale_part: bad arguments");
+    return TFHE_EINVAL;
+  }
+  const Ctx& c = h->c;
+  const int nout = std::max(0, std::min(row_lo + n_rows, level) - row_lo);  // rows kept
+  if (!nout) return 0;
+  const size_t U = (size_t)batch * c.n;
+  Carve cv{static_cast<uint8_t*>(ws), ws_bytes};
+  const size_t nws = (size_t)2 * nout * U * 4;
+  uint32_t* nw = cv.take<uint32_t>(nws);
+  if (!cv.ok) {
+    set_error("ckks workspace too small");
+    return TFHE_EINVAL;
+  }
+  // out_i = (c_i - NTT_{q_i}(t_top)) * q_top^-1 for the local rows i < level
+  LimbMap mr;
+  EpiArgs ep;
+  memset(&ep, 0, sizeof(ep));
+  ep.mode = EPI_SUB_SCALE;
+  ep.x = ct_local;
+  mr.n = 2 * nout;
+  const uint32_t q_top = c.primes[level];
+  for (int cmp = 0; cmp < 2; ++cmp)
+    for (int t = 0; t < nout; ++t) {
+      const int l = cmp * nout + t, i = row_lo + t;
+      mr.prime[l] = (int16_t)i;
+      mr.in_row[l] = (int16_t)cmp;
+      mr.out_row[l] = (int16_t)l;
+      ep.x_row[l] = (int16_t)(cmp * n_rows + t);
+      ep.base_row[l] = -1;
+      ep.s[l] = invmod(q_top, c.primes[i]);
+      ep.s_shoup[l] = shoup(ep.s[l], c.primes[i]);
+    }
+  return launch_ntt(c, top_coeff, out, mr, batch, 0, &ep, nw, nws, (cudaStream_t)stream);
 }
 
 }  // extern "C"

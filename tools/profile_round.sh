@@ -21,3 +21,8 @@ if [ "${2:-}" = "hmult" ]; then
   echo "hmult full rc=$?"
   ncu -i gpurun_out/${tag}_hmult.ncu-rep --page raw --csv > gpurun_out/${tag}_hmult_raw.csv 2>/dev/null
 fi
+# keep the merged-back gpurun_out/ under 64 MiB: exports only, reports dropped
+ncu -i gpurun_out/${tag}_ntt_ts.ncu-rep --page source --csv --print-source sass > gpurun_out/${tag}_ntt_ts_src.csv 2>/dev/null
+rm -f gpurun_out/*.ncu-rep
+gzip -f gpurun_out/${tag}_*_src.csv
+du -sh gpurun_out
