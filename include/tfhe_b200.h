@@ -76,6 +76,18 @@ int tfhe_ntt(TfheCtx* ctx, const uint32_t* in, uint32_t* out, const int32_t* lim
              const int32_t* in_rows, const int32_t* out_rows, int n_limbs, int batch,
              int inverse, void* ws, size_t ws_bytes, void* stream);
 
+/* Host-to-host form of tfhe_ntt (the e2e path of ntt.transform_rows /
+ * batched_apply on host buffers): rows of host_in (n_limbs, batch, n) are
+ * streamed through `staging` (device, >= tfhe_ntt_host_staging_bytes) in
+ * chunks, H2D copy / transform / D2H copy overlapped on two internal copy
+ * streams and the caller's stream; the call is stream-ordered -- host_out
+ * is complete once `stream` reaches this point.  Pinned host buffers give
+ * full copy/compute overlap (pageable ones work, without overlap). */
+size_t tfhe_ntt_host_staging_bytes(const TfheCtx* ctx, int n_limbs, int batch);
+int tfhe_ntt_host(TfheCtx* ctx, const uint32_t* host_in, uint32_t* host_out,
+                  const int32_t* limb_prime, int n_limbs, int batch, int inverse, void* staging,
+                  size_t staging_bytes, void* stream);
+
 /* ---- element-wise / automorphism / base conversion ---------------------
  * tfhe_eltwise: out[r] = a[r] op b[r] (or op a[r]) for rows r < rows of
  * per_row elements (per_row % 4 == 0), prime primes[row_prime[r]];

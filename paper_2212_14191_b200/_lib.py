@@ -55,6 +55,9 @@ SIGNATURES = {
                                     ctypes.c_size_t, _vp]),
     "tfhe_hrotate": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint32, _vp,
                                     ctypes.c_int, _vp, _vp, ctypes.c_size_t, _vp]),
+    "tfhe_ntt_host_staging_bytes": (ctypes.c_size_t, [_vp, ctypes.c_int, ctypes.c_int]),
+    "tfhe_ntt_host": (ctypes.c_int, [_vp, _vp, _vp, _i32p, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, _vp, ctypes.c_size_t, _vp]),
     "tfhe_tensor_product": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, _vp, _vp]),
     "tfhe_keyswitch_part": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp,

@@ -14,6 +14,10 @@
 struct TfheCtx {
   tfhe::Ctx c;
   int n_chain = 0, n_special = 0;
+  // host-streaming transform (tfhe_ntt_host): copy streams + per-slot events,
+  // created on first use
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_in[3] = {}, ev_done[3] = {}, ev_out[3] = {};
 };
 
 namespace tfhe {
@@ -457,6 +461,16 @@ int tfhe_ctx_create(int device, int log_n, const uint32_t* primes, const uint32_
 void tfhe_ctx_destroy(TfheCtx* h) {
   if (!h) return;
   Ctx& c = h->c;
+  if (h->h2d) {
+    cudaStreamDestroy(h->h2d);
+    cudaStreamDestroy(h->d2h);
+    cudaEventDestroy(h->ev_start);
+    for (int i = 0; i < 3; ++i) {
+      cudaEventDestroy(h->ev_in[i]);
+      cudaEventDestroy(h->ev_done[i]);
+      cudaEventDestroy(h->ev_out[i]);
+    }
+  }
   cudaFree(c.d_pc);
   for (int i = 0; i < 2; ++i) {
     for (int s = 0; s < 2; ++s) {
@@ -781,6 +795,102 @@ int tfhe_rescale_part(TfheCtx* h, const uint32_t* ct_local, const uint32_t* top_
       ep.s_shoup[l] = shoup(ep.s[l], c.primes[i]);
     }
   return launch_ntt(c, top_coeff, out, mr, batch, 0, &ep, nw, nws, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+/* ---- host-streaming transform (e2e path of batched_apply / transform_rows) -- */
+namespace {
+constexpr int kHostSlots = 3;
+constexpr size_t kHostChunkBytes = (size_t)48 << 20;
+
+int host_chunk_rows(const TfheCtx* h, int n_limbs, int batch) {
+  const size_t row = (size_t)batch * h->c.n * 4;
+  return (int)std::max<size_t>(1, std::min<size_t>((size_t)n_limbs, kHostChunkBytes / row));
+}
+}  // namespace
+
+extern "C" {
+
+size_t tfhe_ntt_host_staging_bytes(const TfheCtx* h, int n_limbs, int batch) {
+  if (!h || n_limbs <= 0 || batch <= 0) return 0;
+  const int rc = host_chunk_rows(h, n_limbs, batch);
+  const size_t chunk = ((size_t)rc * batch * h->c.n * 4 + 255) & ~(size_t)255;
+  return (2 * kHostSlots) * chunk + ((ntt_workspace_bytes(h->c, rc, batch) + 255) & ~(size_t)255);
+}
+
+int tfhe_ntt_host(TfheCtx* h, const uint32_t* host_in, uint32_t* host_out,
+                  const int32_t* limb_prime, int n_limbs, int batch, int inverse, void* staging,
+                  size_t staging_bytes, void* stream) {
+  int rc;
+  if ((rc = check_ctx(h)) || (rc = check_limbs(h, limb_prime, n_limbs))) return rc;
+  if (batch <= 0 || (n_limbs && (!host_in || !host_out || !staging)) ||
+      staging_bytes < tfhe_ntt_host_staging_bytes(h, n_limbs, batch)) {
+    set_error("tfhe_ntt_host: bad arguments or staging too small");
+    return TFHE_EINVAL;
+  }
+  if (!n_limbs) return 0;
+  if (!h->h2d) {
+    if (cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming) != cudaSuccess) {
+      set_error("tfhe_ntt_host: stream creation failed");
+      return TFHE_ECUDA;
+    }
+    for (int i = 0; i < kHostSlots; ++i)
+      if (cudaEventCreateWithFlags(&h->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_out[i], cudaEventDisableTiming) != cudaSuccess) {
+        set_error("tfhe_ntt_host: event creation failed");
+        return TFHE_ECUDA;
+      }
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int rows = host_chunk_rows(h, n_limbs, batch);
+  const size_t row_elems = (size_t)batch * h->c.n;
+  const size_t chunk = (rows * row_elems * 4 + 255) & ~(size_t)255;
+  uint8_t* base = static_cast<uint8_t*>(staging);
+  void* ws = base + 2 * kHostSlots * chunk;
+  const size_t ws_bytes = staging_bytes - 2 * kHostSlots * chunk;
+  // staging may still be in use by earlier work on the caller's stream
+  cudaEventRecord(h->ev_start, st);
+  cudaStreamWaitEvent(h->h2d, h->ev_start, 0);
+  cudaStreamWaitEvent(h->d2h, h->ev_start, 0);
+  const int n_chunks = (n_limbs + rows - 1) / rows;
+  for (int i = 0; i < n_chunks; ++i) {
+    const int k = i % kHostSlots, r0 = i * rows, nr = std::min(rows, n_limbs - r0);
+    uint32_t* din = reinterpret_cast<uint32_t*>(base + (2 * k) * chunk);
+    uint32_t* dout = reinterpret_cast<uint32_t*>(base + (2 * k + 1) * chunk);
+    const size_t bytes = nr * row_elems * 4;
+    // H2D into slot k once chunk i-3 has been transformed (din free)
+    if (i >= kHostSlots) cudaStreamWaitEvent(h->h2d, h->ev_done[k], 0);
+    cudaMemcpyAsync(din, host_in + r0 * row_elems, bytes, cudaMemcpyHostToDevice, h->h2d);
+    cudaEventRecord(h->ev_in[k], h->h2d);
+    // transform on the caller's stream once the data is in and dout is drained
+    cudaStreamWaitEvent(st, h->ev_in[k], 0);
+    if (i >= kHostSlots) cudaStreamWaitEvent(st, h->ev_out[k], 0);
+    LimbMap m;
+    m.n = nr;
+    for (int l = 0; l < nr; ++l) {
+      m.prime[l] = (int16_t)limb_prime[r0 + l];
+      m.in_row[l] = m.out_row[l] = (int16_t)l;
+    }
+    if ((rc = launch_ntt(h->c, din, dout, m, batch, inverse != 0, nullptr, ws, ws_bytes, st)))
+      return rc;
+    cudaEventRecord(h->ev_done[k], st);
+    // D2H of the result
+    cudaStreamWaitEvent(h->d2h, h->ev_done[k], 0);
+    cudaMemcpyAsync(host_out + r0 * row_elems, dout, bytes, cudaMemcpyDeviceToHost, h->d2h);
+    cudaEventRecord(h->ev_out[k], h->d2h);
+  }
+  // the caller's stream completes after the last copy back
+  for (int k = 0; k < std::min(n_chunks, kHostSlots); ++k) cudaStreamWaitEvent(st, h->ev_out[k], 0);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("tfhe_ntt_host: ") + cudaGetErrorString(e));
+    return TFHE_ECUDA;
+  }
+  return 0;
 }
 
 }  // extern "C"

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import threading
+import warnings
 
 import numpy as np
 import torch
@@ -109,6 +110,7 @@ class DeviceContext:
         self.lib.tfhe_ctx_plan(self.handle, ctypes.byref(n1), ctypes.byref(n2))
         self.plan = (n1.value, n2.value)
         self._ws = None
+        self._staging = None
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -177,6 +179,35 @@ class DeviceContext:
             L, batch, int(bool(inverse)), _ptr(ws), ws.numel(), _stream(self.device)),
             "tfhe_ntt")
         return out
+
+    def ntt_host(self, x, limb_primes, inverse=False):
+        """Host-to-host batched transform of x (rows, batch, n) -- a CPU torch
+        tensor (pinned for full overlap) or a numpy array -- streamed through
+        the device in chunks with H2D / transform / D2H overlapped
+        (tfhe_ntt_host).  Returns the same kind of host buffer (pinned)."""
+        numpy_in = not isinstance(x, torch.Tensor)
+        if numpy_in:
+            a = np.ascontiguousarray(x, dtype=np.uint32)
+            with warnings.catch_warnings():   # read-only input: only ever read
+                warnings.simplefilter("ignore")
+                xt = torch.from_numpy(a.view(np.int32))
+        else:
+            xt = (x.view(torch.int32) if x.dtype == torch.uint32
+                  else x.to(torch.int32)).contiguous()
+        if xt.ndim != 3:
+            raise ParameterError("ntt_host expects (rows, batch, n)")
+        L, batch = int(xt.shape[0]), int(xt.shape[1])
+        out = torch.empty(tuple(xt.shape), dtype=torch.int32, pin_memory=True)
+        nbytes = max(int(self.lib.tfhe_ntt_host_staging_bytes(self.handle, L, batch)), 256)
+        if self._staging is None or self._staging.numel() < nbytes:
+            self._staging = None
+            self._staging = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        _lib.check(self.lib.tfhe_ntt_host(
+            self.handle, ctypes.c_void_p(xt.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+            _lib.i32_array(self.prime_ids(limb_primes)), L, batch, int(bool(inverse)),
+            _ptr(self._staging), self._staging.numel(), _stream(self.device)), "tfhe_ntt_host")
+        torch.cuda.current_stream(self.device).synchronize()
+        return out.numpy().view(np.uint32) if numpy_in else out
 
     def eltwise(self, op, a, b, row_primes, scalars=None, out=None):
         rows = a.shape[0]

@@ -70,3 +70,33 @@ def test_batched_multilimb_vs_oracle(n, batch):
     assert np.array_equal(f, O.ntt(x, primes))
     b = ctx.ntt(torch.from_numpy(f.view(np.int32)).cuda(), primes, inverse=True)
     assert np.array_equal(b.cpu().numpy().view(np.uint32), x)
+
+
+@pytest.mark.parametrize("n,batch,rows,kind", [(1 << 16, 64, 12, "pinned"),
+                                               (1 << 16, 64, 7, "numpy"),
+                                               (1 << 12, 64, 3, "numpy"),
+                                               (1 << 16, 200, 2, "pinned")])
+def test_batched_apply_host_streaming(n, batch, rows, kind):
+    """batched_apply on host buffers streams through tfhe_ntt_host in chunks
+    (several chunks, slot reuse, ragged last chunk): equal to the device path
+    and to the oracle on a sample of rows, and INTT(NTT(x)) == x."""
+    import torch
+    from paper_2212_14191_b200.batch import BatchBuffer, batched_apply
+    from paper_2212_14191_b200.ntt import TwiddleTable
+    from paper_2212_14191_b200.params import generate_primes
+    primes = generate_primes(n, [29] * rows)
+    table = TwiddleTable(n, primes)
+    rng = np.random.default_rng(rows * batch)
+    x = O.uniform_rows(rng, primes, (batch, n))
+    if kind == "pinned":
+        data = torch.from_numpy(x.view(np.int32)).pin_memory()
+    else:
+        data = x
+    f = batched_apply(BatchBuffer(data=data, basis=primes, domain="coeff"), "ntt", table=table)
+    fh = f.data.numpy().view(np.uint32) if kind == "pinned" else f.data
+    dev = table.context().ntt(torch.from_numpy(x.view(np.int32)).cuda(), primes)
+    assert np.array_equal(fh, dev.cpu().numpy().view(np.uint32))
+    assert np.array_equal(fh[:, :2], O.ntt(x[:, :2], primes))
+    b = batched_apply(f, "intt", table=table)
+    bh = b.data.numpy().view(np.uint32) if kind == "pinned" else b.data
+    assert np.array_equal(bh, x)
