@@ -257,42 +257,81 @@ def run_b200(args):
     ntt_call_ms = ms / (2 * args.steps)             # one batched NTT = 2 kernel launches
     achieved_tops = L * B * ops_per_limb / (ntt_call_ms / 1e3) / 1e12
 
-    # HMULT + relin + rescale (configs[2]), same protocol
+    def timed(fn, steps):
+        """device ms per call of fn (CUDA events on the launching stream,
+        barrier-bracketed, max over ranks), after max(warmup, 1) warm calls"""
+        for _ in range(max(args.warmup, 1)):
+            fn()
+        torch.cuda.synchronize()
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(steps):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(ev0.elapsed_time(ev1)) / steps
+
+    def rand_rows(basis, shape_tail):
+        t = torch.empty((len(basis),) + tuple(shape_tail), dtype=torch.int32, device=dev)
+        for i, q in enumerate(basis):
+            t[i] = torch.randint(0, q, tuple(shape_tail), generator=g, device=dev,
+                                 dtype=torch.int64).to(torch.int32)
+        return t
+
+    def ckks_setup(prm, batch):
+        ck = CkksContext(prm, device=dev)
+        e = tuple(prm.chain.q) + tuple(prm.chain.p)
+        key = rand_rows(e, (prm.dnum, 2, prm.n)).permute(1, 2, 0, 3).contiguous()
+        cts = [CiphertextBatch(rand_rows(prm.chain.q, (2, batch, prm.n)).transpose(0, 1)
+                               .contiguous(), prm.l_max) for _ in range(2)]
+        return ck, key, cts
+
+    # CKKS operators at P-Default (configs[2..4]), same protocol
     hm = None
     if args.hmult_batch > 0:
-        ck = CkksContext(params, device=dev)
-        Bh, l1, E = args.hmult_batch, L, L + len(params.chain.p)
-        key = torch.empty((params.dnum, 2, E, N), dtype=torch.int32, device=dev)
-        for i, q in enumerate(ext):
-            key[:, :, i] = torch.randint(0, q, (params.dnum, 2, N), generator=g, device=dev,
-                                         dtype=torch.int64).to(torch.int32)
-        cts = []
-        for _ in range(2):
-            d = torch.empty((2, l1, Bh, N), dtype=torch.int32, device=dev)
-            for i, q in enumerate(primes):
-                d[:, i] = torch.randint(0, q, (2, Bh, N), generator=g, device=dev,
-                                        dtype=torch.int64).to(torch.int32)
-            cts.append(CiphertextBatch(d, params.l_max))
-
-        def hstep():
-            ck.rescale_batch(ck.hmult_batch(cts[0], cts[1], key))
-
-        for _ in range(max(args.warmup, 1)):
-            hstep()
-        torch.cuda.synchronize()
-        barrier()
-        hs, he = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        Bh = args.hmult_batch
+        ck, key, cts = ckks_setup(params, Bh)
         hsteps = max(1, min(args.steps, 5))
-        hs.record(stream)
-        for _ in range(hsteps):
-            hstep()
-        he.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        hms = max_over_ranks(hs.elapsed_time(he))
-        hm = {"hmult_kops": Bh * hsteps * world / (hms / 1e3) / 1e3,
-              "ms_per_batch": hms / hsteps, "batch_per_gpu": Bh}
+        ms_hm = timed(lambda: ck.rescale_batch(ck.hmult_batch(cts[0], cts[1], key)), hsteps)
+        ms_hm_only = timed(lambda: ck.hmult_batch(cts[0], cts[1], key), hsteps)
+        ms_rot = timed(lambda: ck.hrotate_batch(cts[0], 1, key), hsteps)
+        ms_rs = timed(lambda: ck.rescale_batch(cts[0]), hsteps)
+
+        def mixed():   # configs[4]: HMULT -> rescale -> HROTATE per ciphertext
+            ck.hrotate_batch(ck.rescale_batch(ck.hmult_batch(cts[0], cts[1], key)), 1, key)
+        ms_mix = timed(mixed, hsteps)
+        rate = lambda ms: Bh * world / (ms / 1e3)  # noqa: E731
+        hm = {"hmult_kops": rate(ms_hm) / 1e3, "ms_per_batch": ms_hm, "batch_per_gpu": Bh,
+              "hmult_relin_only_per_s": rate(ms_hm_only), "hrotate_per_s": rate(ms_rot),
+              "hrotate_ms_per_batch": ms_rot, "rescale_per_s": rate(ms_rs),
+              "mixed_ct_per_s": rate(ms_mix), "mixed_ms_per_batch": ms_mix}
         del ck, key, cts
+
+    # Set_A (N=2^12, the paper's 913 KOPS NTT / 88 KOPS HMULT parameters)
+    sa = None
+    if args.set_a_batch > 0:
+        pa = CkksParams.from_preset("set_a")
+        Ba = args.set_a_batch
+        ck, key, cts = ckks_setup(pa, Ba)
+        qa = list(pa.chain.q)
+        xa = rand_rows(qa, (Ba, pa.n))
+        fa, ya = torch.empty_like(xa), torch.empty_like(xa)
+
+        def ntt_a():
+            ck.dev.ntt(xa, qa, out=fa)
+            ck.dev.ntt(fa, qa, inverse=True, out=ya)
+        ms_ntt = timed(ntt_a, 10)
+        ms_hm = timed(lambda: ck.rescale_batch(ck.hmult_batch(cts[0], cts[1], key)), 5)
+        ms_hm_only = timed(lambda: ck.hmult_batch(cts[0], cts[1], key), 5)
+        sa = {"workload": f"set_a (N=2^12, L+1=2, K=2, dnum=2), batch {Ba} per GPU",
+              "ntt_limb_kops": 2 * len(qa) * Ba * world / (ms_ntt / 1e3) / 1e3,
+              "ntt_poly_kops": 2 * Ba * world / (ms_ntt / 1e3) / 1e3,
+              "hmult_relin_kops": Ba * world / (ms_hm_only / 1e3) / 1e3,
+              "hmult_relin_rescale_kops": Ba * world / (ms_hm / 1e3) / 1e3,
+              "paper_a100": {"ntt_kops": 913, "hmult_kops": 88}}
+        del ck, key, cts, xa, fa, ya
 
     # end to end through the reference-facing API (batched_apply) with pinned host buffers
     table = TwiddleTable(N, primes, device=dev)
@@ -301,12 +340,17 @@ def run_b200(args):
     host_in.copy_(x)
     e2e_steps = max(1, min(args.steps, 3))
     buf = BatchBuffer(data=host_in, basis=primes, domain="coeff")
-    batched_apply(batched_apply(buf, "ntt", table=table), "intt", table=table)  # warm
+    # warm-up = the timed loop itself, so the pinned result buffers the API
+    # returns are in torch's host caching allocator (steady state)
+    for _ in range(2):
+        out = batched_apply(buf, "ntt", table=table)
+        back = batched_apply(out, "intt", table=table)
+    torch.cuda.synchronize()
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        out = batched_apply(buf, "ntt", table=table)        # H2D + NTT + D2H
-        back = batched_apply(out, "intt", table=table)       # H2D + INTT + D2H
+        out = batched_apply(buf, "ntt", table=table)        # H2D / NTT / D2H streamed
+        back = batched_apply(out, "intt", table=table)       # H2D / INTT / D2H streamed
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_ok = bool(torch.equal(back.data, host_in))
@@ -366,7 +410,19 @@ def run_b200(args):
                                      f"{PRESET} (L=44, K=1, dnum=45), batch {hm['batch_per_gpu']}"
                                      " per GPU (BASELINE configs[2])",
                          "ms_per_batch": hm["ms_per_batch"],
-                         "ops_per_s": hm["hmult_kops"] * 1e3}
+                         "ops_per_s": hm["hmult_kops"] * 1e3,
+                         "hmult_relin_only_per_s": hm["hmult_relin_only_per_s"],
+                         "rescale_per_s": hm["rescale_per_s"]}
+        line["hrotate"] = {"workload": f"HROTATE r=1 (automorphism + keyswitch), N=2^16, {PRESET}"
+                                       f", batch {hm['batch_per_gpu']} per GPU (configs[3])",
+                           "ops_per_s": hm["hrotate_per_s"],
+                           "ms_per_batch": hm["hrotate_ms_per_batch"]}
+        line["mixed"] = {"workload": "HMULT -> rescale -> HROTATE per ciphertext, N=2^16, "
+                                     f"{PRESET}, batch-sharded x{world} (configs[4])",
+                         "ciphertexts_per_s": hm["mixed_ct_per_s"],
+                         "ms_per_batch": hm["mixed_ms_per_batch"]}
+    if sa:
+        line["set_a"] = sa
     if rates:
         r, dt, threads = rates
         line["cpu_baseline"] = {
@@ -389,6 +445,7 @@ def main():
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--hmult-batch", type=int, default=32)
     ap.add_argument("--cpu-members", type=int, default=32)
+    ap.add_argument("--set-a-batch", type=int, default=4096)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

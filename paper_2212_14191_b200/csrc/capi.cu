@@ -224,12 +224,19 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
       const int S = std::min(g.S, g.nslices - j0);
       LimbMap s1;
       s1.n = S * g.T;
-      const uint32_t* ntt_in = y_full;
+      // one input pointer per launch: if any slice of the group needs a base
+      // conversion, every slice goes through conv (a 1-limb slice's
+      // conversion is the identity reduced mod each target, bit-identical to
+      // the NTT reading its raw row)
+      bool group_conv = false;
+      for (int sl = 0; sl < S; ++sl)
+        group_conv |= std::min((j0 + sl) * g.alpha + g.alpha, g.l1) - (j0 + sl) * g.alpha > 1;
+      const uint32_t* ntt_in = group_conv ? conv : y_full;
       for (int sl = 0; sl < S; ++sl) {
         const int j = j0 + sl, lo = j * g.alpha, hi = std::min(lo + g.alpha, g.l1);
-        if (hi - lo > 1) {
-          // alpha > 1: fast_basis_conv of the slice to every target prime
-          // (slice primes are copied through) into conv rows [sl*T, sl*T+T)
+        if (group_conv) {
+          // fast_basis_conv of the slice to every target prime (slice primes
+          // are copied through) into conv rows [sl*T, sl*T+T)
           std::vector<int> src, dst;
           for (int q = lo; q < hi; ++q) src.push_back(q);
           for (int t = 0; t < g.T; ++t) dst.push_back(tprime(g, t));
@@ -238,7 +245,6 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
           if ((rc = launch_bconv(c, y_full + (size_t)lo * U, conv + (size_t)sl * g.T * U, ba,
                                  batch, st)))
             return rc;
-          ntt_in = conv;
         }
         for (int t = 0; t < g.T; ++t) {
           const int l = sl * g.T + t;
@@ -246,7 +252,7 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
           // alpha = 1: fast_basis_conv is the identity on the slice's
           // coefficients (Q = q_lo, Q/q = 1): the NTT reads y's row directly
           // and reduces it mod each target prime inside the byte-sliced GEMM
-          s1.in_row[l] = (int16_t)(hi - lo > 1 ? l : lo);
+          s1.in_row[l] = (int16_t)(group_conv ? l : lo);
           s1.out_row[l] = (int16_t)l;
         }
       }

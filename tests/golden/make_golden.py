@@ -206,6 +206,10 @@ LARGE_CASES = [
     ("n16_l3", lambda: RP.CkksParams.generate(n=1 << 16, l_max=3, k=1, dnum=4, bit_size=28), 3, 21),
     ("resnet20_l3", lambda: RP.CkksParams.from_preset("resnet20"), 3, 22),
     ("set_c_full", lambda: RP.CkksParams.from_preset("set_c"), 7, 23),
+    # ragged GKS slices on the tensor-core (n >= 2^14) path: alpha = 2, the
+    # last slice holds one limb (level 4) / groups mix 2- and 1-limb slices
+    ("set_c_l4", lambda: RP.CkksParams.from_preset("set_c"), 4, 24),
+    ("set_c_l2", lambda: RP.CkksParams.from_preset("set_c"), 2, 25),
 ]
 
 
@@ -229,7 +233,27 @@ def make_ckks():
         json.dump(rec, fh, indent=1)
 
 
+def add_large(names):
+    """Append selected LARGE_CASES to ckks_large.json (keeps existing records)."""
+    path = os.path.join(HERE, "ckks_large.json")
+    with open(path) as fh:
+        rec = json.load(fh)
+    for name, fac, level, seed in LARGE_CASES:
+        if name not in names:
+            continue
+        t = time.time()
+        res = ref_ops(fac(), seed, level)
+        rec[name] = {k: {"sha256": sha(v), "head": v.reshape(-1)[:8].tolist()}
+                     for k, v in res.items()}
+        print(name, f"{time.time() - t:.1f}s")
+    with open(path, "w") as fh:
+        json.dump(rec, fh, indent=1)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "add-large":
+        add_large(sys.argv[2:])
+        sys.exit(0)
     d = make_params()
     make_ntt_small(d)
     make_ntt_large(d)
