@@ -187,38 +187,6 @@ __global__ void automorph_coeff_kernel(const uint32_t* __restrict__ in, uint32_t
 }
 
 // fast base conversion (rns.py:118-152), one output row per blockIdx.y
-__global__ void bconv_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                             const PrimeConst* __restrict__ pcs,
-                             const __grid_constant__ BconvArgs ba, int64_t per_row) {
-  const int t = blockIdx.y;
-  const int copy = ba.copy_from[t];
-  const PrimeConst pt = pcs[ba.dst_prime[t]];
-  uint32_t* o = out + (int64_t)t * per_row;
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
-       i += (int64_t)gridDim.x * blockDim.x * 4) {
-    if (copy >= 0) {
-      st4(o + i, ld4(in + (int64_t)copy * per_row + i));
-      continue;
-    }
-    uint64_t acc[4] = {0, 0, 0, 0};
-    for (int s = 0; s < ba.n_src; ++s) {
-      const PrimeConst ps = pcs[ba.src_prime[s]];
-      uint4 x = ld4(in + (int64_t)s * per_row + i);
-      const uint32_t hi = ba.qhat_inv[s], hs = ba.qhat_inv_shoup[s];
-      const uint32_t f = ba.factor[s * kMaxBconvDst + t];
-      uint32_t y0 = mul_shoup(x.x, hi, hs, ps.q), y1 = mul_shoup(x.y, hi, hs, ps.q);
-      uint32_t y2 = mul_shoup(x.z, hi, hs, ps.q), y3 = mul_shoup(x.w, hi, hs, ps.q);
-      // y < 2^31, f < 2^31: each product < 2^62; reduce every term
-      acc[0] += reduce64((uint64_t)y0 * f, pt.q, pt.mu);
-      acc[1] += reduce64((uint64_t)y1 * f, pt.q, pt.mu);
-      acc[2] += reduce64((uint64_t)y2 * f, pt.q, pt.mu);
-      acc[3] += reduce64((uint64_t)y3 * f, pt.q, pt.mu);
-    }
-    st4(o + i, make_uint4(reduce64(acc[0], pt.q, pt.mu), reduce64(acc[1], pt.q, pt.mu),
-                          reduce64(acc[2], pt.q, pt.mu), reduce64(acc[3], pt.q, pt.mu)));
-  }
-}
-
 int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -322,15 +290,6 @@ int launch_automorph(const Ctx& c, const uint32_t* in, uint32_t* out, uint32_t t
     automorph_coeff_kernel<<<g, 256, 0, st>>>(in, out, c.d_pc, rp, t, c.log_n, batch);
   }
   return check("automorphism kernel");
-}
-
-int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,
-                 cudaStream_t st) {
-  if (ba.n_dst <= 0) return 0;
-  int64_t per_row = (int64_t)batch * c.n;
-  dim3 g = grid_rows(per_row, ba.n_dst, 256);
-  bconv_kernel<<<g, 256, 0, st>>>(in, out, c.d_pc, ba, per_row);
-  return check("bconv kernel");
 }
 
 }  // namespace tfhe
