@@ -309,6 +309,20 @@ def run_b200(args):
               "mixed_ct_per_s": rate(ms_mix), "mixed_ms_per_batch": ms_mix}
         del ck, key, cts
 
+    # dnum-reduced P-Default (alpha = K = 9): ModUp/ModDown are 9-term base
+    # conversions on the tensor cores (tfhe_bconv) between the NTTs
+    d5 = None
+    if args.dnum5_batch > 0:
+        pd = CkksParams.from_preset("p_dnum5")
+        B5 = args.dnum5_batch
+        ck, key, cts = ckks_setup(pd, B5)
+        ms_hm = timed(lambda: ck.rescale_batch(ck.hmult_batch(cts[0], cts[1], key)), 3)
+        ms_rot = timed(lambda: ck.hrotate_batch(cts[0], 1, key), 3)
+        d5 = {"workload": f"p_dnum5 (N=2^16, L=44, K=9, dnum=5, alpha=9), batch {B5} per GPU",
+              "hmult_relin_rescale_per_s": B5 * world / (ms_hm / 1e3),
+              "hrotate_per_s": B5 * world / (ms_rot / 1e3), "ms_per_batch_hmult": ms_hm}
+        del ck, key, cts
+
     # Set_A (N=2^12, the paper's 913 KOPS NTT / 88 KOPS HMULT parameters)
     sa = None
     if args.set_a_batch > 0:
@@ -332,6 +346,49 @@ def run_b200(args):
               "hmult_relin_rescale_kops": Ba * world / (ms_hm / 1e3) / 1e3,
               "paper_a100": {"ntt_kops": 913, "hmult_kops": 88}}
         del ck, key, cts, xa, fa, ya
+
+    # HBM-bound kernels (element-wise, automorphism, tensor product, base
+    # conversion) on the configs[1] buffers: achieved GB/s of ALGORITHMIC bytes
+    # (each operand read once, each result written once) vs the measured copy
+    # bandwidth.  Inputs >= 1.4 GiB per buffer (> L2).
+    hbm = None
+    if args.hbm_kernels:
+        from paper_2212_14191_b200 import _lib as LIB
+        from paper_2212_14191_b200.device import _ptr, _stream
+        hbm = []
+        coeffs = L * B * N
+        ym = torch.empty_like(x)
+
+        def rec(name, fn, nbytes, reps=10):
+            ms = timed(fn, reps)
+            hbm.append({"kernel": name, "ms": ms, "bytes": nbytes, "gbs": nbytes / ms / 1e6})
+        rec("hada_mult (tfhe_eltwise MUL)", lambda: ctx.eltwise(LIB.OP_MUL, x, f, primes, out=ym),
+            12 * coeffs)
+        rec("ele_add (tfhe_eltwise ADD)", lambda: ctx.eltwise(LIB.OP_ADD, x, f, primes, out=ym),
+            12 * coeffs)
+        rec("automorphism NTT-domain (tfhe_automorphism)",
+            lambda: ctx.automorphism(x, 5, True, primes, out=ym), 8 * coeffs)
+        half = B // 2
+        ct0 = x.view(L, 2, half, N).transpose(0, 1).contiguous()
+        ct1 = f.view(L, 2, half, N).transpose(0, 1).contiguous()
+        tp = torch.empty((3, L, half, N), dtype=torch.int32, device=dev)
+
+        def tensor():
+            LIB.check(ctx.lib.tfhe_tensor_product(ctx.handle, _ptr(ct0), _ptr(ct1), 0, L, half,
+                                                  _ptr(tp), _stream(dev)), "tensor")
+        rec("hmult tensor product (tfhe_tensor_product)", tensor, 28 * L * half * N)
+        del ct0, ct1, tp
+        # alpha = 9 base conversion (p_dnum5 ModUp slice: 9 sources -> 54 targets)
+        pd = CkksParams.from_preset("p_dnum5")
+        ckd = CkksContext(pd, device=dev)
+        ext5 = tuple(pd.chain.q) + tuple(pd.chain.p)
+        Bb = 32
+        src = rand_rows(pd.chain.q[:pd.alpha], (Bb, N))
+        dst = torch.empty((len(ext5), Bb, N), dtype=torch.int32, device=dev)
+        rec(f"fast_basis_conv alpha={pd.alpha} -> {len(ext5)} targets (tfhe_bconv, int8 TC)",
+            lambda: ckd.dev.bconv(src, pd.chain.q[:pd.alpha], ext5, out=dst),
+            4 * (pd.alpha + len(ext5)) * Bb * N)
+        del src, dst, ym, ckd
 
     # end to end through the reference-facing API (batched_apply) with pinned host buffers
     table = TwiddleTable(N, primes, device=dev)
@@ -423,6 +480,18 @@ def run_b200(args):
                          "ms_per_batch": hm["mixed_ms_per_batch"]}
     if sa:
         line["set_a"] = sa
+    if d5:
+        line["p_dnum5"] = d5
+    if hbm:
+        hpeak, hsrc = 6546.6, "fallback (B200_PROFILING.md)"
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+                hpeak, hsrc = float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+        except Exception:
+            pass
+        for h in hbm:
+            h["frac"] = h["gbs"] / hpeak
+        line["hbm_kernels"] = {"peak_gbs": hpeak, "peak_source": hsrc, "kernels": hbm}
     if rates:
         r, dt, threads = rates
         line["cpu_baseline"] = {
@@ -446,6 +515,8 @@ def main():
     ap.add_argument("--hmult-batch", type=int, default=32)
     ap.add_argument("--cpu-members", type=int, default=32)
     ap.add_argument("--set-a-batch", type=int, default=4096)
+    ap.add_argument("--hbm-kernels", type=int, default=1)
+    ap.add_argument("--dnum5-batch", type=int, default=16)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

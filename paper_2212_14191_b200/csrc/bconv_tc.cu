@@ -14,20 +14,24 @@
 // holds V_j(s,t) = 2^(8j) F[s][t] mod p_t split into bytes:
 //     B_i[4s + j][t] = byte i of V_j(s,t),   C_i = A . B_i  (i = 0..3)
 //     sum_i 2^(8i) C_i = sum_{s,j} byte_j(y_s) V_j(s,t) == sum_s y_s F[s][t]  (mod p_t)
-// C_i <= 32*KC*255^2 < 2^24, so sum_i 2^(8i) C_i < 2^48 and one Barrett step
+// C_i <= 32*KC*255^2 < 2^22, so sum_i 2^(8i) C_i < 2^46 < p_t 2^32 and one
+// Montgomery step (V_j pre-scaled by 2^32) plus a conditional subtraction
 // gives the canonical result -- bit-identical to the reference.
 //
 // K = 4*alpha bytes (one 32-byte MMA K-step for alpha <= 8, two for <= 16);
 // targets are processed in chunks of 32 (N = 32): a chunk is 4 MMAs into
 // 4 x 32 TMEM columns, and TMEM holds 4 chunk buffers (512 columns).
 // Persistent, warp-specialised CTA (one per SM):
-//   warps 0-3  producers: y_s = a_s * qhat_inv (Shoup), 16-byte st.shared of
-//              4 sources per row into the K-major A ring (kAStages tiles)
-//   warps 4-7  epilogue: TMEM -> fold -> Barrett mod p_t -> coalesced stores
-//   warp 8     TMEM owner; one elected lane issues the MMAs
+//   warps 0-3  producers: source segments arrive by bulk copy (TMA engine)
+//              kRawBC tiles ahead; y_s = a_s * qhat_inv (Shoup), 16-byte
+//              st.shared of 4 sources per row into the K-major A ring
+//   warps 4-11 epilogue: TMEM -> fold -> Montgomery mod p_t -> coalesced stores
+//              (two warps per TMEM lane group, each half of a target chunk)
+//   warp 12    TMEM owner; one elected lane issues the MMAs
 // The kernel is HBM-bound for small alpha (alpha*4 bytes read, T*4 written
 // per coefficient); the tensor cores remove the alpha*T mul-mods per
 // coefficient that bound the CUDA-core form at large alpha.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -44,9 +48,14 @@ constexpr int kAStages = 4;
 constexpr int kChunk = 32;           // targets per MMA (N)
 constexpr int kMaxChunks = kMaxBconvDst / kChunk;
 constexpr int kMaxKC = 2;            // 32-byte K-steps (alpha <= 16)
-constexpr int kThreadsBC = 288;
+constexpr int kEpiWarpsBC = 8;
+constexpr int kMmaWarpBC = 4 + kEpiWarpsBC;
+constexpr int kThreadsBC = 32 * (kMmaWarpBC + 1);
 constexpr int kATileBC = kRowsBC * 32;           // 4 KB per K-step
 constexpr int kBTileBC = kChunk * 32;            // 1 KB per (i, chunk, K-step)
+constexpr int kRawBC = 6;                        // raw input tiles in flight (TMA ring)
+constexpr int kMaxSrcBC = 16;
+constexpr int kRawTileBC = kMaxSrcBC * kRowsBC * 4;   // 8 KB: 128 coefficients x 16 sources
 
 struct BconvTcArgs {
   const uint32_t* in;
@@ -68,22 +77,30 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
   const int KC = a.KC, nch = a.nchunks;
   uint8_t* sB = smem;                                              // [i][chunk][kc] tiles
   uint8_t* sA = sB + 4 * kMaxChunks * kMaxKC * kBTileBC;           // [stage][kc] tiles
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(sA + kAStages * kMaxKC * kATileBC);
+  uint8_t* sRaw = sA + kAStages * kMaxKC * kATileBC;               // [slot][src][128] u32
+  uint32_t* sQ = reinterpret_cast<uint32_t*>(sRaw + kRawBC * kRawTileBC);  // per target
+  uint32_t* sQinv = sQ + kMaxBconvDst;                             // -q^-1 mod 2^32
+  int* sCopy = reinterpret_cast<int*>(sQinv + kMaxBconvDst);      // copy list: t | s << 16
+  uint32_t* sSkip = reinterpret_cast<uint32_t*>(sCopy + kMaxBconvDst);  // per 16 targets
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sSkip + kMaxBconvDst / 16);
   uint64_t* a_empty = a_full + kAStages;
   uint64_t* acc_full = a_empty + kAStages;
   uint64_t* acc_empty = acc_full + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 4);
+  uint64_t* raw_full = acc_empty + 4;
+  uint64_t* raw_empty = raw_full + kRawBC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + kRawBC);
 
   const int tid = threadIdx.x, warp = tid >> 5;
 
-  // constant operand: B_i[4s + j][t] = byte i of (2^(8j) F[s][t] mod p_t)
+  // constant operand: B_i[4s + j][t] = byte i of (2^(8j+32) F[s][t] mod p_t)
+  // (the 2^32 is the Montgomery factor the epilogue's REDC removes)
   for (int w = tid; w < 4 * kMaxChunks * kMaxKC * kBTileBC / 4; w += blockDim.x)
     reinterpret_cast<uint32_t*>(sB)[w] = 0;
   __syncthreads();
   for (int e = tid; e < ba.n_src * ba.n_dst; e += blockDim.x) {
     const int s = e / ba.n_dst, t = e % ba.n_dst;
     const PrimeConst pt = a.pc[ba.dst_prime[t]];
-    const uint64_t f = ba.factor[s * kMaxBconvDst + t];
+    const uint64_t f = reduce64((uint64_t)ba.factor[s * kMaxBconvDst + t] << 32, pt.q, pt.mu);
     const int ch = t / kChunk, tr = t % kChunk;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -95,18 +112,44 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
             (uint8_t)(v >> (8 * i));
     }
   }
+  for (int t = tid; t < kMaxBconvDst; t += blockDim.x) {
+    const bool live = t < ba.n_dst;
+    const PrimeConst pt = a.pc[live ? ba.dst_prime[t] : ba.dst_prime[0]];
+    sQ[t] = pt.q;
+    sQinv[t] = pt.qneg_inv;
+  }
+  int n_copy = 0;
+  for (int t = 0; t < ba.n_dst; ++t) n_copy += ba.copy_from[t] >= 0;
+  if (tid < kMaxBconvDst / 16) {
+    // epilogue skip mask per 16 targets: copies (stored by the producers) and padding
+    uint32_t m = 0;
+    for (int e = 0; e < 16; ++e) {
+      const int t = tid * 16 + e;
+      if (t >= ba.n_dst || ba.copy_from[t] >= 0) m |= 1u << e;
+    }
+    sSkip[tid] = m;
+  }
+  if (tid == 0) {
+    int k = 0;
+    for (int t = 0; t < ba.n_dst; ++t)
+      if (ba.copy_from[t] >= 0) sCopy[k++] = t | (ba.copy_from[t] << 16);
+  }
   if (tid == 0) {
     for (int s = 0; s < kAStages; ++s) {
       mbar_init(&a_full[s], 128);
       mbar_init(&a_empty[s], 1);
     }
+    for (int s = 0; s < kRawBC; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], 128);
+    }
     for (int b = 0; b < 4; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 128);
+      mbar_init(&acc_empty[b], 32 * kEpiWarpsBC);
     }
     fence_mbar_init();
   }
-  if (warp == 8) tmem_alloc<512>(tmem_slot);
+  if (warp == kMmaWarpBC) tmem_alloc<512>(tmem_slot);
   fence_proxy_async_smem();  // B tiles written by the generic proxy, read by the MMA
   tc_fence_before();
   __syncthreads();
@@ -120,36 +163,71 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
 
   if (warp < 4) {
     // ---------------------------------------------------------------- producers
+    // Raw tiles (128 coefficients of each source row, contiguous 512-byte
+    // segments) arrive by bulk copy kRawBC tiles ahead (one elected thread);
+    // each thread then converts its coefficient: y_s = a_s * qhat_inv_s.
     const int r = tid;
+    const int nsrc = ba.n_src;
+    uint32_t qs[kMaxSrcBC], hs[kMaxSrcBC], hss[kMaxSrcBC];
+#pragma unroll
+    for (int s = 0; s < kMaxSrcBC; ++s) {
+      qs[s] = s < nsrc ? a.pc[ba.src_prime[s]].q : 1;
+      hs[s] = s < nsrc ? ba.qhat_inv[s] : 0;
+      hss[s] = s < nsrc ? ba.qhat_inv_shoup[s] : 0;
+    }
+    auto issue = [&](int it) {
+      const int slot = it % kRawBC;
+      const int64_t x0 = (t_lo + it) * kRowsBC;
+      const uint32_t cnt = (uint32_t)std::min<int64_t>(kRowsBC, a.per_row - x0);
+      mbar_arrive_expect_tx(&raw_full[slot], cnt * 4 * nsrc);
+      for (int s = 0; s < nsrc; ++s)
+        bulk_g2s(sRaw + slot * kRawTileBC + s * kRowsBC * 4, a.in + (int64_t)s * a.per_row + x0,
+                 cnt * 4, &raw_full[slot]);
+    };
+    if (tid == 0)
+      for (int it = 0; it < kRawBC && it < n_tiles; ++it) issue(it);
     for (int it = 0; it < n_tiles; ++it) {
-      const int st = it % kAStages;
+      const int st = it % kAStages, slot = it % kRawBC;
       if (it >= kAStages) mbar_wait(&a_empty[st], ((it / kAStages) & 1) ^ 1);
+      mbar_wait(&raw_full[slot], (it / kRawBC) & 1);
       const int64_t x = (t_lo + it) * kRowsBC + r;
       const bool valid = x < a.per_row;
-      uint8_t* tile = sA + st * kMaxKC * kATileBC;
-      for (int s0 = 0; s0 < 8 * KC; s0 += 4) {   // 4 sources = one 16-byte segment
-        uint32_t y[4];
+      const uint32_t* raw = reinterpret_cast<const uint32_t*>(sRaw + slot * kRawTileBC);
+      uint32_t y[kMaxSrcBC];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int s = s0 + q;
-          y[q] = 0;
-          if (valid && s < ba.n_src) {
-            const uint32_t v = __ldg(a.in + (int64_t)s * a.per_row + x);
-            y[q] = mul_shoup(v, ba.qhat_inv[s], ba.qhat_inv_shoup[s],
-                             a.pc[ba.src_prime[s]].q);
-          }
+      for (int s = 0; s < kMaxSrcBC; ++s)
+        y[s] = (valid && s < nsrc) ? mul_shoup(raw[s * kRowsBC + r], hs[s], hss[s], qs[s]) : 0;
+      // targets that are source primes copy the source row through (rns.py:140-142)
+      if (valid)
+        for (int c = 0; c < n_copy; ++c) {
+          const int e = sCopy[c];
+          a.out[(int64_t)(e & 0xFFFF) * a.per_row + x] = raw[(e >> 16) * kRowsBC + r];
         }
+      mbar_arrive(&raw_empty[slot]);
+      uint8_t* tile = sA + st * kMaxKC * kATileBC;
+#pragma unroll
+      for (int s0 = 0; s0 < kMaxSrcBC; s0 += 4) {   // 4 sources = one 16-byte segment
+        if (s0 >= 8 * KC) break;
         const int k = 4 * s0;
         *reinterpret_cast<uint4*>(tile + (k >> 5) * kATileBC + tile_off_bc(r, k & 31, kRowsBC)) =
-            make_uint4(y[0], y[1], y[2], y[3]);
+            make_uint4(y[s0], y[s0 + 1], y[s0 + 2], y[s0 + 3]);
       }
       fence_proxy_async_smem();
       mbar_arrive(&a_full[st]);
+      // refill this raw slot once every producer thread has read it
+      if (tid == 0 && it + kRawBC < n_tiles) {
+        mbar_wait(&raw_empty[slot], (it / kRawBC) & 1);
+        issue(it + kRawBC);
+      }
     }
-  } else if (warp < 8) {
+  } else if (warp < 4 + kEpiWarpsBC) {
     // ---------------------------------------------------------------- epilogue
-    const int ew = warp - 4, r = ew * 32 + (tid & 31);
-    const uint32_t lane_base = tmem + ((uint32_t)(ew * 32) << 16);
+    // warp 4 + 4h + g reads TMEM lane group g (rows 32g..32g+31) and the
+    // targets [16h, 16h + 16) of each 32-target chunk.  The fold
+    // v = sum_i 2^(8i) C_i (< 2^48) is reduced by one Montgomery step
+    // (R = 2^32, compensated in the constant operand: V_j carries 2^32).
+    const int g = (warp - 4) & 3, h = (warp - 4) >> 2, r = g * 32 + (tid & 31);
+    const uint32_t lane_base = tmem + ((uint32_t)(g * 32) << 16);
     int u = 0;
     for (int it = 0; it < n_tiles; ++it) {
       const int64_t x = (t_lo + it) * kRowsBC + r;
@@ -158,37 +236,31 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
         const int buf = u & 3;
         mbar_wait(&acc_full[buf], (u >> 2) & 1);
         tc_fence_after();
-        uint32_t c[4][16], d[4][16];
+        uint32_t c[4][16];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          tmem_ld16(lane_base + buf * 128 + i * kChunk, c[i]);
-          tmem_ld16(lane_base + buf * 128 + i * kChunk + 16, d[i]);
-        }
+        for (int i = 0; i < 4; ++i) tmem_ld16(lane_base + buf * 128 + i * kChunk + h * 16, c[i]);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&acc_empty[buf]);
-        if (!valid) continue;
-        const int tb = ch * kChunk;
+        const int tb = ch * kChunk + h * 16;
+        if (!valid || tb >= ba.n_dst) continue;
+        const uint32_t skip = sSkip[tb >> 4];
+        uint32_t qv[16], qi[16];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int e = 0; e < 16; e += 4) {
+          const uint4 q4 = *reinterpret_cast<const uint4*>(sQ + tb + e);
+          const uint4 i4 = *reinterpret_cast<const uint4*>(sQinv + tb + e);
+          qv[e] = q4.x; qv[e + 1] = q4.y; qv[e + 2] = q4.z; qv[e + 3] = q4.w;
+          qi[e] = i4.x; qi[e + 1] = i4.y; qi[e + 2] = i4.z; qi[e + 3] = i4.w;
+        }
+        uint32_t* o = a.out + (int64_t)tb * a.per_row + x;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int t = tb + h * 16 + e;
-            if (t >= ba.n_dst) break;
-            const uint32_t c0 = h ? d[0][e] : c[0][e], c1 = h ? d[1][e] : c[1][e];
-            const uint32_t c2 = h ? d[2][e] : c[2][e], c3 = h ? d[3][e] : c[3][e];
-            uint32_t v;
-            const int cp = ba.copy_from[t];
-            if (cp >= 0) {
-              v = __ldg(a.in + (int64_t)cp * a.per_row + x);
-            } else {
-              const PrimeConst pt = a.pc[ba.dst_prime[t]];
-              const uint64_t f = (uint64_t)c0 + ((uint64_t)c1 << 8) + ((uint64_t)c2 << 16) +
-                                 ((uint64_t)c3 << 24);
-              v = reduce64(f, pt.q, pt.mu);
-            }
-            a.out[(int64_t)t * a.per_row + x] = v;
-          }
+        for (int e = 0; e < 16; ++e) {
+          const uint32_t lo = c[0][e] + (c[1][e] << 8), hi = c[2][e] + (c[3][e] << 8);
+          const uint64_t f = (uint64_t)lo + ((uint64_t)hi << 16);
+          const uint32_t m = (uint32_t)f * qi[e];
+          const uint32_t w = (uint32_t)((f + (uint64_t)m * qv[e]) >> 32);
+          if (!((skip >> e) & 1)) o[(int64_t)e * a.per_row] = w >= qv[e] ? w - qv[e] : w;
         }
       }
     }
@@ -228,7 +300,7 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kMmaWarpBC) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -252,7 +324,8 @@ int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArg
   a.KC = (4 * ba.n_src + 31) / 32;
   a.nchunks = (ba.n_dst + kChunk - 1) / kChunk;
   const int smem = 4 * kMaxChunks * kMaxKC * kBTileBC + kAStages * kMaxKC * kATileBC +
-                   (2 * kAStages + 8) * 8 + 16;
+                   kRawBC * kRawTileBC + kMaxBconvDst * (4 + 4 + 4) + kMaxBconvDst / 16 * 4 +
+                   (2 * kAStages + 8 + 2 * kRawBC) * 8 + 16;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(bconv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

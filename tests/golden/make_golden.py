@@ -62,6 +62,11 @@ def p_default():
     return RP.CkksParams(n=1 << 16, l_max=44, k=1, dnum=45, chain=chain)
 
 
+def p_dnum5():
+    chain = RP.generate_chain_widths(1 << 16, [29] * 17 + [28] * 28, [30] * 9)
+    return RP.CkksParams(n=1 << 16, l_max=44, k=9, dnum=5, chain=chain)
+
+
 def make_params():
     doc = {"presets": {}, "adhoc": {}}
     for name in RP.PRESETS:
@@ -210,6 +215,9 @@ LARGE_CASES = [
     # last slice holds one limb (level 4) / groups mix 2- and 1-limb slices
     ("set_c_l4", lambda: RP.CkksParams.from_preset("set_c"), 4, 24),
     ("set_c_l2", lambda: RP.CkksParams.from_preset("set_c"), 2, 25),
+    # dnum-reduced N=2^16 set (alpha = K = 9): 9-term tensor-core base
+    # conversions in ModUp and ModDown; level 12 = one full + one ragged slice
+    ("p_dnum5_l12", p_dnum5, 12, 26),
 ]
 
 

@@ -23,7 +23,7 @@ SMALL = [("small_full", "small", 5, 11), ("small_l4", "small", 4, 12),
          ("set_a_full", "set_a", 1, 15), ("set_b_full", "set_b", 2, 16)]
 LARGE = [("n16_l3", "n16", 3, 21), ("resnet20_l3", "resnet20", 3, 22),
          ("set_c_full", "set_c", 7, 23), ("set_c_l4", "set_c", 4, 24),
-         ("set_c_l2", "set_c", 2, 25)]
+         ("set_c_l2", "set_c", 2, 25), ("p_dnum5_l12", "p_dnum5", 12, 26)]
 
 
 def _params(kind):

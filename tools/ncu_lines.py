@@ -1,6 +1,6 @@
 """Aggregate ncu SASS-level samples / executed instructions per CUDA source line.
 
-usage: ncu_lines.py <ncu source csv (sass)> <nvdisasm --print-line-info dump> <mangled kernel> [N]
+usage: ncu_lines.py <ncu source csv (sass)> <nvdisasm --print-line-info dump> <mangled kernel> [N] [source.cu]
 """
 import csv, re, sys
 from collections import Counter
@@ -29,7 +29,7 @@ samp, exe = Counter(), Counter()
 for a, s, e in recs:
     ln = off2line.get(a - base, -1)
     samp[ln] += s; exe[ln] += e
-src = open("paper_2212_14191_b200/csrc/ntt_ts.cu").read().split("\n")
+src = open(sys.argv[5] if len(sys.argv) > 5 else "paper_2212_14191_b200/csrc/ntt_ts.cu").read().split("\n")
 tot = sum(samp.values()); tote = sum(exe.values())
 N = int(sys.argv[4]) if len(sys.argv) > 4 else 30
 print(f"total samples {tot}, executed {tote}")
