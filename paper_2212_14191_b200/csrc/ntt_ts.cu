@@ -44,7 +44,6 @@ namespace {
 
 constexpr int kNC = 16;                  // data columns per chunk
 constexpr int kRing = 4;                 // smem operand ring depth (chunks)
-constexpr int kRaw = 4;                  // TMA raw-data ring depth (chunks in flight)
 // 4 warpgroups: producers (warps 0-3), epilogue (4-11), MMA issuer (warp 12;
 // warps 13-15 idle).  Registers are rebalanced with setmaxnreg: each SMSP
 // holds one warp of every warpgroup, so 96 + 2 * 176 + 64 <= 512 per lane.
@@ -124,33 +123,34 @@ TFHE_DEV uint32_t ring_off(int row, int k) {
 }
 
 // iteration state shared by the three roles: every role walks the same unit
-// sequence (limb, chunk) and the same ring / accumulator phases
+// sequence (limb, chunk) and the same ring / accumulator phases.  Chunks of a
+// limb run column-block-major: c = (x0 / kNC) * batch + b, so the batch
+// members sharing a column block (and its epilogue operands: W2 twiddles in
+// stage 1, switching-key columns in the fused key switch) are consecutive.
 struct UnitIter {
   int limb, c, b, x0;
   int sl;         // slice within the (limb, chunk) group (EPI_KS_ACC)
   int S;          // slices per group
+  int nb;         // batch members
   int s;          // ring slot
   uint32_t rph;   // ring phase parity of slot s
   int ab;         // accumulator buffer
   uint32_t aph;   // accumulator phase parity
-  TFHE_DEV void init(long long g0, int C, int logR, int R, int S_) {
+  TFHE_DEV void init(long long g0, int C, int nb_, int S_) {
     limb = (int)(g0 / C);
     c = (int)(g0 % C);
-    set_col(logR, R);
+    nb = nb_;
+    b = c % nb;
+    x0 = (c / nb) * kNC;
     sl = 0; S = S_;
     s = 0; rph = 0; ab = 0; aph = 0;
   }
-  TFHE_DEV void set_col(int logR, int R) {
-    const int col0 = c * kNC;
-    b = col0 >> logR;
-    x0 = col0 & (R - 1);
-  }
-  TFHE_DEV void next(int C, int logR, int R) {
+  TFHE_DEV void next(int C) {
     if (++sl == S) {
       sl = 0;
-      if (++c == C) { c = 0; ++limb; }
+      if (++c == C) { c = 0; ++limb; b = 0; x0 = 0; }
+      else if (++b == nb) { b = 0; x0 += kNC; }
     }
-    set_col(logR, R);
     if (++s == kRing) { s = 0; rph ^= 1; }
     ab ^= 1;
     if (ab == 0) aph ^= 1;
@@ -166,8 +166,27 @@ TFHE_DEV uint32_t ring_off_mn(int j, int c, int k) {
 }
 
 
-constexpr int kWarpStg = 10 * 1024;               // per epilogue warp: in[2][4] | out[2] tiles
-constexpr int kStgBytes = kEpiWarps * kWarpStg;   // all epilogue warps
+// Epilogue staging per warp: in[2][T] operand tiles (double-buffered
+// prefetch) | out[2] transpose tiles, 1 KB each; T depends on what the
+// epilogue reads: W2 (stage 1), nothing (store), x + base (ModDown /
+// rescale), key rows + accumulators (fused key switch).
+template <int STAGE, int MODE>
+__host__ __device__ constexpr int in_tiles() {
+  return STAGE == 1 ? 1 : MODE == EPI_STORE ? 0 : MODE == EPI_SUB_SCALE ? 2 : 4;
+}
+template <int STAGE, int MODE>
+__host__ __device__ constexpr int warp_stg_bytes() { return (2 * in_tiles<STAGE, MODE>() + 2) * 1024; }
+// TMA raw-data ring depth: whatever shared memory the operand ring and the
+// epilogue staging leave (up to 8 chunks in flight hides DRAM latency)
+constexpr int kSmemBudget = 226 * 1024;
+template <int STAGE, int K, int MODE>
+__host__ __device__ constexpr int raw_slots() {
+  return (kSmemBudget - kRing * ring_stage_bytes<K>() - kEpiWarps * warp_stg_bytes<STAGE, MODE>()) /
+                     (K * 64) > 8
+             ? 8
+             : (kSmemBudget - kRing * ring_stage_bytes<K>() -
+                kEpiWarps * warp_stg_bytes<STAGE, MODE>()) / (K * 64);
+}
 
 // 32 rows x 64 B staging, 16-byte chunks XOR-swizzled so both the row-wise
 // and the 4-lanes-per-row accesses are bank-conflict free
@@ -220,6 +239,11 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
   constexpr int KC = K / 32;
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int kRawBytes = K * 64;            // one raw data chunk (16 u32 x K)
+  constexpr int kRaw = raw_slots<STAGE, K, MODE>();
+  static_assert(kRaw >= 2, "shared memory budget leaves no TMA ring");
+  constexpr int kWarpStg = warp_stg_bytes<STAGE, MODE>();
+  constexpr int kStgBytes = kEpiWarps * kWarpStg;
+  constexpr int kInBuf = in_tiles<STAGE, MODE>() * 1024;  // one prefetch buffer
   uint8_t* stg = smem + kRing * kStageBytes;  // epilogue staging
   uint64_t* b_full = reinterpret_cast<uint64_t*>(stg + kStgBytes + kRaw * kRawBytes);
   uint64_t* b_empty = b_full + kRing;
@@ -246,7 +270,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
   const long long G = (long long)a.n_limbs * a.C;
   const long long g0 = G * grp / groups;
   const int cnt = (int)(G * (grp + 1) / groups - g0) * a.S;
-  const int C = a.C, R = a.R, logR = 31 - __clz(a.R);
+  const int C = a.C;
 
   if (tid == 0) {
     for (int s = 0; s < kRing; ++s) {
@@ -270,7 +294,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   UnitIter w;
-  w.init(g0, C, logR, R, a.S);
+  w.init(g0, C, a.batch, a.S);
   // Each role's register budget is set at the top of its own branch so that
   // ptxas allocates every role's code under the matching setmaxnreg limit.
   if (warp < 4) {
@@ -303,9 +327,9 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     };
     UnitIter ahead = w;
     if (tid == 0 && !(kDbg & 32)) {
-      for (int i = 0; i < kRaw && i < cnt; ++i, ahead.next(C, logR, R)) issue_raw(ahead, i);
+      for (int i = 0; i < kRaw && i < cnt; ++i, ahead.next(C)) issue_raw(ahead, i);
     }
-    for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
+    for (int i = 0; i < cnt; ++i, w.next(C)) {
       const int rs = i % kRaw;
       const uint32_t rph = (uint32_t)((i / kRaw) & 1);
       if (warp == 0) TS_TRACE(7, i);
@@ -354,7 +378,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
         // refill this raw slot once every producer thread has read it
         mbar_wait(&raw_empty[rs], rph);
         issue_raw(ahead, rs);
-        ahead.next(C, logR, R);
+        ahead.next(C);
       }
     }
   } else if (warp < 4 + kEpiWarps) {
@@ -368,13 +392,13 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     const int wq = warp & 3, hf = (warp - 4) >> 2, cb = hf * kCW;
     const int m = wq * 32 + lane;          // TMEM lane = twiddle row within the half
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    uint8_t* wstg = stg + (warp - 4) * kWarpStg;   // in[2][4] tiles | out[2] tiles (1 KB each)
+    uint8_t* wstg = stg + (warp - 4) * kWarpStg;   // in[2][T] tiles | out[2] tiles (1 KB each)
     constexpr int mode = STAGE == 2 ? MODE : EPI_STORE;
     // Epilogue operands (W2 tile, x/base rows, key rows, accumulators) are
     // fetched one chunk ahead with cp.async into a double-buffered staging
     // area: 32 rows x 32 bytes per tile, 2 lanes per row (full sectors).
     auto prefetch = [&](const UnitIter& it, int buf) {
-      uint8_t* dstb = wstg + buf * 4096;
+      uint8_t* dstb = wstg + buf * kInBuf;
       if (STAGE == 1) {
         // W2 * 2^96 in [prime][i2][k1] layout: for each of this warp's 8 i2
         // columns the warp's 32 k1 rows are 128 contiguous bytes -> staged as
@@ -425,7 +449,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       }
     };
     auto read_row = [&](int buf, int tI, uint32_t (&v)[kCW]) {
-      const uint8_t* t = wstg + buf * 4096 + tI * 1024;
+      const uint8_t* t = wstg + buf * kInBuf + tI * 1024;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         uint4 u = *reinterpret_cast<const uint4*>(t + stg8_off(lane, q));
@@ -435,7 +459,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     // coalesced store of this warp's 32 rows x 8 values (row stride in elements):
     // transposed through smem so each store instruction writes 16 full sectors
     auto store_tile = [&](int oI, const uint32_t (&v)[kCW], uint32_t* dst, size_t row_stride) {
-      uint8_t* t = wstg + 8192 + oI * 1024;
+      uint8_t* t = wstg + 2 * kInBuf + oI * 1024;
 #pragma unroll
       for (int q = 0; q < 2; ++q)
         *reinterpret_cast<uint4*>(t + stg8_off(lane, q)) =
@@ -451,10 +475,12 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     UnitIter ahead = w;
     if (cnt > 0 && !(kDbg & 64)) prefetch(ahead, 0);
     uint32_t regb[kCW], rega[kCW];   // EPI_KS_ACC group accumulators
+    uint64_t lzb[kCW], lza[kCW];     // ... and their pending lazy sums
+    int npend = 0;
     cp_async_commit();
     int prev = -1;
     PrimeConst pc;
-    for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
+    for (int i = 0; i < cnt; ++i, w.next(C)) {
       const int limb = w.limb;
       const int prime = a.map.prime[limb];
       const int buf = i & 1;
@@ -483,7 +509,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       const int b = w.b;
       __syncwarp();  // every lane is done with the staging buffer about to be refilled
       if (i + 1 < cnt) {
-        ahead.next(C, logR, R);
+        ahead.next(C);
         if (!(kDbg & 64)) prefetch(ahead, buf ^ 1);
       }
       cp_async_commit();
@@ -524,7 +550,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       cp_async_wait1();   // this chunk's operand tiles have landed (own copies)
       __syncwarp();       // ... and every lane's copies are visible
       if (STAGE == 1) {
-        const uint8_t* wt = wstg + buf * 4096;
+        const uint8_t* wt = wstg + buf * kInBuf;
 #pragma unroll
         for (int e = 0; e < kCW; ++e)
           y[e] = mont_reduce((uint64_t)y[e] * *reinterpret_cast<const uint32_t*>(wt + e * 128 + lane * 4), pc);
@@ -538,7 +564,10 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
       const size_t wrow = (size_t)(h * 128 + wq * 32) * a.n1 + w.x0 + cb;
       if (mode == EPI_KS_ACC) {
         // y is in Montgomery form (twiddles carry 2^96); the S slices of this
-        // (target, chunk) group accumulate in registers, acc touches HBM once
+        // (target, chunk) group accumulate in registers, acc touches HBM once.
+        // Products y R * k (< q^2) are summed lazily in 64 bits -- one
+        // IMAD.WIDE each -- and reduced (Barrett, then one Montgomery step to
+        // drop R) every ks_lazy slices and at the group end.
         if (w.sl == 0) {
           if (a.epi.init_acc[limb]) {
             read_row(buf, 2, regb);
@@ -547,6 +576,9 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
 #pragma unroll
             for (int e = 0; e < kCW; ++e) regb[e] = rega[e] = 0;
           }
+#pragma unroll
+          for (int e = 0; e < kCW; ++e) lzb[e] = lza[e] = 0;
+          npend = 0;
         }
         if (a.epi.j0 + w.sl != a.epi.js[limb]) {
           uint32_t kb[kCW], ka[kCW];
@@ -554,9 +586,19 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
           read_row(buf, 1, ka);
 #pragma unroll
           for (int e = 0; e < kCW; ++e) {
-            regb[e] = add_mod(regb[e], mont_reduce((uint64_t)y[e] * kb[e], pc), pc.q);
-            rega[e] = add_mod(rega[e], mont_reduce((uint64_t)y[e] * ka[e], pc), pc.q);
+            lzb[e] += (uint64_t)y[e] * kb[e];
+            lza[e] += (uint64_t)y[e] * ka[e];
           }
+          ++npend;
+        }
+        if (npend && (npend == a.epi.ks_lazy || w.sl == w.S - 1)) {
+#pragma unroll
+          for (int e = 0; e < kCW; ++e) {
+            regb[e] = add_mod(regb[e], mont_reduce(reduce64(lzb[e], pc.q, pc.mu), pc), pc.q);
+            rega[e] = add_mod(rega[e], mont_reduce(reduce64(lza[e], pc.q, pc.mu), pc), pc.q);
+            lzb[e] = lza[e] = 0;
+          }
+          npend = 0;
         }
         if (w.sl == w.S - 1) {
           const size_t ar = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n + wrow;
@@ -651,7 +693,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
     };
     int prev = -1;
     uint32_t twph = 0;
-    for (int i = 0; i < cnt; ++i, w.next(C, logR, R)) {
+    for (int i = 0; i < cnt; ++i, w.next(C)) {
       if (w.limb != prev) {
         if (handshake) {
           if (prev >= 0) twph ^= 1;
@@ -685,8 +727,9 @@ role_done:
 
 template <int STAGE, int K, int MODE>
 int launch_ts(const Ctx& c, TsArgs& a, cudaStream_t st) {
-  const int smem = kRing * ring_stage_bytes<K>() + kStgBytes + kRaw * K * 64 +
-                   (2 * kRing + 5 + 2 * kRaw) * 8 + 16;
+  constexpr int kRaw = raw_slots<STAGE, K, MODE>();
+  const int smem = kRing * ring_stage_bytes<K>() + kEpiWarps * warp_stg_bytes<STAGE, MODE>() +
+                   kRaw * K * 64 + (2 * kRing + 5 + 2 * kRaw) * 8 + 16;
   auto kern = ntt_ts_kernel<STAGE, K, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const long long U = (long long)a.n_limbs * a.C;
@@ -989,6 +1032,14 @@ int launch_ntt_ts_ks_group(const Ctx& c, const uint32_t* in, void* ws, const Lim
   a.map = tmap;
   a.epi = epi;
   a.epi.mode = EPI_KS_ACC;
+  {
+    // lazy slice sums: k products of (q-1)^2 must fit in 64 bits
+    uint64_t qm = 2;
+    for (int l = 0; l < tmap.n; ++l) qm = std::max<uint64_t>(qm, c.primes[tmap.prime[l]]);
+    const unsigned __int128 sq = (unsigned __int128)(qm - 1) * (qm - 1);
+    const uint64_t k = (uint64_t)(((unsigned __int128)~0ull) / sq);
+    a.epi.ks_lazy = (int)std::max<uint64_t>(1, std::min<uint64_t>(k, 1u << 20));
+  }
   a.in = static_cast<const uint32_t*>(ws);
   a.out = nullptr;
   a.twa = c.d_twa_ks;

@@ -65,6 +65,7 @@ struct EpiArgs {
   int j0;                   // first slice of the group
   int16_t js[kMaxLimbs];    // slice that owns target row l (-1: none) -> skipped
   int16_t init_acc[kMaxLimbs];  // 1: start from acc, 0: start from zero
+  int ks_lazy;                  // slice products summed in 64 bits between reductions
 };
 
 struct Ctx {
