@@ -259,6 +259,28 @@ class CkksContext:
         d = self.dev.eltwise(_lib.OP_ADD, c0.data, c1.data, rows)
         return CiphertextBatch(data=d, level=c0.level, scale=c0.scale)
 
+    def cmult_batch(self, cb: CiphertextBatch, pt):
+        """Plaintext product (ref `ckks.py:258-263`) of every member: pt is a
+        (level+1, B, N) NTT-domain tensor (one plaintext per member) or a
+        single `Plaintext` / (level+1, N) tensor shared by the batch."""
+        basis = self.params.q_basis(cb.level)
+        l1, B, n = len(basis), cb.batch_size, cb.n
+        scale = cb.scale
+        if isinstance(pt, Plaintext):
+            if pt.level != cb.level:
+                raise ParameterError("plaintext level does not match ciphertext")
+            scale = cb.scale * pt.scale
+            pt = pt.poly.rows
+        t, _ = to_device(pt, self.dev.device)
+        if tuple(t.shape) == (l1, n):
+            t = t.unsqueeze(1).expand(l1, B, n).contiguous()
+        if tuple(t.shape) != (l1, B, n):
+            raise ParameterError("plaintext batch must be (level+1, B, N) or (level+1, N)")
+        out = torch.empty_like(cb.data)
+        for c in range(2):
+            self.dev.eltwise(_lib.OP_MUL, cb.data[c], t, basis, out=out[c])
+        return CiphertextBatch(data=out, level=cb.level, scale=scale)
+
     def hsub_batch(self, c0: CiphertextBatch, c1: CiphertextBatch):
         rows = self.params.q_basis(c0.level) * 2
         d = self.dev.eltwise(_lib.OP_SUB, c0.data, c1.data, rows)

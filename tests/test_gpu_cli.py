@@ -1,0 +1,78 @@
+"""CLI on the B200 (ref tests `test_cli.py`): selftest passes on the device
+path, bench rows follow the CSV schema with ops_per_sec = batch * 1000 /
+wall_ms, sweep-n emits one row per degree; cmult_batch parity."""
+
+import csv
+import json
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def run(argv):
+    from paper_2212_14191_b200 import cli
+    return cli.main(argv)
+
+
+def test_selftest_default(capsys):
+    assert run(["selftest", "--preset", "default"]) == 0
+    assert "transform: PASS" in capsys.readouterr().out
+
+
+def test_selftest_fault_injection(capsys, monkeypatch):
+    from paper_2212_14191_b200 import cli
+    monkeypatch.setattr(cli, "INJECT_TWIDDLE_FAULT", True)
+    assert run(["selftest"]) == 1
+    assert "transform: FAIL" in capsys.readouterr().out
+
+
+@pytest.mark.parametrize("resident", [False, True])
+def test_bench_schema_and_rate_identity(tmp_path, resident):
+    from paper_2212_14191_b200 import cli
+    out = tmp_path / "b.csv"
+    argv = ["bench", "--ops", "ntt,hadd,hmult,rescale,hrotate,cmult,forbenius_map,intt",
+            "--batch-sizes", "1,4", "--reps", "2", "--out", str(out)]
+    assert run(argv + (["--resident"] if resident else [])) == 0
+    rows = list(csv.DictReader(out.open()))
+    assert [r["op"] for r in rows] == [o for o in ("ntt", "hadd", "hmult", "rescale", "hrotate",
+                                                   "cmult", "forbenius_map", "intt")
+                                       for _ in range(2)]
+    assert list(rows[0]) == cli.CSV_FIELDS
+    for r in rows:
+        rate = float(r["batch"]) * 1000.0 / float(r["wall_ms_median"])
+        assert abs(rate - float(r["ops_per_sec"])) / rate < 0.01
+
+
+def test_bench_json_and_sweep(tmp_path):
+    out = tmp_path / "b.json"
+    assert run(["bench", "--ops", "ntt", "--batch-sizes", "2", "--reps", "1",
+                "--out", str(out), "--preset", "p_default"]) == 0
+    assert json.loads(out.read_text())[0]["n"] == 1 << 16
+    out = tmp_path / "s.csv"
+    assert run(["sweep-n", "--n-values", "1024,2048,65536", "--batch-sizes", "2",
+                "--reps", "1", "--out", str(out)]) == 0
+    assert [int(r["n"]) for r in csv.DictReader(out.open())] == [1024, 2048, 65536]
+
+
+def test_cmult_batch_vs_oracle():
+    from oracle import oracle as O
+    from paper_2212_14191_b200.ckks import CiphertextBatch, CkksContext
+    from paper_2212_14191_b200.params import CkksParams
+    p = CkksParams.from_preset("set_b")
+    ck = CkksContext(p)
+    rng = np.random.default_rng(7)
+    basis = p.q_basis(p.l_max)
+    ct = np.stack([O.uniform_rows(rng, basis, (3, p.n)) for _ in range(2)])
+    pt = O.uniform_rows(rng, basis, (3, p.n))
+    d = lambda a: torch.from_numpy(a.view(np.int32)).cuda()  # noqa: E731
+    got = ck.cmult_batch(CiphertextBatch(d(ct), p.l_max), d(pt)).data.cpu().numpy().view(np.uint32)
+    for c in range(2):
+        assert np.array_equal(got[c], O.hada_mult(ct[c], pt, basis))
+    shared = pt[:, 0]
+    got = ck.cmult_batch(CiphertextBatch(d(ct), p.l_max), d(np.ascontiguousarray(shared)))
+    got = got.data.cpu().numpy().view(np.uint32)
+    for c in range(2):
+        assert np.array_equal(got[c], O.hada_mult(ct[c], shared[:, None, :], basis))
