@@ -241,6 +241,34 @@ def make_ckks():
         json.dump(rec, fh, indent=1)
 
 
+def make_tfhe1():
+    """Reference-written TFHE1 blobs of synthetic objects (small params)."""
+    from fractions import Fraction
+    from rnsckks import serialize as RS
+    from rnsckks.ckks import Plaintext, PublicKey, SecretKey
+    params = RP.CkksParams.generate(n=64, l_max=3, k=2, dnum=2, bit_size=28)
+    digest = params.digest()
+    rng = np.random.default_rng(9090)
+    basis = tuple(params.chain.q[:3])
+    ext = tuple(params.chain.q) + tuple(params.chain.p)
+
+    def poly(b, dom=NTT):
+        return RnsPolynomial(rows=synth.rows(rng, b, (params.n,)), basis=b, domain=dom)
+
+    ct = Ciphertext(b=poly(basis), a=poly(basis), scale=Fraction(2 ** 40, 3), level=2)
+    swk = SwitchingKey(pairs=tuple((poly(ext), poly(ext)) for _ in range(params.dnum)))
+    out = {"digest": np.frombuffer(digest, np.uint8),
+           "poly": np.frombuffer(RS.dump_polynomial(poly(basis, COEFF), digest), np.uint8),
+           "ct": np.frombuffer(RS.dump_ciphertext(ct, digest), np.uint8),
+           "pt": np.frombuffer(RS.dump_plaintext(Plaintext(poly=poly(basis), scale=Fraction(7),
+                                                           level=2), digest), np.uint8),
+           "pk": np.frombuffer(RS.dump_public_key(PublicKey(b=poly(ext), a=poly(ext)), digest),
+                               np.uint8),
+           "sk": np.frombuffer(RS.dump_secret_key(SecretKey(s=poly(ext)), digest), np.uint8),
+           "swk": np.frombuffer(RS.dump_switching_key(swk, digest), np.uint8)}
+    np.savez_compressed(os.path.join(HERE, "tfhe1.npz"), **out)
+
+
 def add_large(names):
     """Append selected LARGE_CASES to ckks_large.json (keeps existing records)."""
     path = os.path.join(HERE, "ckks_large.json")
@@ -259,6 +287,9 @@ def add_large(names):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "tfhe1":
+        make_tfhe1()
+        sys.exit(0)
     if len(sys.argv) > 2 and sys.argv[1] == "add-large":
         add_large(sys.argv[2:])
         sys.exit(0)
@@ -267,4 +298,5 @@ if __name__ == "__main__":
     make_ntt_large(d)
     make_kernels(d)
     make_ckks()
+    make_tfhe1()
     print("golden fixtures written to", HERE)
