@@ -12,10 +12,11 @@ level-major -- and run ONE native pipeline for the whole batch
 (tfhe_hmult / tfhe_rescale / tfhe_hrotate / tfhe_keyswitch in csrc/capi.cu).
 Each member equals the reference's per-member call (cli.py:175-191).
 
-Key generation, encoding and encryption are client-side and out of scope for
-this build; keys made by the reference's
-`make_relin_key` / `make_rotation_key` (any `SwitchingKey` whose pairs cover
-chain.q ++ chain.p) are accepted directly.
+Key generation, encoding and encryption (the client side) come
+from `client.ClientMixin`: host sampling / FFT / CRT exactly as the
+reference (same seed -> same keys and ciphertexts), device transforms.  Keys
+made by the reference itself (any `SwitchingKey` whose pairs cover
+chain.q ++ chain.p) are accepted directly too.
 """
 
 from __future__ import annotations
@@ -27,6 +28,7 @@ import numpy as np
 import torch
 
 from . import _lib, kernels
+from .client import ClientMixin
 from .device import DeviceContext, to_device
 from .errors import DomainError, ParameterError
 from .ntt import BACKENDS, TwiddleTable, ntt_forward, ntt_inverse
@@ -85,7 +87,7 @@ class CiphertextBatch:
         return int(self.data.shape[3])
 
 
-class CkksContext:
+class CkksContext(ClientMixin):
     """Evaluation engine bound to one parameter set (ref `ckks.py:63-83`)."""
 
     def __init__(self, params, backend="segmented", seed=0, workers=None, device=None):

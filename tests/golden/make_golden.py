@@ -269,6 +269,46 @@ def make_tfhe1():
     np.savez_compressed(os.path.join(HERE, "tfhe1.npz"), **out)
 
 
+CLIENT_CASES = [
+    ("small", lambda: RP.CkksParams.generate(n=256, l_max=5, k=3, dnum=3, bit_size=30)),
+    ("default", lambda: RP.CkksParams.from_preset("default")),
+    ("set_a", lambda: RP.CkksParams.from_preset("set_a")),
+]
+
+
+def make_client():
+    """Reference keygen / encode / encrypt / decrypt on fixed seeds: sha256 of
+    every key and ciphertext row set, and the decoded slots (client.json)."""
+    rec = {}
+    for name, fac in CLIENT_CASES:
+        params = fac()
+        ctx = CkksContext(params, backend="butterfly", seed=99)
+        z = np.random.default_rng(5).uniform(-1, 1, params.slots) \
+            + 1j * np.random.default_rng(6).uniform(-1, 1, params.slots)
+        sk, pk = ctx.keygen()
+        rlk = ctx.make_relin_key(sk)
+        rk = ctx.make_rotation_key(sk, 1)
+        ck = ctx.make_conjugation_key(sk)
+        pt = ctx.encode(z)
+        ct = ctx.encrypt(pk, pt)
+        dec = ctx.decrypt_decode(sk, ct)
+        r = {"sk": sha(sk.s.rows), "pk_b": sha(pk.b.rows), "pk_a": sha(pk.a.rows),
+             "pt": sha(pt.poly.rows), "ct_b": sha(ct.b.rows), "ct_a": sha(ct.a.rows),
+             "scale": [pt.scale.numerator, pt.scale.denominator],
+             "dec_re": [float(v) for v in dec.real[:16]], "dec_im": [float(v) for v in dec.imag[:16]]}
+        for kname, key in (("rlk", rlk), ("rk", rk), ("ck", ck)):
+            r[kname] = [[sha(b.rows), sha(a.rows)] for b, a in key.pairs]
+        # one evaluated product through the reference, for an end-to-end check
+        m = ctx.rescale(ctx.hmult(ct, ct, rlk))
+        r["hmult_rescale_b"], r["hmult_rescale_a"] = sha(m.b.rows), sha(m.a.rows)
+        dm = ctx.decrypt_decode(sk, m)
+        r["dec_sq_re"] = [float(v) for v in dm.real[:16]]
+        rec[name] = r
+        print("client", name)
+    with open(os.path.join(HERE, "client.json"), "w") as fh:
+        json.dump(rec, fh, indent=1)
+
+
 def add_large(names):
     """Append selected LARGE_CASES to ckks_large.json (keeps existing records)."""
     path = os.path.join(HERE, "ckks_large.json")
@@ -287,6 +327,9 @@ def add_large(names):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "client":
+        make_client()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "tfhe1":
         make_tfhe1()
         sys.exit(0)
@@ -299,4 +342,5 @@ if __name__ == "__main__":
     make_kernels(d)
     make_ckks()
     make_tfhe1()
+    make_client()
     print("golden fixtures written to", HERE)

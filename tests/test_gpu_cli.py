@@ -19,7 +19,22 @@ def run(argv):
 
 def test_selftest_default(capsys):
     assert run(["selftest", "--preset", "default"]) == 0
-    assert "transform: PASS" in capsys.readouterr().out
+    out = capsys.readouterr().out
+    assert "transform: PASS" in out
+    assert "roundtrip: PASS" in out
+    assert "homomorphism: PASS" in out
+
+
+@pytest.mark.parametrize("length,rot", [(1, 0), (128, 7)])
+def test_workload_dotproduct(capsys, length, rot):
+    assert run(["workload-dotproduct", "--length", str(length)]) == 0
+    report = json.loads(capsys.readouterr().out)
+    assert report["op_counts"]["hrotate"] == rot
+    assert report["relative_error"] < 2 ** -15
+
+
+def test_workload_too_long(capsys):
+    assert run(["workload-dotproduct", "--length", "99999"]) == 2
 
 
 def test_selftest_fault_injection(capsys, monkeypatch):
