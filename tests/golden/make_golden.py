@@ -72,6 +72,7 @@ def make_params():
     for name in RP.PRESETS:
         doc["presets"][name] = chain_doc(RP.CkksParams.from_preset(name))
     doc["presets"]["p_default"] = chain_doc(p_default())
+    doc["presets"]["p_dnum5"] = chain_doc(p_dnum5())
     doc["adhoc"]["small_params"] = chain_doc(
         RP.CkksParams.generate(n=256, l_max=5, k=3, dnum=3, bit_size=30))
     for n in (16, 64, 256, 1024, 4096, 1 << 13, 1 << 14, 1 << 15, 1 << 16):
@@ -327,6 +328,14 @@ def add_large(names):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "add-preset-p_dnum5":
+        path = os.path.join(HERE, "params.json")
+        with open(path) as fh:
+            doc = json.load(fh)
+        doc["presets"]["p_dnum5"] = chain_doc(p_dnum5())
+        with open(path, "w") as fh:
+            json.dump(doc, fh, indent=1)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "client":
         make_client()
         sys.exit(0)
