@@ -124,24 +124,24 @@ TFHE_DEV uint32_t ring_off(int row, int k) {
 
 // iteration state shared by the three roles: every role walks the same unit
 // sequence (limb, chunk) and the same ring / accumulator phases.  Chunks of a
-// limb run column-block-major: c = (x0 / kNC) * batch + b, so the batch
-// members sharing a column block (and its epilogue operands: W2 twiddles in
-// stage 1, switching-key columns in the fused key switch) are consecutive.
+// limb run member-major (c = b * R / kNC + x0 / kNC): a member's columns are
+// contiguous in memory, which measured ~3% faster than grouping the members
+// that share a column block.
 struct UnitIter {
   int limb, c, b, x0;
   int sl;         // slice within the (limb, chunk) group (EPI_KS_ACC)
   int S;          // slices per group
-  int nb;         // batch members
+  int R;          // data columns per member
   int s;          // ring slot
   uint32_t rph;   // ring phase parity of slot s
   int ab;         // accumulator buffer
   uint32_t aph;   // accumulator phase parity
-  TFHE_DEV void init(long long g0, int C, int nb_, int S_) {
+  TFHE_DEV void init(long long g0, int C, int R_, int S_) {
     limb = (int)(g0 / C);
     c = (int)(g0 % C);
-    nb = nb_;
-    b = c % nb;
-    x0 = (c / nb) * kNC;
+    R = R_;
+    b = c * kNC / R;
+    x0 = c * kNC % R;
     sl = 0; S = S_;
     s = 0; rph = 0; ab = 0; aph = 0;
   }
@@ -149,7 +149,7 @@ struct UnitIter {
     if (++sl == S) {
       sl = 0;
       if (++c == C) { c = 0; ++limb; b = 0; x0 = 0; }
-      else if (++b == nb) { b = 0; x0 += kNC; }
+      else if ((x0 += kNC) == R) { x0 = 0; ++b; }
     }
     if (++s == kRing) { s = 0; rph ^= 1; }
     ab ^= 1;
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   UnitIter w;
-  w.init(g0, C, a.batch, a.S);
+  w.init(g0, C, a.R, a.S);
   // Each role's register budget is set at the top of its own branch so that
   // ptxas allocates every role's code under the matching setmaxnreg limit.
   if (warp < 4) {
