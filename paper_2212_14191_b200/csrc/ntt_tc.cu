@@ -269,6 +269,304 @@ int launch_stage_bn(int bn, const StageArgs& a, int npad, int n_limbs, cudaStrea
   return 2;
 }
 
+// ---------------------------------------------------------------------------
+// Persistent twiddle-resident variant (small n: BN * KC <= 128, e.g. the
+// 64 x 64 plan of N = 2^12).  Same math and tile layouts as
+// ntt_stage_kernel, but one CTA per SM walks a contiguous range of
+// (limb, 128-row tile) units: the byte-split twiddle tiles of the current
+// prime (16 * KC tiles, <= 64 KB) are bulk-copied into shared memory once
+// per limb instead of once per tile, data tiles stream through a
+// kResStages-deep ring, and the TMEM accumulators are double-buffered so the
+// epilogue of tile t overlaps the MMAs of tile t+1.
+//   warps 0-3  producers (one data row each: load K values, byte-split);
+//              thread 0 also reloads the twiddles on a limb change
+//   warps 4-7  epilogue (TMEM lane = data row)
+//   warp 8     TMEM owner; one elected lane issues the MMAs
+// ---------------------------------------------------------------------------
+constexpr int kResStages = 3;
+constexpr int kResThreads = 288;
+
+__host__ __device__ constexpr uint32_t res_tmem_cols(int bn) {
+  return 8 * bn <= 32 ? 32 : 8 * bn <= 64 ? 64 : 8 * bn <= 128 ? 128 : 8 * bn <= 256 ? 256 : 512;
+}
+// stage 1 also keeps the prime's Hadamard twiddles W2 (+ Shoup) resident
+template <int STAGE>
+__host__ __device__ constexpr int res_w2_bytes() { return STAGE == 1 ? 2 * 4096 * 4 : 0; }
+template <int STAGE, int BN, int KC>
+__host__ __device__ constexpr int res_smem_bytes() {
+  return KC * 16 * BN * kKC + res_w2_bytes<STAGE>() + kResStages * KC * 4 * kATile +
+         (2 * kResStages + 7) * 8 + 16;
+}
+
+template <int STAGE, int BN, int KC>
+__global__ void __launch_bounds__(kResThreads, 1)
+    ntt_res_kernel(const __grid_constant__ StageArgs a, int tiles_per_limb, long long units) {
+  constexpr int kBTile = BN * kKC;
+  constexpr int kTwBytes = KC * 16 * kBTile;
+  constexpr int kDataBytes = KC * 4 * kATile;
+  constexpr uint32_t kAccCols = 4 * BN;
+  constexpr uint32_t kTmemCols = res_tmem_cols(BN);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sTw = smem;
+  uint32_t* sW2 = reinterpret_cast<uint32_t*>(smem + kTwBytes);   // stage 1: [n] W2 | [n] Shoup
+  uint8_t* sData = smem + kTwBytes + res_w2_bytes<STAGE>();
+  uint64_t* d_full = reinterpret_cast<uint64_t*>(sData + kResStages * kDataBytes);
+  uint64_t* d_empty = d_full + kResStages;
+  uint64_t* acc_full = d_empty + kResStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* tw_full = acc_empty + 2;
+  uint64_t* tw_empty = tw_full + 1;
+  uint64_t* epi_done = tw_empty + 1;   // epilogue finished a limb (W2 may be replaced)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_done + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const long long u0 = units * blockIdx.x / gridDim.x;
+  const int cnt = (int)(units * (blockIdx.x + 1) / gridDim.x - u0);
+  if (tid == 0) {
+    for (int s = 0; s < kResStages; ++s) {
+      mbar_init(&d_full[s], 128);
+      mbar_init(&d_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 128);
+    }
+    mbar_init(tw_full, 1);
+    mbar_init(tw_empty, 1);
+    mbar_init(epi_done, 128);
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // ---------------------------------------------------------------- producers
+    int prev_limb = -1;
+    uint32_t tw_ph = 0;
+    for (int it = 0; it < cnt; ++it) {
+      const long long u = u0 + it;
+      const int limb = (int)(u / tiles_per_limb), tile = (int)(u % tiles_per_limb);
+      if (limb != prev_limb) {
+        if (tid == 0) {
+          if (prev_limb >= 0) {
+            mbar_wait(tw_empty, tw_ph);   // every MMA of the previous limb has completed
+            if (STAGE == 1) mbar_wait(epi_done, tw_ph);   // ... and its epilogue (W2)
+            tw_ph ^= 1;
+          }
+          const int pr = a.map.prime[limb];
+          mbar_arrive_expect_tx(tw_full, kTwBytes + (STAGE == 1 ? 2 * a.n * 4 : 0));
+          bulk_g2s(sTw, a.tw + (size_t)pr * a.tw_stride, kTwBytes, tw_full);
+          if (STAGE == 1) {
+            bulk_g2s(sW2, a.w2 + (size_t)pr * a.n, a.n * 4, tw_full);
+            bulk_g2s(sW2 + a.n, a.w2s + (size_t)pr * a.n, a.n * 4, tw_full);
+          }
+        }
+        prev_limb = limb;
+      }
+      const int s = it % kResStages;
+      const int gr = tile * kRows + tid;
+      const bool valid = gr < a.total_rows;
+      const int b = valid ? gr / a.R : 0;
+      const int x = valid ? gr % a.R : 0;
+      const uint32_t* src =
+          STAGE == 1 ? a.in + ((size_t)a.map.in_row[limb] * a.batch + b) * a.n + x
+                     : a.in + ((size_t)limb * a.batch + b) * a.n + (size_t)x * a.n2;
+      // every load of the tile is issued before any is consumed (one memory
+      // latency per tile instead of one per 4-value group)
+      uint32_t v[KC * 8][4];
+#pragma unroll
+      for (int g = 0; g < KC * 8; ++g) {
+        const int k = g * 4;
+        if (valid && k < a.K) {
+          if (STAGE == 1) {
+            const uint32_t* p = src + (size_t)k * a.n2;
+            v[g][0] = __ldg(p);
+            v[g][1] = __ldg(p + a.n2);
+            v[g][2] = __ldg(p + 2 * a.n2);
+            v[g][3] = __ldg(p + 3 * a.n2);
+          } else {
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(src + k));
+            v[g][0] = q.x; v[g][1] = q.y; v[g][2] = q.z; v[g][3] = q.w;
+          }
+        } else {
+          v[g][0] = v[g][1] = v[g][2] = v[g][3] = 0;
+        }
+      }
+      if (it >= kResStages) mbar_wait(&d_empty[s], ((it / kResStages) & 1) ^ 1);
+      uint8_t* sA = sData + s * kDataBytes;
+#pragma unroll
+      for (int g = 0; g < KC * 8; ++g) {
+        const int kc = g / 8, kq = g % 8;
+        uint32_t w[4];
+        byte_planes(v[g][0], v[g][1], v[g][2], v[g][3], w);
+        const uint32_t off = tile_off(tid, kq * 4, kRows);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<uint32_t*>(sA + (kc * 4 + j) * kATile + off) = w[j];
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&d_full[s]);
+    }
+  } else if (warp < 8) {
+    // ---------------------------------------------------------------- epilogue
+    const int r = tid - 128;
+    const uint32_t lane_base = tmem + ((uint32_t)((warp - 4) * 32) << 16);
+    int prev_limb = -1;
+    uint32_t tw_ph = 0;
+    for (int it = 0; it < cnt; ++it) {
+      const long long u = u0 + it;
+      const int limb = (int)(u / tiles_per_limb), tile = (int)(u % tiles_per_limb);
+      const int ab = it & 1;
+      if (STAGE == 1 && limb != prev_limb) {
+        mbar_wait(tw_full, tw_ph);   // this limb's W2 is resident
+        tw_ph ^= 1;
+        prev_limb = limb;
+      }
+      mbar_wait(&acc_full[ab], (it >> 1) & 1);
+      tc_fence_after();
+      const int gr = tile * kRows + r;
+      const bool valid = gr < a.total_rows;
+      const int b = valid ? gr / a.R : 0;
+      const int x = valid ? gr % a.R : 0;
+      const int prime = a.map.prime[limb];
+      const PrimeConst pc = a.pc[prime];
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t acc[4][16];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tmem_ld16(lane_base + ab * kAccCols + i * BN + c0, acc[i]);
+        tmem_ld_wait();
+        if (c0 + 16 >= BN) {
+          tc_fence_before();
+          mbar_arrive(&acc_empty[ab]);   // buffer drained: the next tile's MMAs may start
+        }
+        if (!valid) continue;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int col = c0 + e;
+          if (col >= a.Ntw) break;
+          const uint64_t v = (uint64_t)acc[0][e] + ((uint64_t)acc[1][e] << 8) +
+                             ((uint64_t)acc[2][e] << 16) + ((uint64_t)acc[3][e] << 24);
+          uint32_t y = reduce64(v, pc.q, pc.mu);
+          if (STAGE == 1) {
+            const int widx = col * a.n2 + x;
+            y = mul_shoup(y, sW2[widx], sW2[a.n + widx], pc.q);
+            a.out[((size_t)limb * a.batch + b) * a.n + (size_t)col * a.n2 + x] = y;
+            continue;
+          }
+          const size_t pos = (size_t)col * a.n1 + x;
+          const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n;
+          if (a.epi.mode == EPI_KS_MAC) {
+            const size_t kr = (size_t)a.epi.key_row[limb] * a.n + pos;
+            const uint32_t tb = mul_mod(y, __ldg(a.epi.kb + kr), pc.q, pc.mu);
+            const uint32_t ta = mul_mod(y, __ldg(a.epi.ka + kr), pc.q, pc.mu);
+            uint32_t* ob = a.epi.acc_b + orow + pos;
+            uint32_t* oa = a.epi.acc_a + orow + pos;
+            *ob = a.epi.first ? tb : add_mod(*ob, tb, pc.q);
+            *oa = a.epi.first ? ta : add_mod(*oa, ta, pc.q);
+            continue;
+          }
+          if (a.epi.mode == EPI_SUB_SCALE) {
+            const uint32_t xv = a.epi.x[((size_t)a.epi.x_row[limb] * a.batch + b) * a.n + pos];
+            y = mul_shoup(sub_mod(xv, y, pc.q), a.epi.s[limb], a.epi.s_shoup[limb], pc.q);
+            const int br = a.epi.base_row[limb];
+            if (br >= 0) y = add_mod(a.epi.base[((size_t)br * a.batch + b) * a.n + pos], y, pc.q);
+          }
+          a.out[orow + pos] = y;
+        }
+      }
+      if (STAGE == 1 && (it + 1 == cnt || (u + 1) / tiles_per_limb != limb))
+        mbar_arrive(epi_done);   // done reading this limb's W2
+    }
+  } else {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = idesc_i8(kRows, BN);
+    const bool leader = elect_one();
+    int prev_limb = -1;
+    uint32_t tw_ph = 0;
+    for (int it = 0; it < cnt; ++it) {
+      const long long u = u0 + it;
+      const int limb = (int)(u / tiles_per_limb);
+      if (limb != prev_limb) {
+        mbar_wait(tw_full, tw_ph);
+        tw_ph ^= 1;
+        prev_limb = limb;
+      }
+      const int s = it % kResStages, ab = it & 1;
+      mbar_wait(&d_full[s], (it / kResStages) & 1);
+      if (it >= 2) mbar_wait(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (leader) {
+        const uint32_t sA = smem_u32(sData + s * kDataBytes);
+        const uint32_t sB = smem_u32(sTw);
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t adesc = smem_desc_kmajor(sA + (kc * 4 + j) * kATile, kRows * 16, 128);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint64_t bdesc =
+                  smem_desc_kmajor(sB + ((kc * 4 + j) * 4 + i) * kBTile, BN * 16, 128);
+              mma_i8_ss(tmem + ab * kAccCols + i * BN, adesc, bdesc, idesc, (kc | j) != 0);
+            }
+          }
+        mma_commit(&d_empty[s]);
+        mma_commit(&acc_full[ab]);
+        const bool last_of_limb = it + 1 == cnt || (u + 1) / tiles_per_limb != limb;
+        if (last_of_limb) mma_commit(tw_empty);
+      }
+      __syncwarp();
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+template <int STAGE, int BN, int KC>
+int launch_res(const Ctx& c, const StageArgs& a, int n_limbs, cudaStream_t st) {
+  constexpr int smem = res_smem_bytes<STAGE, BN, KC>();
+  auto kern = ntt_res_kernel<STAGE, BN, KC>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int tiles = (a.total_rows + kRows - 1) / kRows;
+  const long long units = (long long)tiles * n_limbs;
+  const int grid = (int)std::min<long long>(c.sms, units);
+  kern<<<grid, kResThreads, smem, st>>>(a, tiles, units);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("ntt resident-stage launch: ") + cudaGetErrorString(e));
+    return 3;
+  }
+  return 0;
+}
+
+// stage 1 runs the resident variant when the prime's twiddle tiles fit
+// (BN * KC <= 128, n <= 4096); stage 2 -- whose fused epilogues (ModDown,
+// rescale, key-switch MAC) read global operands per element -- measured
+// faster as v1 (two CTAs per SM hide that latency better)
+template <int STAGE>
+int launch_stage_any(const Ctx& c, int bn, int kc, const StageArgs& a, int npad, int n_limbs,
+                     cudaStream_t st) {
+  if (STAGE == 1 && npad == bn && c.n <= 4096) {
+    switch (bn * 8 + kc) {
+      case 16 * 8 + 1: return launch_res<STAGE, 16, 1>(c, a, n_limbs, st);
+      case 32 * 8 + 1: return launch_res<STAGE, 32, 1>(c, a, n_limbs, st);
+      case 32 * 8 + 2: return launch_res<STAGE, 32, 2>(c, a, n_limbs, st);
+      case 64 * 8 + 1: return launch_res<STAGE, 64, 1>(c, a, n_limbs, st);
+      case 64 * 8 + 2: return launch_res<STAGE, 64, 2>(c, a, n_limbs, st);
+    }
+  }
+  return launch_stage_bn<STAGE>(bn, a, npad, n_limbs, st);
+}
+
 // --------------------------------------------------------------- host tables
 
 uint32_t mulmod_h(uint64_t a, uint64_t b, uint32_t q) { return (uint32_t)(a * b % q); }
@@ -437,7 +735,7 @@ int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& m
   a.KC = c.kpad[0] / kKC;
   a.Ntw = c.n1;
   a.total_rows = batch * c.n2;
-  int rc = launch_stage_bn<1>(c.bn[0], a, c.npad[0], map.n, st);
+  int rc = launch_stage_any<1>(c, c.bn[0], a.KC, a, c.npad[0], map.n, st);
   if (rc) return rc;
   // stage 2: columns of W3 (k2), contraction over i2, rows (b, k1)
   a.in = P;
@@ -449,7 +747,7 @@ int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& m
   a.KC = c.kpad[1] / kKC;
   a.Ntw = c.n2;
   a.total_rows = batch * c.n1;
-  return launch_stage_bn<2>(c.bn[1], a, c.npad[1], map.n, st);
+  return launch_stage_any<2>(c, c.bn[1], a.KC, a, c.npad[1], map.n, st);
 }
 
 }  // namespace tfhe
