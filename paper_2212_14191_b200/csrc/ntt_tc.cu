@@ -280,11 +280,14 @@ int launch_stage_bn(int bn, const StageArgs& a, int npad, int n_limbs, cudaStrea
 // epilogue of tile t overlaps the MMAs of tile t+1.
 //   warps 0-3  producers (one data row each: load K values, byte-split);
 //              thread 0 also reloads the twiddles on a limb change
-//   warps 4-7  epilogue (TMEM lane = data row)
-//   warp 8     TMEM owner; one elected lane issues the MMAs
+//   warps 4-11 epilogue (TMEM lane = data row; two warps per lane quarter,
+//              each half of the columns, to hide the fold / reduce latency)
+//   warp 12    TMEM owner; one elected lane issues the MMAs
 // ---------------------------------------------------------------------------
 constexpr int kResStages = 3;
-constexpr int kResThreads = 288;
+constexpr int kResEpiWarps = 8;                     // two per TMEM lane quarter
+constexpr int kResMmaWarp = 4 + kResEpiWarps;
+constexpr int kResThreads = 32 * (kResMmaWarp + 1);
 
 __host__ __device__ constexpr uint32_t res_tmem_cols(int bn) {
   return 8 * bn <= 32 ? 32 : 8 * bn <= 64 ? 64 : 8 * bn <= 128 ? 128 : 8 * bn <= 256 ? 256 : 512;
@@ -292,10 +295,13 @@ __host__ __device__ constexpr uint32_t res_tmem_cols(int bn) {
 // stage 1 also keeps the prime's Hadamard twiddles W2 (+ Shoup) resident
 template <int STAGE>
 __host__ __device__ constexpr int res_w2_bytes() { return STAGE == 1 ? 2 * 4096 * 4 : 0; }
+// stage 2 stages its (contiguous) P tiles through a 2-deep raw ring by bulk copy
+template <int STAGE, int KC>
+__host__ __device__ constexpr int res_raw_bytes() { return STAGE == 2 ? 2 * kRows * KC * kKC * 4 : 0; }
 template <int STAGE, int BN, int KC>
 __host__ __device__ constexpr int res_smem_bytes() {
-  return KC * 16 * BN * kKC + res_w2_bytes<STAGE>() + kResStages * KC * 4 * kATile +
-         (2 * kResStages + 7) * 8 + 16;
+  return KC * 16 * BN * kKC + res_w2_bytes<STAGE>() + res_raw_bytes<STAGE, KC>() +
+         kResStages * KC * 4 * kATile + (2 * kResStages + 11) * 8 + 16;
 }
 
 template <int STAGE, int BN, int KC>
@@ -309,7 +315,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sTw = smem;
   uint32_t* sW2 = reinterpret_cast<uint32_t*>(smem + kTwBytes);   // stage 1: [n] W2 | [n] Shoup
-  uint8_t* sData = smem + kTwBytes + res_w2_bytes<STAGE>();
+  uint8_t* sRaw = smem + kTwBytes + res_w2_bytes<STAGE>();          // stage 2: [2] P tiles
+  constexpr int kRawTile = kRows * KC * kKC * 4;
+  uint8_t* sData = sRaw + res_raw_bytes<STAGE, KC>();
   uint64_t* d_full = reinterpret_cast<uint64_t*>(sData + kResStages * kDataBytes);
   uint64_t* d_empty = d_full + kResStages;
   uint64_t* acc_full = d_empty + kResStages;
@@ -317,7 +325,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
   uint64_t* tw_full = acc_empty + 2;
   uint64_t* tw_empty = tw_full + 1;
   uint64_t* epi_done = tw_empty + 1;   // epilogue finished a limb (W2 may be replaced)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_done + 1);
+  uint64_t* raw_full = epi_done + 1;
+  uint64_t* raw_empty = raw_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const long long u0 = units * blockIdx.x / gridDim.x;
@@ -329,14 +339,18 @@ __global__ void __launch_bounds__(kResThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], 128);
+      mbar_init(&acc_empty[s], 32 * kResEpiWarps);
     }
     mbar_init(tw_full, 1);
     mbar_init(tw_empty, 1);
-    mbar_init(epi_done, 128);
+    mbar_init(epi_done, 32 * kResEpiWarps);
+    for (int sl = 0; sl < 2; ++sl) {
+      mbar_init(&raw_full[sl], 1);
+      mbar_init(&raw_empty[sl], 128);
+    }
     fence_mbar_init();
   }
-  if (warp == 8) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == kResMmaWarp) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -346,6 +360,18 @@ __global__ void __launch_bounds__(kResThreads, 1)
     // ---------------------------------------------------------------- producers
     int prev_limb = -1;
     uint32_t tw_ph = 0;
+    auto issue_raw = [&](int it, int rs) {   // stage 2: P tile of unit u0 + it
+      const long long u = u0 + it;
+      const int limb = (int)(u / tiles_per_limb), tile = (int)(u % tiles_per_limb);
+      const int rows = min(kRows, a.total_rows - tile * kRows);
+      const uint32_t bytes = (uint32_t)rows * a.K * 4;
+      mbar_arrive_expect_tx(&raw_full[rs], bytes);
+      bulk_g2s(sRaw + rs * kRawTile,
+               a.in + (size_t)limb * a.batch * a.n + (size_t)tile * kRows * a.n2, bytes,
+               &raw_full[rs]);
+    };
+    if (STAGE == 2 && tid == 0)
+      for (int it = 0; it < 2 && it < cnt; ++it) issue_raw(it, it);
     for (int it = 0; it < cnt; ++it) {
       const long long u = u0 + it;
       const int limb = (int)(u / tiles_per_limb), tile = (int)(u % tiles_per_limb);
@@ -369,11 +395,37 @@ __global__ void __launch_bounds__(kResThreads, 1)
       const int s = it % kResStages;
       const int gr = tile * kRows + tid;
       const bool valid = gr < a.total_rows;
+      uint8_t* sA = sData + s * kDataBytes;
+      if (STAGE == 2) {
+        // P rows of a tile are contiguous (row (b, x) at gr * n2 within the limb):
+        // one bulk copy per tile, issued one tile ahead into a 2-slot ring
+        const int rs = it & 1;
+        mbar_wait(&raw_full[rs], (it >> 1) & 1);
+        if (it >= kResStages) mbar_wait(&d_empty[s], ((it / kResStages) & 1) ^ 1);
+        const uint8_t* row = sRaw + rs * kRawTile + (size_t)tid * a.K * 4;
+        const int ng = (a.K + 3) / 4;
+#pragma unroll
+        for (int g0 = 0; g0 < KC * 8; ++g0) {
+          // groups of 4 k in a per-thread rotated order: conflict-free 16-byte reads
+          const int g = g0 < ng ? (g0 + tid) % ng : g0;
+          uint4 q = make_uint4(0, 0, 0, 0);
+          if (valid && g0 < ng) q = *reinterpret_cast<const uint4*>(row + g * 16);
+          uint32_t w[4];
+          byte_planes(q.x, q.y, q.z, q.w, w);
+          const uint32_t off = tile_off(tid, (g % 8) * 4, kRows);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint32_t*>(sA + ((g / 8) * 4 + j) * kATile + off) = w[j];
+        }
+        mbar_arrive(&raw_empty[rs]);
+        if (tid == 0 && it + 2 < cnt) {
+          mbar_wait(&raw_empty[rs], (it >> 1) & 1);
+          issue_raw(it + 2, rs);
+        }
+      } else {
       const int b = valid ? gr / a.R : 0;
       const int x = valid ? gr % a.R : 0;
-      const uint32_t* src =
-          STAGE == 1 ? a.in + ((size_t)a.map.in_row[limb] * a.batch + b) * a.n + x
-                     : a.in + ((size_t)limb * a.batch + b) * a.n + (size_t)x * a.n2;
+      const uint32_t* src = a.in + ((size_t)a.map.in_row[limb] * a.batch + b) * a.n + x;
       // every load of the tile is issued before any is consumed (one memory
       // latency per tile instead of one per 4-value group)
       uint32_t v[KC * 8][4];
@@ -381,22 +433,16 @@ __global__ void __launch_bounds__(kResThreads, 1)
       for (int g = 0; g < KC * 8; ++g) {
         const int k = g * 4;
         if (valid && k < a.K) {
-          if (STAGE == 1) {
-            const uint32_t* p = src + (size_t)k * a.n2;
-            v[g][0] = __ldg(p);
-            v[g][1] = __ldg(p + a.n2);
-            v[g][2] = __ldg(p + 2 * a.n2);
-            v[g][3] = __ldg(p + 3 * a.n2);
-          } else {
-            const uint4 q = __ldg(reinterpret_cast<const uint4*>(src + k));
-            v[g][0] = q.x; v[g][1] = q.y; v[g][2] = q.z; v[g][3] = q.w;
-          }
+          const uint32_t* p = src + (size_t)k * a.n2;
+          v[g][0] = __ldg(p);
+          v[g][1] = __ldg(p + a.n2);
+          v[g][2] = __ldg(p + 2 * a.n2);
+          v[g][3] = __ldg(p + 3 * a.n2);
         } else {
           v[g][0] = v[g][1] = v[g][2] = v[g][3] = 0;
         }
       }
       if (it >= kResStages) mbar_wait(&d_empty[s], ((it / kResStages) & 1) ^ 1);
-      uint8_t* sA = sData + s * kDataBytes;
 #pragma unroll
       for (int g = 0; g < KC * 8; ++g) {
         const int kc = g / 8, kq = g % 8;
@@ -407,13 +453,16 @@ __global__ void __launch_bounds__(kResThreads, 1)
         for (int j = 0; j < 4; ++j)
           *reinterpret_cast<uint32_t*>(sA + (kc * 4 + j) * kATile + off) = w[j];
       }
+      }
       fence_proxy_async_smem();
       mbar_arrive(&d_full[s]);
     }
-  } else if (warp < 8) {
+  } else if (warp < kResMmaWarp) {
     // ---------------------------------------------------------------- epilogue
-    const int r = tid - 128;
-    const uint32_t lane_base = tmem + ((uint32_t)((warp - 4) * 32) << 16);
+    constexpr int kCWr = BN / 2 >= 16 ? 16 : 8;     // columns per TMEM load
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int r = quarter * 32 + (tid & 31);
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     int prev_limb = -1;
     uint32_t tw_ph = 0;
     for (int it = 0; it < cnt; ++it) {
@@ -434,18 +483,21 @@ __global__ void __launch_bounds__(kResThreads, 1)
       const int prime = a.map.prime[limb];
       const PrimeConst pc = a.pc[prime];
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t acc[4][16];
+      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += kCWr) {
+        uint32_t acc[4][kCWr];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) tmem_ld16(lane_base + ab * kAccCols + i * BN + c0, acc[i]);
+        for (int i = 0; i < 4; ++i) {
+          if constexpr (kCWr == 16) tmem_ld16(lane_base + ab * kAccCols + i * BN + c0, acc[i]);
+          else tmem_ld8(lane_base + ab * kAccCols + i * BN + c0, acc[i]);
+        }
         tmem_ld_wait();
-        if (c0 + 16 >= BN) {
+        if (c0 + kCWr >= (half + 1) * (BN / 2)) {
           tc_fence_before();
           mbar_arrive(&acc_empty[ab]);   // buffer drained: the next tile's MMAs may start
         }
         if (!valid) continue;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
+        for (int e = 0; e < kCWr; ++e) {
           const int col = c0 + e;
           if (col >= a.Ntw) break;
           const uint64_t v = (uint64_t)acc[0][e] + ((uint64_t)acc[1][e] << 8) +
@@ -525,7 +577,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kResMmaWarp) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
   }
@@ -548,14 +600,12 @@ int launch_res(const Ctx& c, const StageArgs& a, int n_limbs, cudaStream_t st) {
   return 0;
 }
 
-// stage 1 runs the resident variant when the prime's twiddle tiles fit
-// (BN * KC <= 128, n <= 4096); stage 2 -- whose fused epilogues (ModDown,
-// rescale, key-switch MAC) read global operands per element -- measured
-// faster as v1 (two CTAs per SM hide that latency better)
+// the resident variant runs when the prime's twiddle tiles fit (BN * KC <= 128,
+// n <= 4096), else v1
 template <int STAGE>
 int launch_stage_any(const Ctx& c, int bn, int kc, const StageArgs& a, int npad, int n_limbs,
                      cudaStream_t st) {
-  if (STAGE == 1 && npad == bn && c.n <= 4096) {
+  if (npad == bn && c.n <= 4096) {
     switch (bn * 8 + kc) {
       case 16 * 8 + 1: return launch_res<STAGE, 16, 1>(c, a, n_limbs, st);
       case 32 * 8 + 1: return launch_res<STAGE, 32, 1>(c, a, n_limbs, st);
