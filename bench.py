@@ -117,6 +117,15 @@ def cpu_oracle_rate(primes, members, reps=1):
     return 2 * len(primes) * members * reps / dt, dt, threads
 
 
+def headline_config(L, B, world, plan):
+    """The headline workload (BASELINE configs[1]); both arms report it."""
+    return {"workload": f"batched forward+inverse NTT, N=2^16, {PRESET} chain "
+                        f"({L} RNS limbs), batch {B} per GPU (BASELINE configs[1])",
+            "N": N, "limbs": L, "batch_per_gpu": B, "plan": list(plan),
+            "l2": f"inputs larger than L2 ({L * B * N * 4 / 2**30:.2f} GiB per buffer)",
+            "parallelism": f"batch-sharded x{world}, no collective"}
+
+
 def run_reference(args):
     rank = _env_int("RANK", 0)
     if rank != 0:
@@ -139,8 +148,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / max(args.steps, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"batched NTT/INTT N=2^16, {PRESET} ({len(primes)} limbs)",
-                   "sample_members": members},
+        "config": dict(headline_config(len(primes), args.batch, args.gpus, (256, 256)),
+                       cpu_sample_members=members),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -441,11 +450,7 @@ def run_b200(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"batched forward+inverse NTT, N=2^16, {PRESET} chain "
-                               f"({L} RNS limbs), batch {B} per GPU (BASELINE configs[1])",
-                   "N": N, "limbs": L, "batch_per_gpu": B, "plan": [n1, n2],
-                   "l2": f"inputs larger than L2 ({L * B * N * 4 / 2**30:.2f} GiB per buffer)",
-                   "parallelism": f"batch-sharded x{world}, no collective"},
+        "config": headline_config(L, B, world, (n1, n2)),
         "poly_ntt_kops": value / L,
         "parity_spot_check": parity,
         "roofline": {"bound": "tensor", "achieved": achieved_tops, "peak": peak,
