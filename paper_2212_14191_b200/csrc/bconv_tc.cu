@@ -30,7 +30,9 @@
 //   warp 12    TMEM owner; one elected lane issues the MMAs
 // The kernel is HBM-bound for small alpha (alpha*4 bytes read, T*4 written
 // per coefficient); the tensor cores remove the alpha*T mul-mods per
-// coefficient that bound the CUDA-core form at large alpha.
+// coefficient that bound the CUDA-core form at large alpha.  Tiny
+// conversions (alpha <= 4, alpha * T <= 32) take an element-wise fast path
+// (bconv_small_kernel) instead of mostly-padding MMA tiles.
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -306,6 +308,55 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
   }
 }
 
+// Element-wise fast path for tiny conversions (n_src <= 4, n_src * n_dst <=
+// 32: ModDown with K = 2..4 specials, ModUp slices of alpha = 2..4 onto a
+// few targets), where a 128-row MMA tile would carry mostly padding: each
+// thread converts 4 coefficients (uint4) for every target -- the alpha
+// products of one target (< 4 * 2^62) are summed in 64 bits and reduced once.
+__global__ void __launch_bounds__(256)
+    bconv_small_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                       const PrimeConst* __restrict__ pcs, const __grid_constant__ BconvArgs ba,
+                       int64_t per_row) {
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+    uint32_t a[4][4], y[4][4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      if (s >= ba.n_src) break;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(in + (int64_t)s * per_row + i));
+      a[s][0] = v.x; a[s][1] = v.y; a[s][2] = v.z; a[s][3] = v.w;
+      const uint32_t q = pcs[ba.src_prime[s]].q;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) y[s][e] = mul_shoup(a[s][e], ba.qhat_inv[s], ba.qhat_inv_shoup[s], q);
+    }
+    for (int t = 0; t < ba.n_dst; ++t) {
+      uint32_t r[4];
+      const int cp = ba.copy_from[t];
+      if (cp >= 0) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+          if (s == cp) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) r[e] = a[s][e];
+          }
+      } else {
+        const PrimeConst pt = pcs[ba.dst_prime[t]];
+        uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          if (s >= ba.n_src) break;
+          const uint64_t f = ba.factor[s * kMaxBconvDst + t];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[e] += (uint64_t)y[s][e] * f;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) r[e] = reduce64(acc[e], pt.q, pt.mu);
+      }
+      *reinterpret_cast<uint4*>(out + (int64_t)t * per_row + i) = make_uint4(r[0], r[1], r[2], r[3]);
+    }
+  }
+}
+
 }  // namespace
 
 int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,
@@ -314,6 +365,18 @@ int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArg
   if (ba.n_src < 1 || ba.n_src > 4 * kMaxKC * 2 || ba.n_dst > kMaxBconvDst) {
     set_error("base conversion: 1..16 sources and at most 128 targets");
     return 2;
+  }
+  if (ba.n_src <= 4 && ba.n_src * ba.n_dst <= 32 && (batch * (int64_t)c.n) % 4 == 0) {
+    const int64_t per_row = (int64_t)batch * c.n;
+    const int64_t blocks = std::min<int64_t>((per_row / 4 + 255) / 256, (int64_t)c.sms * 8);
+    bconv_small_kernel<<<(int)std::max<int64_t>(blocks, 1), 256, 0, st>>>(in, out, c.d_pc, ba,
+                                                                        per_row);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      set_error(std::string("bconv_small launch: ") + cudaGetErrorString(e));
+      return 3;
+    }
+    return 0;
   }
   BconvTcArgs a;
   a.in = in;
