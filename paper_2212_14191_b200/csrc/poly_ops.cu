@@ -1,4 +1,5 @@
-// HBM-bound element-wise, automorphism and base-conversion kernels.
+// HBM-bound element-wise and automorphism kernels (base conversion lives in
+// bconv_tc.cu).
 //
 // All operate on level-major buffers (rows, batch, n) of canonical u32
 // residues, one prime per row (reference layout, batch.py:22-47).  Row r of a
@@ -8,7 +9,6 @@
 //   tensor product (hmult's d0, d1, d2)                       ckks.py:265-271
 //   key-switch inner product acc += raised * key              ckks.py:345-351
 //   NTT-domain automorphism gather / coeff-domain signed scatter kernels.py:77-107
-//   fast base conversion                                      rns.py:118-152
 //
 // Each thread moves 16-byte vectors (uint4) with a grid-stride loop; grids
 // are sized as a multiple of the SM count.
@@ -186,7 +186,6 @@ __global__ void automorph_coeff_kernel(const uint32_t* __restrict__ in, uint32_t
   }
 }
 
-// fast base conversion (rns.py:118-152), one output row per blockIdx.y
 int sm_count() {
   static int sms = 0;
   if (!sms) {

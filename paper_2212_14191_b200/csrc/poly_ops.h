@@ -1,4 +1,5 @@
-// Launchers for the HBM-bound polynomial kernels (poly_ops.cu).
+// Launchers for the HBM-bound polynomial kernels (poly_ops.cu) and the base
+// conversion (bconv_tc.cu: int8 tensor cores, element-wise for tiny shapes).
 #pragma once
 #include "tfhe_internal.h"
 
