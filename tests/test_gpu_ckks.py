@@ -103,3 +103,29 @@ def test_ckks_ops_golden_large(case, kind, level, seed):
         h = hashlib.sha256(np.ascontiguousarray(arr, dtype=np.uint32).tobytes()).hexdigest()
         assert arr.reshape(-1)[:8].tolist() == rec[op]["head"], (case, op)
         assert h == rec[op]["sha256"], (case, op)
+
+
+@pytest.mark.parametrize("kind,batch", [("small", 3), ("n16", 2), ("set_c", 1)])
+def test_level0_ops_vs_oracle(kind, batch):
+    """Edge of the chain: level 0 (a single chain limb, one GKS slice) for the
+    batched hmult / key switch / hrotate, against the CPU oracle."""
+    import torch
+    from oracle import oracle as O
+    from paper_2212_14191_b200.ckks import CiphertextBatch
+    ctx = _ctx(kind)
+    p = ctx.params
+    rng = np.random.default_rng(500 + batch)
+    basis = (p.chain.q[0],)
+    c0 = np.stack([synth.rows(rng, basis, (batch, p.n)) for _ in range(2)])
+    c1 = np.stack([synth.rows(rng, basis, (batch, p.n)) for _ in range(2)])
+    key = synth.switching_key(rng, p.chain.q, p.chain.p, p.n, p.dnum)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()  # noqa
+    tk = d(key)
+    got = ctx.hmult_batch(CiphertextBatch(d(c0), 0), CiphertextBatch(d(c1), 0), tk)
+    got = got.data.cpu().numpy().view(np.uint32)
+    hb, ha = O.hmult(c0[0], c0[1], c1[0], c1[1], basis, key, p.chain.q, p.chain.p,
+                     p.alpha, p.dnum)
+    assert np.array_equal(got[0], hb) and np.array_equal(got[1], ha)
+    got = ctx.hrotate_batch(CiphertextBatch(d(c0), 0), 1, tk).data.cpu().numpy().view(np.uint32)
+    rb, ra = O.hrotate(c0[0], c0[1], 1, basis, key, p.chain.q, p.chain.p, p.alpha, p.dnum)
+    assert np.array_equal(got[0], rb) and np.array_equal(got[1], ra)
