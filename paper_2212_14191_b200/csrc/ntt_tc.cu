@@ -293,8 +293,9 @@ __host__ __device__ constexpr uint32_t res_tmem_cols(int bn) {
   return 8 * bn <= 32 ? 32 : 8 * bn <= 64 ? 64 : 8 * bn <= 128 ? 128 : 8 * bn <= 256 ? 256 : 512;
 }
 // stage 1 also keeps the prime's Hadamard twiddles W2 (+ Shoup) resident
+constexpr int kResMaxN = 8192;   // resident stage 1 keeps W2 (+ Shoup) of n <= 8192
 template <int STAGE>
-__host__ __device__ constexpr int res_w2_bytes() { return STAGE == 1 ? 2 * 4096 * 4 : 0; }
+__host__ __device__ constexpr int res_w2_bytes() { return STAGE == 1 ? 2 * kResMaxN * 4 : 0; }
 // stage 2 stages its (contiguous) P tiles through a 2-deep raw ring by bulk copy
 template <int STAGE, int KC>
 __host__ __device__ constexpr int res_raw_bytes() { return STAGE == 2 ? 2 * kRows * KC * kKC * 4 : 0; }
@@ -600,12 +601,12 @@ int launch_res(const Ctx& c, const StageArgs& a, int n_limbs, cudaStream_t st) {
   return 0;
 }
 
-// the resident variant runs when the prime's twiddle tiles fit (BN * KC <= 128,
-// n <= 4096), else v1
+// the resident variant runs when the prime's twiddle tiles fit (BN * KC <= 128;
+// n <= 8192 for stage 1, whose W2 is resident too, n <= 4096 for stage 2), else v1
 template <int STAGE>
 int launch_stage_any(const Ctx& c, int bn, int kc, const StageArgs& a, int npad, int n_limbs,
                      cudaStream_t st) {
-  if (npad == bn && c.n <= 4096) {
+  if (npad == bn && c.n <= (STAGE == 1 ? kResMaxN : 4096)) {
     switch (bn * 8 + kc) {
       case 16 * 8 + 1: return launch_res<STAGE, 16, 1>(c, a, n_limbs, st);
       case 32 * 8 + 1: return launch_res<STAGE, 32, 1>(c, a, n_limbs, st);
