@@ -356,6 +356,37 @@ def run_b200(args):
               "paper_a100": {"ntt_kops": 913, "hmult_kops": 88}}
         del ck, key, cts, xa, fa, ya
 
+    # configs[0] (the reference's CPU-runnable case: N=2^12, one 30-bit prime,
+    # batch 64, fwd+inv) and a degree sweep (2 limbs, 32 Mi coefficients per call)
+    sweep = None
+    if args.sweep:
+        from paper_2212_14191_b200.params import generate_primes
+        sweep = {}
+        q0 = generate_primes(1 << 12, [30])
+        c0ctx = DeviceContext.get(1 << 12, tuple(q0), device=dev)
+        x0 = rand_rows(q0, (64, 1 << 12))
+        f0, y0 = torch.empty_like(x0), torch.empty_like(x0)
+
+        def cfg0():
+            c0ctx.ntt(x0, q0, out=f0)
+            c0ctx.ntt(f0, q0, inverse=True, out=y0)
+        ms0 = timed(cfg0, 20)
+        sweep["config0"] = {"workload": "fwd+inv NTT, N=2^12, one 30-bit prime, batch 64 "
+                                        "(BASELINE configs[0])",
+                            "limb_ntt_kops": 2 * 64 * world / (ms0 / 1e3) / 1e3,
+                            "us_per_step": ms0 * 1e3}
+        for logn in range(12, 17):
+            nn = 1 << logn
+            qs = generate_primes(nn, [29, 29])
+            sctx = DeviceContext.get(nn, tuple(qs), device=dev)
+            bb = (1 << 25) // nn
+            xs = rand_rows(qs, (bb, nn))
+            fs = torch.empty_like(xs)
+            ms_s = timed(lambda: sctx.ntt(xs, qs, out=fs), 5)
+            sweep[f"N=2^{logn}"] = {"limb_ntt_kops": 2 * bb * world / (ms_s / 1e3) / 1e3,
+                                    "batch": bb, "plan": list(sctx.plan)}
+            del xs, fs
+
     # HBM-bound kernels (element-wise, automorphism, tensor product, base
     # conversion) on the configs[1] buffers: achieved GB/s of ALGORITHMIC bytes
     # (each operand read once, each result written once) vs the measured copy
@@ -487,6 +518,8 @@ def run_b200(args):
         line["set_a"] = sa
     if d5:
         line["p_dnum5"] = d5
+    if sweep:
+        line["ntt_sweep"] = sweep
     if hbm:
         hpeak, hsrc = 6546.6, "fallback (B200_PROFILING.md)"
         try:
@@ -522,6 +555,7 @@ def main():
     ap.add_argument("--set-a-batch", type=int, default=4096)
     ap.add_argument("--hbm-kernels", type=int, default=1)
     ap.add_argument("--dnum5-batch", type=int, default=16)
+    ap.add_argument("--sweep", type=int, default=1)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
