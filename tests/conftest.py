@@ -13,8 +13,8 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA (B200, sm_100a) device")
-    # the in-tree sm_100a library and the CPU checker are normally built by
-    # __graft_entry__.build(); build them here if a fresh checkout lacks them
+    # the in-tree sm_100a library is normally built by __graft_entry__.build();
+    # build it here if a fresh checkout lacks it (the CPU checker builds itself)
     from paper_2212_14191_b200 import _lib
     if not os.path.exists(_lib.LIB_PATH):
         _lib.build()
