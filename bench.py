@@ -353,7 +353,10 @@ def run_b200(args):
               "ntt_poly_kops": 2 * Ba * world / (ms_ntt / 1e3) / 1e3,
               "hmult_relin_kops": Ba * world / (ms_hm_only / 1e3) / 1e3,
               "hmult_relin_rescale_kops": Ba * world / (ms_hm / 1e3) / 1e3,
-              "paper_a100": {"ntt_kops": 913, "hmult_kops": 88}}
+              "paper_a100": {"ntt_kops": 913, "hmult_kops": 88},
+              # N=2^12 is HBM-bound: 8 N bytes in+out per limb-NTT
+              # (compulsory; the two-stage kernels move 16 N)
+              "ntt_hbm_gbs_compulsory": 2 * len(qa) * Ba * world * 8 * pa.n / (ms_ntt / 1e3) / 1e9}
         del ck, key, cts, xa, fa, ya
 
     # configs[0] (the reference's CPU-runnable case: N=2^12, one 30-bit prime,
@@ -506,6 +509,18 @@ def run_b200(args):
                          "ops_per_s": hm["hmult_kops"] * 1e3,
                          "hmult_relin_only_per_s": hm["hmult_relin_only_per_s"],
                          "rescale_per_s": hm["rescale_per_s"]}
+        # whole-operator roofline: int8 tensor work of the limb transforms one
+        # HMULT+relin+rescale runs (INTT l+1, ModUp (l+1)(l+1+K) incl. the
+        # skipped own-slice raises, ModDown 2K + 2(l+1), rescale 2 + 2l)
+        l1 = L
+        transforms = l1 + l1 * (l1 + len(params.chain.p)) + 2 * len(params.chain.p) + 2 * l1 \
+            + 2 + 2 * (l1 - 1)
+        hm_tops = hm["hmult_kops"] * 1e3 * transforms * ops_per_limb / 1e12
+        line["hmult"]["roofline"] = {
+            "bound": "tensor", "achieved": hm_tops, "peak": peak, "unit": "TOPS (int8)",
+            "frac": hm_tops / peak,
+            "algorithmic": f"{transforms} limb-transforms x {ops_per_limb / 1e9:.3f} G int8-ops "
+                           "per HMULT+relin+rescale"}
         line["hrotate"] = {"workload": f"HROTATE r=1 (automorphism + keyswitch), N=2^16, {PRESET}"
                                        f", batch {hm['batch_per_gpu']} per GPU (configs[3])",
                            "ops_per_s": hm["hrotate_per_s"],
