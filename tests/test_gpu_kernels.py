@@ -72,3 +72,18 @@ def test_bconv_tensor_core_vs_oracle(n, batch, n_src, n_dst, shared):
     got = out.cpu().numpy().view(np.uint32)
     want = O.fast_basis_conv(x, tuple(src), tuple(dst))
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n,t", [(1 << 16, 5), (1 << 16, 25), (1 << 16, 63), (1 << 16, 5 + (1 << 16)),
+                                 (1 << 12, 5), (1 << 13, 61), (1 << 16, 625), (1 << 16, (1 << 17) - 1)])
+def test_ntt_automorphism_vs_oracle(n, t):
+    """NTT-domain automorphism at full size: small multipliers take the
+    smem-window kernel, others the gather; both equal the oracle's gather."""
+    from paper_2212_14191_b200.device import DeviceContext
+    from paper_2212_14191_b200.params import generate_primes
+    primes = generate_primes(n, [29, 28])
+    ctx = DeviceContext.get(n, tuple(primes))
+    rng = np.random.default_rng(t % 1000 + n)
+    x = O.uniform_rows(rng, primes, (3, n))
+    got = ctx.automorphism(torch.from_numpy(x.view(np.int32)).cuda(), t, True, primes)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), O.apply_automorphism(x, t, tuple(primes), "ntt"))
