@@ -100,10 +100,10 @@ __global__ void tensor_kernel(const uint32_t* __restrict__ b0, const uint32_t* _
     const int64_t o = base + i;
     uint4 xb0 = ld4(b0 + o), xa0 = ld4(a0 + o), xb1 = ld4(b1 + o), xa1 = ld4(a1 + o);
     uint4 r0, r1, r2;
+    // d1's two products (< 2^62 each) are summed before one reduction
 #define TFHE_TP(c)                                                                  \
   r0.c = mul_mod(xb0.c, xb1.c, pc.q, pc.mu);                                        \
-  r1.c = add_mod(mul_mod(xa0.c, xb1.c, pc.q, pc.mu), mul_mod(xa1.c, xb0.c, pc.q, pc.mu), \
-                 pc.q);                                                             \
+  r1.c = reduce64((uint64_t)xa0.c * xb1.c + (uint64_t)xa1.c * xb0.c, pc.q, pc.mu);  \
   r2.c = mul_mod(xa0.c, xa1.c, pc.q, pc.mu);
     TFHE_TP(x) TFHE_TP(y) TFHE_TP(z) TFHE_TP(w)
 #undef TFHE_TP
