@@ -52,27 +52,64 @@ def _env_int(name, default):
 # ----------------------------------------------------------------------------
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled during the timed region: NVML
+    every 5 ms (the handle found by the torch device's PCI bus id), else
+    nvidia-smi every 0.2 s."""
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
         self.index = index
-        self.samples = []
+        self.samples = []          # (sm_mhz, max_mhz, set of reason names)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml as N
+            import torch
+            N.nvmlInit()
+            prop = torch.cuda.get_device_properties(index)
+            bus = f"{prop.pci_domain_id:08x}:{prop.pci_bus_id:02x}:{prop.pci_device_id:02x}.0"
+            try:
+                h = N.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = N.nvmlDeviceGetHandleByIndex(index)
+            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+            self._nvml = (N, h, bits)
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        N, h, bits = self._nvml
+        sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        try:
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        return float(sm), float(mx), {k for k, v in bits.items() if r & v}
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                              "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5)
+        f = [x.strip() for x in out.stdout.strip().split(",")]
+        return (float(f[1]), float(f[2]),
+                {self.REASONS[i] for i in range(4) if len(f) > 5 + i and f[5 + i].lower() == "active"})
 
     def _run(self):
+        period = 0.005 if self._nvml else 0.2
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([s.strip() for s in out.stdout.strip().split(",")])
+                self.samples.append(self._sample_nvml() if self._nvml else self._sample_smi())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(period)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -87,14 +124,11 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 5 + i and s[5 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        return {"sm_mhz": float(np.median([s[0] for s in self.samples])),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(set().union(*[s[2] for s in self.samples])),
+                "samples": len(self.samples),
+                "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------
