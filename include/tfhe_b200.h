@@ -82,7 +82,8 @@ int tfhe_ntt(TfheCtx* ctx, const uint32_t* in, uint32_t* out, const int32_t* lim
  * chunks, H2D copy / transform / D2H copy overlapped on two internal copy
  * streams and the caller's stream; the call is stream-ordered -- host_out
  * is complete once `stream` reaches this point.  Pinned host buffers give
- * full copy/compute overlap (pageable ones work, without overlap). */
+ * full copy/compute overlap; pageable ones are bounced through pinned slots
+ * by a parallel host memcpy, which makes the call host-blocking. */
 size_t tfhe_ntt_host_staging_bytes(const TfheCtx* ctx, int n_limbs, int batch);
 int tfhe_ntt_host(TfheCtx* ctx, const uint32_t* host_in, uint32_t* host_out,
                   const int32_t* limb_prime, int n_limbs, int batch, int inverse, void* staging,

@@ -18,6 +18,9 @@ struct TfheCtx {
   // created on first use
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_start = nullptr, ev_in[3] = {}, ev_done[3] = {}, ev_out[3] = {};
+  // pinned host bounce slots [in 3 | out 3] for pageable host buffers
+  uint8_t* h_bounce = nullptr;
+  size_t h_bounce_chunk = 0;
 };
 
 namespace tfhe {
@@ -467,6 +470,7 @@ int tfhe_ctx_create(int device, int log_n, const uint32_t* primes, const uint32_
 void tfhe_ctx_destroy(TfheCtx* h) {
   if (!h) return;
   Ctx& c = h->c;
+  if (h->h_bounce) cudaFreeHost(h->h_bounce);
   if (h->h2d) {
     cudaStreamDestroy(h->h2d);
     cudaStreamDestroy(h->d2h);
@@ -814,6 +818,27 @@ int host_chunk_rows(const TfheCtx* h, int n_limbs, int batch) {
   const size_t row = (size_t)batch * h->c.n * 4;
   return (int)std::max<size_t>(1, std::min<size_t>((size_t)n_limbs, kHostChunkBytes / row));
 }
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// host memcpy split over the host cores (pageable <-> pinned bounce slots)
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const size_t blk = (size_t)1 << 20;
+  const long long nb = (long long)((bytes + blk - 1) / blk);
+#pragma omp parallel for schedule(static)
+  for (long long b = 0; b < nb; ++b) {
+    const size_t off = (size_t)b * blk;
+    memcpy(static_cast<uint8_t*>(dst) + off, static_cast<const uint8_t*>(src) + off,
+           std::min(blk, bytes - off));
+  }
+}
 }  // namespace
 
 extern "C" {
@@ -858,6 +883,28 @@ int tfhe_ntt_host(TfheCtx* h, const uint32_t* host_in, uint32_t* host_out,
   uint8_t* base = static_cast<uint8_t*>(staging);
   void* ws = base + 2 * kHostSlots * chunk;
   const size_t ws_bytes = staging_bytes - 2 * kHostSlots * chunk;
+  // pageable host buffers go through pinned bounce slots, filled / drained
+  // by a parallel host memcpy (a pageable cudaMemcpyAsync is synchronous and
+  // serialises the copy engines); this makes the call host-blocking
+  const bool stage_in = !is_pinned(host_in), stage_out = !is_pinned(host_out);
+  if ((stage_in || stage_out) && h->h_bounce_chunk < chunk) {
+    if (h->h_bounce) cudaFreeHost(h->h_bounce);
+    h->h_bounce = nullptr;
+    h->h_bounce_chunk = 0;
+    if (cudaHostAlloc(&h->h_bounce, 2 * kHostSlots * chunk, cudaHostAllocDefault) != cudaSuccess) {
+      set_error("tfhe_ntt_host: pinned bounce allocation failed");
+      return TFHE_ECUDA;
+    }
+    h->h_bounce_chunk = chunk;
+  }
+  auto bounce = [&](int slot, int out) {
+    return h->h_bounce + (size_t)(out * kHostSlots + slot) * h->h_bounce_chunk;
+  };
+  auto drain_out = [&](int i) {
+    const int k = i % kHostSlots, r0 = i * rows, nr = std::min(rows, n_limbs - r0);
+    cudaEventSynchronize(h->ev_out[k]);
+    par_memcpy(host_out + r0 * row_elems, bounce(k, 1), nr * row_elems * 4);
+  };
   // staging may still be in use by earlier work on the caller's stream
   cudaEventRecord(h->ev_start, st);
   cudaStreamWaitEvent(h->h2d, h->ev_start, 0);
@@ -868,9 +915,16 @@ int tfhe_ntt_host(TfheCtx* h, const uint32_t* host_in, uint32_t* host_out,
     uint32_t* din = reinterpret_cast<uint32_t*>(base + (2 * k) * chunk);
     uint32_t* dout = reinterpret_cast<uint32_t*>(base + (2 * k + 1) * chunk);
     const size_t bytes = nr * row_elems * 4;
+    const uint32_t* src = host_in + r0 * row_elems;
+    if (stage_in) {
+      // bounce slot k is free once chunk i-3's H2D has completed
+      if (i >= kHostSlots) cudaEventSynchronize(h->ev_in[k]);
+      par_memcpy(bounce(k, 0), src, bytes);
+      src = reinterpret_cast<const uint32_t*>(bounce(k, 0));
+    }
     // H2D into slot k once chunk i-3 has been transformed (din free)
     if (i >= kHostSlots) cudaStreamWaitEvent(h->h2d, h->ev_done[k], 0);
-    cudaMemcpyAsync(din, host_in + r0 * row_elems, bytes, cudaMemcpyHostToDevice, h->h2d);
+    cudaMemcpyAsync(din, src, bytes, cudaMemcpyHostToDevice, h->h2d);
     cudaEventRecord(h->ev_in[k], h->h2d);
     // transform on the caller's stream once the data is in and dout is drained
     cudaStreamWaitEvent(st, h->ev_in[k], 0);
@@ -884,11 +938,19 @@ int tfhe_ntt_host(TfheCtx* h, const uint32_t* host_in, uint32_t* host_out,
     if ((rc = launch_ntt(h->c, din, dout, m, batch, inverse != 0, nullptr, ws, ws_bytes, st)))
       return rc;
     cudaEventRecord(h->ev_done[k], st);
-    // D2H of the result
+    // D2H of the result (into the bounce slot first for a pageable output,
+    // whose previous chunk is copied out before the slot is reused)
     cudaStreamWaitEvent(h->d2h, h->ev_done[k], 0);
-    cudaMemcpyAsync(host_out + r0 * row_elems, dout, bytes, cudaMemcpyDeviceToHost, h->d2h);
+    if (stage_out) {
+      if (i >= kHostSlots) drain_out(i - kHostSlots);
+      cudaMemcpyAsync(bounce(k, 1), dout, bytes, cudaMemcpyDeviceToHost, h->d2h);
+    } else {
+      cudaMemcpyAsync(host_out + r0 * row_elems, dout, bytes, cudaMemcpyDeviceToHost, h->d2h);
+    }
     cudaEventRecord(h->ev_out[k], h->d2h);
   }
+  if (stage_out)
+    for (int i = std::max(0, n_chunks - kHostSlots); i < n_chunks; ++i) drain_out(i);
   // the caller's stream completes after the last copy back
   for (int k = 0; k < std::min(n_chunks, kHostSlots); ++k) cudaStreamWaitEvent(st, h->ev_out[k], 0);
   cudaError_t e = cudaGetLastError();

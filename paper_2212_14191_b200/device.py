@@ -197,6 +197,9 @@ class DeviceContext:
         if xt.ndim != 3:
             raise ParameterError("ntt_host expects (rows, batch, n)")
         L, batch = int(xt.shape[0]), int(xt.shape[1])
+        # the result lands in pinned memory from torch's caching host allocator
+        # (reused across calls; a fresh pageable array would page-fault on
+        # every call); a pageable numpy input is bounced by the library
         out = torch.empty(tuple(xt.shape), dtype=torch.int32, pin_memory=True)
         nbytes = max(int(self.lib.tfhe_ntt_host_staging_bytes(self.handle, L, batch)), 256)
         if self._staging is None or self._staging.numel() < nbytes:

@@ -47,3 +47,16 @@ for i in range(4):
     print(f"ntt_host call {i}: {dt * 1e3:.1f} ms -> {L * B / dt / 1e3:.1f} K limb-NTT/s, "
           f"{2 * nbytes / dt / 1e9:.1f} GB/s moved")
     del out
+# numpy (pageable) host buffers through batched_apply, as a reference user calls it
+import numpy as np  # noqa: E402
+from paper_2212_14191_b200.batch import BatchBuffer, batched_apply  # noqa: E402
+from paper_2212_14191_b200.ntt import TwiddleTable  # noqa: E402
+table = TwiddleTable(n, primes)
+table._ctx = ctx
+xn = xin.numpy().view(np.uint32).copy()
+buf = BatchBuffer(data=xn, basis=primes, domain="coeff")
+for i in range(3):
+    t = time.perf_counter()
+    out = batched_apply(buf, "ntt", table=table)
+    dt = time.perf_counter() - t
+    print(f"numpy batched_apply ntt {i}: {dt * 1e3:.1f} ms -> {L * B / dt / 1e3:.1f} K limb-NTT/s")
