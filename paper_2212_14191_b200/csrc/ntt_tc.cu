@@ -284,7 +284,12 @@ int launch_stage_bn(int bn, const StageArgs& a, int npad, int n_limbs, cudaStrea
 //              each half of the columns, to hide the fold / reduce latency)
 //   warp 12    TMEM owner; one elected lane issues the MMAs
 // ---------------------------------------------------------------------------
-constexpr int kResStages = 3;
+// data (byte-plane) ring depth and, for stage 2, the raw P-tile ring depth:
+// stage 2 trades a data stage for a third raw slot (its 32 KB bulk copies
+// need the deeper prefetch); stage 1 loads straight from global memory
+template <int STAGE>
+__host__ __device__ constexpr int res_stages() { return STAGE == 1 ? 3 : 2; }
+constexpr int kResRaw = 3;
 constexpr int kResEpiWarps = 8;                     // two per TMEM lane quarter
 constexpr int kResMmaWarp = 4 + kResEpiWarps;
 constexpr int kResThreads = 32 * (kResMmaWarp + 1);
@@ -298,11 +303,11 @@ template <int STAGE>
 __host__ __device__ constexpr int res_w2_bytes() { return STAGE == 1 ? 2 * kResMaxN * 4 : 0; }
 // stage 2 stages its (contiguous) P tiles through a 2-deep raw ring by bulk copy
 template <int STAGE, int KC>
-__host__ __device__ constexpr int res_raw_bytes() { return STAGE == 2 ? 2 * kRows * KC * kKC * 4 : 0; }
+__host__ __device__ constexpr int res_raw_bytes() { return STAGE == 2 ? kResRaw * kRows * KC * kKC * 4 : 0; }
 template <int STAGE, int BN, int KC>
 __host__ __device__ constexpr int res_smem_bytes() {
   return KC * 16 * BN * kKC + res_w2_bytes<STAGE>() + res_raw_bytes<STAGE, KC>() +
-         kResStages * KC * 4 * kATile + (2 * kResStages + 11) * 8 + 16;
+         res_stages<STAGE>() * KC * 4 * kATile + (2 * res_stages<STAGE>() + 2 * kResRaw + 7) * 8 + 16;
 }
 
 template <int STAGE, int BN, int KC>
@@ -311,6 +316,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
   constexpr int kBTile = BN * kKC;
   constexpr int kTwBytes = KC * 16 * kBTile;
   constexpr int kDataBytes = KC * 4 * kATile;
+  constexpr int kResStages = res_stages<STAGE>();
   constexpr uint32_t kAccCols = 4 * BN;
   constexpr uint32_t kTmemCols = res_tmem_cols(BN);
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -327,8 +333,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
   uint64_t* tw_empty = tw_full + 1;
   uint64_t* epi_done = tw_empty + 1;   // epilogue finished a limb (W2 may be replaced)
   uint64_t* raw_full = epi_done + 1;
-  uint64_t* raw_empty = raw_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 2);
+  uint64_t* raw_empty = raw_full + kResRaw;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + kResRaw);
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const long long u0 = units * blockIdx.x / gridDim.x;
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
     mbar_init(tw_full, 1);
     mbar_init(tw_empty, 1);
     mbar_init(epi_done, 32 * kResEpiWarps);
-    for (int sl = 0; sl < 2; ++sl) {
+    for (int sl = 0; sl < kResRaw; ++sl) {
       mbar_init(&raw_full[sl], 1);
       mbar_init(&raw_empty[sl], 128);
     }
@@ -372,7 +378,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
                &raw_full[rs]);
     };
     if (STAGE == 2 && tid == 0)
-      for (int it = 0; it < 2 && it < cnt; ++it) issue_raw(it, it);
+      for (int it = 0; it < kResRaw && it < cnt; ++it) issue_raw(it, it);
     for (int it = 0; it < cnt; ++it) {
       const long long u = u0 + it;
       const int limb = (int)(u / tiles_per_limb), tile = (int)(u % tiles_per_limb);
@@ -399,9 +405,10 @@ __global__ void __launch_bounds__(kResThreads, 1)
       uint8_t* sA = sData + s * kDataBytes;
       if (STAGE == 2) {
         // P rows of a tile are contiguous (row (b, x) at gr * n2 within the limb):
-        // one bulk copy per tile, issued one tile ahead into a 2-slot ring
-        const int rs = it & 1;
-        mbar_wait(&raw_full[rs], (it >> 1) & 1);
+        // one bulk copy per tile, issued kResRaw tiles ahead
+        const int rs = it % kResRaw;
+        const uint32_t rph = (uint32_t)((it / kResRaw) & 1);
+        mbar_wait(&raw_full[rs], rph);
         if (it >= kResStages) mbar_wait(&d_empty[s], ((it / kResStages) & 1) ^ 1);
         const uint8_t* row = sRaw + rs * kRawTile + (size_t)tid * a.K * 4;
         const int ng = (a.K + 3) / 4;
@@ -419,9 +426,9 @@ __global__ void __launch_bounds__(kResThreads, 1)
             *reinterpret_cast<uint32_t*>(sA + ((g / 8) * 4 + j) * kATile + off) = w[j];
         }
         mbar_arrive(&raw_empty[rs]);
-        if (tid == 0 && it + 2 < cnt) {
-          mbar_wait(&raw_empty[rs], (it >> 1) & 1);
-          issue_raw(it + 2, rs);
+        if (tid == 0 && it + kResRaw < cnt) {
+          mbar_wait(&raw_empty[rs], rph);
+          issue_raw(it + kResRaw, rs);
         }
       } else {
       const int b = valid ? gr / a.R : 0;
