@@ -64,6 +64,24 @@ struct StageArgs {
   EpiArgs epi;
 };
 
+// fold of the 4 accumulators, v = sum_i 2^(8i) C_i (< 2^49), to the residue.
+// Primes > 2^20 (pc.pad[0] = 1) have twiddles pre-scaled by 2^32, so one
+// Montgomery step (v < q 2^32) replaces the 64-bit Barrett reduction.  With
+// K <= 64 (KC <= 2) every C_i < 4 K 255^2 <= 2^24, so the pairs C_0 + 2^8 C_1
+// and C_2 + 2^8 C_3 fit 32 bits; larger K folds in 64 bits throughout.
+template <int KC>
+TFHE_DEV uint32_t fold4(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const PrimeConst& pc) {
+  const uint64_t v =
+      KC <= 2 ? (uint64_t)(c0 + (c1 << 8)) + ((uint64_t)(c2 + (c3 << 8)) << 16)
+              : (uint64_t)c0 + ((uint64_t)c1 << 8) + ((uint64_t)c2 << 16) + ((uint64_t)c3 << 24);
+  if (pc.pad[0]) {
+    const uint32_t m = (uint32_t)v * pc.qneg_inv;
+    const uint32_t t = (uint32_t)((v + (uint64_t)m * pc.q) >> 32);
+    return t >= pc.q ? t - pc.q : t;
+  }
+  return reduce64(v, pc.q, pc.mu);
+}
+
 __host__ __device__ constexpr int tmem_cols_for(int bn) {
   return 4 * bn <= 32 ? 32 : 4 * bn <= 64 ? 64 : 4 * bn <= 128 ? 128 : 4 * bn <= 256 ? 256 : 512;
 }
@@ -177,9 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) ntt_stage_kernel(const __grid_con
       for (int e = 0; e < 16; ++e) {
         const int col = ct * BN + c0 + e;
         if (col >= a.Ntw) break;
-        uint64_t v = (uint64_t)acc[0][e] + ((uint64_t)acc[1][e] << 8) +
-                     ((uint64_t)acc[2][e] << 16) + ((uint64_t)acc[3][e] << 24);
-        uint32_t y = reduce64(v, pc.q, pc.mu);
+        uint32_t y = fold4<4>(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
         if (STAGE == 1) {
           // P[k1=col][i2=x] = S * W2[k1][i2]
           const size_t widx = (size_t)prime * a.n + (size_t)col * a.n2 + x;
@@ -508,9 +524,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
         for (int e = 0; e < kCWr; ++e) {
           const int col = c0 + e;
           if (col >= a.Ntw) break;
-          const uint64_t v = (uint64_t)acc[0][e] + ((uint64_t)acc[1][e] << 8) +
-                             ((uint64_t)acc[2][e] << 16) + ((uint64_t)acc[3][e] << 24);
-          uint32_t y = reduce64(v, pc.q, pc.mu);
+          uint32_t y = fold4<KC>(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
           if (STAGE == 1) {
             const int widx = col * a.n2 + x;
             y = mul_shoup(y, sW2[widx], sW2[a.n + widx], pc.q);
@@ -669,6 +683,8 @@ int build_ntt_tables(Ctx& c) {
       T.resize((size_t)ntw * K);
       for (int p = 0; p < np; ++p) {
         const uint32_t q = c.primes[p];
+        const bool mont = q > (1u << 20);   // Montgomery fold (fold4) for this prime
+        const uint32_t r32 = powmod_h(2, 32, q);
         uint32_t root = inv ? powmod_h(c.psis[p], q - 2, q) : c.psis[p];
         pw[0] = 1;
         for (uint64_t e = 1; e < two_n; ++e) pw[e] = mulmod_h(pw[e - 1], root, q);
@@ -686,7 +702,8 @@ int build_ntt_tables(Ctx& c) {
           uint32_t inv = 1;  // Newton iteration for q^-1 mod 2^32
           for (int t = 0; t < 5; ++t) inv *= 2u - q * inv;
           k.qneg_inv = 0u - inv;
-          k.pad[0] = k.pad[1] = 0;
+          k.pad[0] = mont ? 1u : 0u;   // fold4: twiddles carry 2^32
+          k.pad[1] = 0;
         }
         // T[c][k]: value multiplying data index k for output column c
         for (int cc = 0; cc < ntw; ++cc)
@@ -707,7 +724,8 @@ int build_ntt_tables(Ctx& c) {
             const int kc = k / kKC, kr = k % kKC;
             uint32_t t = T[(size_t)cc * K + k];
             for (int j = 0; j < 4; ++j) {
-              uint32_t vj = mulmod_h(t, 1ull << (8 * j), q);
+              // V_j = 2^(8j) T (x 2^32 for the Montgomery fold) mod q
+              uint32_t vj = mulmod_h(mont ? mulmod_h(t, r32, q) : t, 1ull << (8 * j), q);
               for (int i = 0; i < 4; ++i) {
                 size_t tile = ((size_t)(ct * KC + kc) * 4 + j) * 4 + i;
                 size_t off = tile * (BN * kKC) + (kr >> 4) * (BN * 16) + (cr >> 3) * 128 +

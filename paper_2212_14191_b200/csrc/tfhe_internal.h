@@ -20,7 +20,7 @@ struct PrimeConst {
   uint32_t r[3];        // 2^32, 2^40, 2^48 mod q (byte weights 4..6 of the TS kernel)
   uint32_t w3;          // 2^24 mod q
   uint32_t qneg_inv;    // -q^-1 mod 2^32 (Montgomery, R = 2^32)
-  uint32_t pad[2];
+  uint32_t pad[2];      // pad[0] = 1: small-n (ntt_tc.cu) twiddles carry 2^32 (fold4)
 };
 
 // Per-launch limb map: output row l uses prime `prime[l]`, reads input row
