@@ -300,12 +300,12 @@ int launch_stage_bn(int bn, const StageArgs& a, int npad, int n_limbs, cudaStrea
 //              each half of the columns, to hide the fold / reduce latency)
 //   warp 12    TMEM owner; one elected lane issues the MMAs
 // ---------------------------------------------------------------------------
-// data (byte-plane) ring depth and, for stage 2, the raw P-tile ring depth:
-// stage 2 trades a data stage for a third raw slot (its 32 KB bulk copies
-// need the deeper prefetch); stage 1 loads straight from global memory
+// data (byte-plane) ring depth; stage 2 also stages its contiguous P tiles
+// through a kResRaw-deep raw ring by bulk copy (stage 1 loads straight from
+// global memory)
 template <int STAGE>
 __host__ __device__ constexpr int res_stages() { return STAGE == 1 ? 3 : 2; }
-constexpr int kResRaw = 3;
+constexpr int kResRaw = 2;
 constexpr int kResEpiWarps = 8;                     // two per TMEM lane quarter
 constexpr int kResMmaWarp = 4 + kResEpiWarps;
 constexpr int kResThreads = 32 * (kResMmaWarp + 1);
@@ -313,10 +313,12 @@ constexpr int kResThreads = 32 * (kResMmaWarp + 1);
 __host__ __device__ constexpr uint32_t res_tmem_cols(int bn) {
   return 8 * bn <= 32 ? 32 : 8 * bn <= 64 ? 64 : 8 * bn <= 128 ? 128 : 8 * bn <= 256 ? 256 : 512;
 }
-// stage 1 also keeps the prime's Hadamard twiddles W2 (+ Shoup) resident
-constexpr int kResMaxN = 8192;   // resident stage 1 keeps W2 (+ Shoup) of n <= 8192
+// per-limb resident operand: stage 1 keeps the prime's Hadamard twiddles W2
+// (+ Shoup, n <= 8192); stage 2 with the key-switch MAC epilogue keeps the
+// target's two switching-key rows (shared by every batch member, n <= 4096)
+constexpr int kResMaxN = 8192;
 template <int STAGE>
-__host__ __device__ constexpr int res_w2_bytes() { return STAGE == 1 ? 2 * kResMaxN * 4 : 0; }
+__host__ __device__ constexpr int res_w2_bytes() { return STAGE == 1 ? 2 * kResMaxN * 4 : 2 * 4096 * 4; }
 // stage 2 stages its (contiguous) P tiles through a 2-deep raw ring by bulk copy
 template <int STAGE, int KC>
 __host__ __device__ constexpr int res_raw_bytes() { return STAGE == 2 ? kResRaw * kRows * KC * kKC * 4 : 0; }
@@ -353,6 +355,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + kResRaw);
 
   const int tid = threadIdx.x, warp = tid >> 5;
+  // a per-limb operand (W2, or the key rows of the MAC epilogue) is resident
+  const bool limb_operand = STAGE == 1 || a.epi.mode == EPI_KS_MAC;
   const long long u0 = units * blockIdx.x / gridDim.x;
   const int cnt = (int)(units * (blockIdx.x + 1) / gridDim.x - u0);
   if (tid == 0) {
@@ -402,15 +406,19 @@ __global__ void __launch_bounds__(kResThreads, 1)
         if (tid == 0) {
           if (prev_limb >= 0) {
             mbar_wait(tw_empty, tw_ph);   // every MMA of the previous limb has completed
-            if (STAGE == 1) mbar_wait(epi_done, tw_ph);   // ... and its epilogue (W2)
+            if (limb_operand) mbar_wait(epi_done, tw_ph);   // ... and its epilogue
             tw_ph ^= 1;
           }
           const int pr = a.map.prime[limb];
-          mbar_arrive_expect_tx(tw_full, kTwBytes + (STAGE == 1 ? 2 * a.n * 4 : 0));
+          mbar_arrive_expect_tx(tw_full, kTwBytes + (limb_operand ? 2 * a.n * 4 : 0));
           bulk_g2s(sTw, a.tw + (size_t)pr * a.tw_stride, kTwBytes, tw_full);
           if (STAGE == 1) {
             bulk_g2s(sW2, a.w2 + (size_t)pr * a.n, a.n * 4, tw_full);
             bulk_g2s(sW2 + a.n, a.w2s + (size_t)pr * a.n, a.n * 4, tw_full);
+          } else if (limb_operand) {
+            const size_t kr = (size_t)a.epi.key_row[limb] * a.n;
+            bulk_g2s(sW2, a.epi.kb + kr, a.n * 4, tw_full);
+            bulk_g2s(sW2 + a.n, a.epi.ka + kr, a.n * 4, tw_full);
           }
         }
         prev_limb = limb;
@@ -493,8 +501,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
       const long long u = u0 + it;
       const int limb = (int)(u / tiles_per_limb), tile = (int)(u % tiles_per_limb);
       const int ab = it & 1;
-      if (STAGE == 1 && limb != prev_limb) {
-        mbar_wait(tw_full, tw_ph);   // this limb's W2 is resident
+      if (limb_operand && limb != prev_limb) {
+        mbar_wait(tw_full, tw_ph);   // this limb's W2 / key rows are resident
         tw_ph ^= 1;
         prev_limb = limb;
       }
@@ -534,9 +542,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
           const size_t pos = (size_t)col * a.n1 + x;
           const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n;
           if (a.epi.mode == EPI_KS_MAC) {
-            const size_t kr = (size_t)a.epi.key_row[limb] * a.n + pos;
-            const uint32_t tb = mul_mod(y, __ldg(a.epi.kb + kr), pc.q, pc.mu);
-            const uint32_t ta = mul_mod(y, __ldg(a.epi.ka + kr), pc.q, pc.mu);
+            const uint32_t tb = mul_mod(y, sW2[pos], pc.q, pc.mu);
+            const uint32_t ta = mul_mod(y, sW2[a.n + pos], pc.q, pc.mu);
             uint32_t* ob = a.epi.acc_b + orow + pos;
             uint32_t* oa = a.epi.acc_a + orow + pos;
             *ob = a.epi.first ? tb : add_mod(*ob, tb, pc.q);
@@ -552,8 +559,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
           a.out[orow + pos] = y;
         }
       }
-      if (STAGE == 1 && (it + 1 == cnt || (u + 1) / tiles_per_limb != limb))
-        mbar_arrive(epi_done);   // done reading this limb's W2
+      if (limb_operand && (it + 1 == cnt || (u + 1) / tiles_per_limb != limb))
+        mbar_arrive(epi_done);   // done reading this limb's W2 / key rows
     }
   } else {
     // ---------------------------------------------------------------- MMA issuer
