@@ -88,3 +88,25 @@ def test_hmult_additive_in_d0(setup):
     da = ctx.eltwise(2, delta, c1[1].contiguous(), primes)   # d1 = a0 b1 + b0 a1 by delta a1
     assert torch.equal(shifted[0], _add(base[0], db, q))
     assert torch.equal(shifted[1], _add(base[1], da, q))
+
+
+def test_small_n_full_shape_roundtrip_and_samples():
+    """The Set_A-shaped resident small-n kernels at a large batch (N=2^12,
+    2 limbs, B=8192, 8192 tiles per limb over all SMs): roundtrip exact and
+    sampled rows equal the oracle."""
+    from oracle import oracle as O
+    from paper_2212_14191_b200.device import DeviceContext
+    from paper_2212_14191_b200.params import generate_primes
+    n, B = 1 << 12, 8192
+    primes = generate_primes(n, [29, 29])
+    ctx = DeviceContext.get(n, tuple(primes))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    q = torch.tensor(primes, dtype=torch.int64, device="cuda").view(2, 1, 1)
+    x = (torch.randint(0, 1 << 62, (2, B, n), generator=g, device="cuda") % q).to(torch.int32)
+    f = ctx.ntt(x, primes)
+    assert torch.equal(ctx.ntt(f, primes, inverse=True), x)
+    for limb, member in ((0, 0), (1, 4097), (0, B - 1), (1, 1234)):
+        xs = x[limb, member].cpu().numpy().view(np.uint32)[None]
+        assert np.array_equal(f[limb, member].cpu().numpy().view(np.uint32),
+                              O.ntt(xs, [primes[limb]])[0]), (limb, member)
