@@ -82,6 +82,57 @@ TFHE_DEV uint32_t fold4(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, cons
   return reduce64(v, pc.q, pc.mu);
 }
 
+// Stage-2 epilogue operands of W consecutive output columns col0.. of row
+// (b, x): the accumulator (EPI_KS_MAC, not first) or x and base (EPI_SUB_SCALE).
+// Every load is issued before any of the row's stores: written inline, each
+// column's load would wait on the previous column's store (the pointers may
+// alias), one full memory latency per output.
+template <int W>
+TFHE_DEV void epi2_load(const StageArgs& a, int limb, int b, int x, int col0, bool valid,
+                        uint32_t (&p0)[W], uint32_t (&p1)[W]) {
+  if (!valid || a.epi.mode == EPI_STORE || (a.epi.mode == EPI_KS_MAC && a.epi.first)) return;
+  const uint32_t* s0;
+  const uint32_t* s1 = nullptr;
+  if (a.epi.mode == EPI_KS_MAC) {
+    const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n;
+    s0 = a.epi.acc_b + orow;
+    s1 = a.epi.acc_a + orow;
+  } else {
+    s0 = a.epi.x + ((size_t)a.epi.x_row[limb] * a.batch + b) * a.n;
+    const int br = a.epi.base_row[limb];
+    if (br >= 0) s1 = a.epi.base + ((size_t)br * a.batch + b) * a.n;
+  }
+#pragma unroll
+  for (int e = 0; e < W; ++e) {
+    const size_t pos = (size_t)(col0 + e) * a.n1 + x;
+    if (col0 + e < a.Ntw) {
+      p0[e] = s0[pos];
+      if (s1) p1[e] = s1[pos];
+    }
+  }
+}
+
+// stage-2 epilogue of one output y at column col of row (b, x), operands from
+// epi2_load; kb / ka are the key rows of EPI_KS_MAC (indexed by position)
+TFHE_DEV void epi2_store(const StageArgs& a, int limb, int b, int x, int col, uint32_t y,
+                         uint32_t p0, uint32_t p1, const uint32_t* kb, const uint32_t* ka,
+                         const PrimeConst& pc) {
+  const size_t pos = (size_t)col * a.n1 + x;   // out[n1*k2 + k1], k2 = col, k1 = x
+  const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n;
+  if (a.epi.mode == EPI_KS_MAC) {
+    const uint32_t tb = mul_mod(y, kb[pos], pc.q, pc.mu);
+    const uint32_t ta = mul_mod(y, ka[pos], pc.q, pc.mu);
+    a.epi.acc_b[orow + pos] = a.epi.first ? tb : add_mod(p0, tb, pc.q);
+    a.epi.acc_a[orow + pos] = a.epi.first ? ta : add_mod(p1, ta, pc.q);
+    return;
+  }
+  if (a.epi.mode == EPI_SUB_SCALE) {
+    y = mul_shoup(sub_mod(p0, y, pc.q), a.epi.s[limb], a.epi.s_shoup[limb], pc.q);
+    if (a.epi.base_row[limb] >= 0) y = add_mod(p1, y, pc.q);
+  }
+  a.out[orow + pos] = y;
+}
+
 __host__ __device__ constexpr int tmem_cols_for(int bn) {
   return 4 * bn <= 32 ? 32 : 4 * bn <= 64 ? 64 : 4 * bn <= 128 ? 128 : 4 * bn <= 256 ? 256 : 512;
 }
@@ -187,8 +238,10 @@ __global__ void __launch_bounds__(kThreads, 1) ntt_stage_kernel(const __grid_con
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
       uint32_t acc[4][16];
+      uint32_t p0[16], p1[16];
 #pragma unroll
       for (int i = 0; i < 4; ++i) tmem_ld16(lane_base + i * BN + c0, acc[i]);
+      if (STAGE == 2) epi2_load<16>(a, limb, b, x, ct * BN + c0, valid, p0, p1);
       tmem_ld_wait();
       if (!valid) continue;
 #pragma unroll
@@ -202,27 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1) ntt_stage_kernel(const __grid_con
           y = mul_shoup(y, __ldg(a.w2 + widx), __ldg(a.w2s + widx), pc.q);
           a.out[((size_t)limb * a.batch + b) * a.n + (size_t)col * a.n2 + x] = y;
         } else {
-          // out[n1*k2 + k1], k2 = col, k1 = x
-          const size_t pos = (size_t)col * a.n1 + x;
-          const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n;
-          if (a.epi.mode == EPI_KS_MAC) {
-            const size_t kr = (size_t)a.epi.key_row[limb] * a.n + pos;
-            const uint32_t tb = mul_mod(y, __ldg(a.epi.kb + kr), pc.q, pc.mu);
-            const uint32_t ta = mul_mod(y, __ldg(a.epi.ka + kr), pc.q, pc.mu);
-            uint32_t* ob = a.epi.acc_b + orow + pos;
-            uint32_t* oa = a.epi.acc_a + orow + pos;
-            *ob = a.epi.first ? tb : add_mod(*ob, tb, pc.q);
-            *oa = a.epi.first ? ta : add_mod(*oa, ta, pc.q);
-            continue;
-          }
-          if (a.epi.mode == EPI_SUB_SCALE) {
-            const uint32_t xv = a.epi.x[((size_t)a.epi.x_row[limb] * a.batch + b) * a.n + pos];
-            y = mul_shoup(sub_mod(xv, y, pc.q), a.epi.s[limb], a.epi.s_shoup[limb], pc.q);
-            const int br = a.epi.base_row[limb];
-            if (br >= 0)
-              y = add_mod(a.epi.base[((size_t)br * a.batch + b) * a.n + pos], y, pc.q);
-          }
-          a.out[orow + pos] = y;
+          const size_t kr = a.epi.mode == EPI_KS_MAC ? (size_t)a.epi.key_row[limb] * a.n : 0;
+          epi2_store(a, limb, b, x, col, y, p0[e], p1[e], a.epi.kb + kr, a.epi.ka + kr, pc);
         }
       }
     }
@@ -491,7 +525,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
     }
   } else if (warp < kResMmaWarp) {
     // ---------------------------------------------------------------- epilogue
-    constexpr int kCWr = BN / 2 >= 16 ? 16 : 8;     // columns per TMEM load
+    // columns per TMEM load (stage 2 holds the prefetched operands beside them)
+    constexpr int kCWr = BN / 2 >= 16 && STAGE == 1 ? 16 : 8;
     const int quarter = warp & 3, half = (warp - 4) >> 2;
     const int r = quarter * 32 + (tid & 31);
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
@@ -517,11 +552,13 @@ __global__ void __launch_bounds__(kResThreads, 1)
 #pragma unroll 1
       for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += kCWr) {
         uint32_t acc[4][kCWr];
+        uint32_t p0[kCWr], p1[kCWr];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           if constexpr (kCWr == 16) tmem_ld16(lane_base + ab * kAccCols + i * BN + c0, acc[i]);
           else tmem_ld8(lane_base + ab * kAccCols + i * BN + c0, acc[i]);
         }
+        if (STAGE == 2) epi2_load<kCWr>(a, limb, b, x, c0, valid, p0, p1);
         tmem_ld_wait();
         if (c0 + kCWr >= (half + 1) * (BN / 2)) {
           tc_fence_before();
@@ -539,24 +576,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
             a.out[((size_t)limb * a.batch + b) * a.n + (size_t)col * a.n2 + x] = y;
             continue;
           }
-          const size_t pos = (size_t)col * a.n1 + x;
-          const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n;
-          if (a.epi.mode == EPI_KS_MAC) {
-            const uint32_t tb = mul_mod(y, sW2[pos], pc.q, pc.mu);
-            const uint32_t ta = mul_mod(y, sW2[a.n + pos], pc.q, pc.mu);
-            uint32_t* ob = a.epi.acc_b + orow + pos;
-            uint32_t* oa = a.epi.acc_a + orow + pos;
-            *ob = a.epi.first ? tb : add_mod(*ob, tb, pc.q);
-            *oa = a.epi.first ? ta : add_mod(*oa, ta, pc.q);
-            continue;
-          }
-          if (a.epi.mode == EPI_SUB_SCALE) {
-            const uint32_t xv = a.epi.x[((size_t)a.epi.x_row[limb] * a.batch + b) * a.n + pos];
-            y = mul_shoup(sub_mod(xv, y, pc.q), a.epi.s[limb], a.epi.s_shoup[limb], pc.q);
-            const int br = a.epi.base_row[limb];
-            if (br >= 0) y = add_mod(a.epi.base[((size_t)br * a.batch + b) * a.n + pos], y, pc.q);
-          }
-          a.out[orow + pos] = y;
+          epi2_store(a, limb, b, x, col, y, p0[e], p1[e], sW2, sW2 + a.n, pc);
         }
       }
       if (limb_operand && (it + 1 == cnt || (u + 1) / tiles_per_limb != limb))
