@@ -87,7 +87,7 @@ TFHE_DEV uint32_t fold4(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, cons
 // Every load is issued before any of the row's stores: written inline, each
 // column's load would wait on the previous column's store (the pointers may
 // alias), one full memory latency per output.
-template <int W>
+template <int W, bool kGuard = true>
 TFHE_DEV void epi2_load(const StageArgs& a, int limb, int b, int x, int col0, bool valid,
                         uint32_t (&p0)[W], uint32_t (&p1)[W]) {
   if (!valid || a.epi.mode == EPI_STORE || (a.epi.mode == EPI_KS_MAC && a.epi.first)) return;
@@ -105,7 +105,7 @@ TFHE_DEV void epi2_load(const StageArgs& a, int limb, int b, int x, int col0, bo
 #pragma unroll
   for (int e = 0; e < W; ++e) {
     const size_t pos = (size_t)(col0 + e) * a.n1 + x;
-    if (col0 + e < a.Ntw) {
+    if (!kGuard || col0 + e < a.Ntw) {
       p0[e] = s0[pos];
       if (s1) p1[e] = s1[pos];
     }
@@ -558,26 +558,65 @@ __global__ void __launch_bounds__(kResThreads, 1)
           if constexpr (kCWr == 16) tmem_ld16(lane_base + ab * kAccCols + i * BN + c0, acc[i]);
           else tmem_ld8(lane_base + ab * kAccCols + i * BN + c0, acc[i]);
         }
-        if (STAGE == 2) epi2_load<kCWr>(a, limb, b, x, c0, valid, p0, p1);
+        if (STAGE == 2) epi2_load<kCWr, false>(a, limb, b, x, c0, valid, p0, p1);
         tmem_ld_wait();
         if (c0 + kCWr >= (half + 1) * (BN / 2)) {
           tc_fence_before();
           mbar_arrive(&acc_empty[ab]);   // buffer drained: the next tile's MMAs may start
         }
         if (!valid) continue;
+        // Ntw == BN on this path: no per-column guard, and every per-unit mode
+        // branch sits outside the column loops so the kCWr folds interleave
+        uint32_t y[kCWr];
 #pragma unroll
-        for (int e = 0; e < kCWr; ++e) {
-          const int col = c0 + e;
-          if (col >= a.Ntw) break;
-          uint32_t y = fold4<KC>(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
-          if (STAGE == 1) {
-            const int widx = col * a.n2 + x;
-            y = mul_shoup(y, sW2[widx], sW2[a.n + widx], pc.q);
-            a.out[((size_t)limb * a.batch + b) * a.n + (size_t)col * a.n2 + x] = y;
-            continue;
-          }
-          epi2_store(a, limb, b, x, col, y, p0[e], p1[e], sW2, sW2 + a.n, pc);
+        for (int e = 0; e < kCWr; ++e) y[e] = fold4<KC>(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
+        if (STAGE == 1) {
+          // P[k1 = col][i2 = x] = S * W2[k1][i2]
+          const int n2 = a.n2;
+          uint32_t* o = a.out + ((size_t)limb * a.batch + b) * a.n + (size_t)c0 * n2 + x;
+          const uint32_t* w = sW2 + c0 * n2 + x;
+#pragma unroll
+          for (int e = 0; e < kCWr; ++e)
+            o[e * n2] = mul_shoup(y[e], w[e * n2], w[a.n + e * n2], pc.q);
+          continue;
         }
+        // out[n1*k2 + k1], k2 = col, k1 = x
+        const int n1 = a.n1;
+        const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n + (size_t)c0 * n1 + x;
+        if (a.epi.mode == EPI_KS_MAC) {
+          const uint32_t* kb = sW2 + c0 * n1 + x;
+          uint32_t* ob = a.epi.acc_b + orow;
+          uint32_t* oa = a.epi.acc_a + orow;
+          uint32_t tb[kCWr], ta[kCWr];
+#pragma unroll
+          for (int e = 0; e < kCWr; ++e) {
+            tb[e] = mul_mod(y[e], kb[e * n1], pc.q, pc.mu);
+            ta[e] = mul_mod(y[e], kb[a.n + e * n1], pc.q, pc.mu);
+          }
+          if (a.epi.first) {
+#pragma unroll
+            for (int e = 0; e < kCWr; ++e) { ob[e * n1] = tb[e]; oa[e * n1] = ta[e]; }
+          } else {
+#pragma unroll
+            for (int e = 0; e < kCWr; ++e) {
+              ob[e * n1] = add_mod(p0[e], tb[e], pc.q);
+              oa[e * n1] = add_mod(p1[e], ta[e], pc.q);
+            }
+          }
+          continue;
+        }
+        uint32_t* o = a.out + orow;
+        if (a.epi.mode == EPI_SUB_SCALE) {
+          const uint32_t s = a.epi.s[limb], ss = a.epi.s_shoup[limb];
+#pragma unroll
+          for (int e = 0; e < kCWr; ++e) y[e] = mul_shoup(sub_mod(p0[e], y[e], pc.q), s, ss, pc.q);
+          if (a.epi.base_row[limb] >= 0) {
+#pragma unroll
+            for (int e = 0; e < kCWr; ++e) y[e] = add_mod(p1[e], y[e], pc.q);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < kCWr; ++e) o[e * n1] = y[e];
       }
       if (limb_operand && (it + 1 == cnt || (u + 1) / tiles_per_limb != limb))
         mbar_arrive(epi_done);   // done reading this limb's W2 / key rows
@@ -650,11 +689,12 @@ int launch_res(const Ctx& c, const StageArgs& a, int n_limbs, cudaStream_t st) {
 }
 
 // the resident variant runs when the prime's twiddle tiles fit (BN * KC <= 128;
-// n <= 8192 for stage 1, whose W2 is resident too, n <= 4096 for stage 2), else v1
+// n <= 8192 for stage 1, whose W2 is resident too, n <= 4096 for stage 2) and
+// the tile is exactly the twiddle width (its epilogue has no column guard), else v1
 template <int STAGE>
 int launch_stage_any(const Ctx& c, int bn, int kc, const StageArgs& a, int npad, int n_limbs,
                      cudaStream_t st) {
-  if (npad == bn && c.n <= (STAGE == 1 ? kResMaxN : 4096)) {
+  if (a.Ntw == bn && npad == bn && c.n <= (STAGE == 1 ? kResMaxN : 4096)) {
     switch (bn * 8 + kc) {
       case 16 * 8 + 1: return launch_res<STAGE, 16, 1>(c, a, n_limbs, st);
       case 32 * 8 + 1: return launch_res<STAGE, 32, 1>(c, a, n_limbs, st);
