@@ -244,19 +244,24 @@ __global__ void __launch_bounds__(kThreads, 1) ntt_stage_kernel(const __grid_con
       if (STAGE == 2) epi2_load<16>(a, limb, b, x, ct * BN + c0, valid, p0, p1);
       tmem_ld_wait();
       if (!valid) continue;
+      // fold every column first (branch-free, so the 16 folds interleave);
+      // columns past Ntw only occur for n1 or n2 < 16 and are dropped at the store
+      uint32_t y[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) y[e] = fold4<4>(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const int col = ct * BN + c0 + e;
-        if (col >= a.Ntw) break;
-        uint32_t y = fold4<4>(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
-        if (STAGE == 1) {
-          // P[k1=col][i2=x] = S * W2[k1][i2]
-          const size_t widx = (size_t)prime * a.n + (size_t)col * a.n2 + x;
-          y = mul_shoup(y, __ldg(a.w2 + widx), __ldg(a.w2s + widx), pc.q);
-          a.out[((size_t)limb * a.batch + b) * a.n + (size_t)col * a.n2 + x] = y;
-        } else {
-          const size_t kr = a.epi.mode == EPI_KS_MAC ? (size_t)a.epi.key_row[limb] * a.n : 0;
-          epi2_store(a, limb, b, x, col, y, p0[e], p1[e], a.epi.kb + kr, a.epi.ka + kr, pc);
+        if (col < a.Ntw) {
+          if (STAGE == 1) {
+            // P[k1=col][i2=x] = S * W2[k1][i2]
+            const size_t widx = (size_t)prime * a.n + (size_t)col * a.n2 + x;
+            a.out[((size_t)limb * a.batch + b) * a.n + (size_t)col * a.n2 + x] =
+                mul_shoup(y[e], __ldg(a.w2 + widx), __ldg(a.w2s + widx), pc.q);
+          } else {
+            const size_t kr = a.epi.mode == EPI_KS_MAC ? (size_t)a.epi.key_row[limb] * a.n : 0;
+            epi2_store(a, limb, b, x, col, y[e], p0[e], p1[e], a.epi.kb + kr, a.epi.ka + kr, pc);
+          }
         }
       }
     }
@@ -734,7 +739,9 @@ int build_ntt_tables(Ctx& c) {
   // geometry per stage: stage 0 contracts over n1 (twiddle cols n1), stage 1 over n2
   for (int s = 0; s < 2; ++s) {
     const int ntw = s == 0 ? n1 : n2;
-    c.bn[s] = ntw >= 128 ? 128 : ntw >= 64 ? 64 : ntw >= 32 ? 32 : 16;
+    // tiles of at most 64 twiddle columns: two v1 CTAs (96 KB smem each) share an
+    // SM, so one CTA's epilogue overlaps the other's loads
+    c.bn[s] = ntw >= 64 ? 64 : ntw >= 32 ? 32 : 16;
     c.npad[s] = round_up(ntw, c.bn[s]);
     c.kpad[s] = round_up(ntw, kKC);
     c.tw_stride[s] = (size_t)c.npad[s] * c.kpad[s] * 16;
