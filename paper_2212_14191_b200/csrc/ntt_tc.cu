@@ -367,6 +367,16 @@ __host__ __device__ constexpr int res_smem_bytes() {
          res_stages<STAGE>() * KC * 4 * kATile + (2 * res_stages<STAGE>() + 2 * kResRaw + 7) * 8 + 16;
 }
 
+// Timing probes of the resident kernel (-DTFHE_RES_DBG_VAL=k, tools/ab_res_dbg.sh;
+// 0 in normal builds, where every test below folds away): 1 epilogue drops
+// all math and stores, 2 epilogue does no stores (most folds then dead), 512
+// epilogue folds every column but does not store, 4 producers skip the data
+// loads (stage 2: no raw P tiles), 8 producers skip loads and byte split.
+#ifndef TFHE_RES_DBG_VAL
+#define TFHE_RES_DBG_VAL 0
+#endif
+constexpr int kResDbg = TFHE_RES_DBG_VAL;
+
 template <int STAGE, int BN, int KC>
 __global__ void __launch_bounds__(kResThreads, 1)
     ntt_res_kernel(const __grid_constant__ StageArgs a, int tiles_per_limb, long long units) {
@@ -436,7 +446,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
                a.in + (size_t)limb * a.batch * a.n + (size_t)tile * kRows * a.n2, bytes,
                &raw_full[rs]);
     };
-    if (STAGE == 2 && tid == 0)
+    if (STAGE == 2 && tid == 0 && !(kResDbg & 12))
       for (int it = 0; it < kResRaw && it < cnt; ++it) issue_raw(it, it);
     for (int it = 0; it < cnt; ++it) {
       const long long u = u0 + it;
@@ -466,12 +476,14 @@ __global__ void __launch_bounds__(kResThreads, 1)
       const int gr = tile * kRows + tid;
       const bool valid = gr < a.total_rows;
       uint8_t* sA = sData + s * kDataBytes;
-      if (STAGE == 2) {
+      if (kResDbg & 8) {
+        if (it >= kResStages) mbar_wait(&d_empty[s], ((it / kResStages) & 1) ^ 1);
+      } else if (STAGE == 2) {
         // P rows of a tile are contiguous (row (b, x) at gr * n2 within the limb):
         // one bulk copy per tile, issued kResRaw tiles ahead
         const int rs = it % kResRaw;
         const uint32_t rph = (uint32_t)((it / kResRaw) & 1);
-        mbar_wait(&raw_full[rs], rph);
+        if (!(kResDbg & 4)) mbar_wait(&raw_full[rs], rph);
         if (it >= kResStages) mbar_wait(&d_empty[s], ((it / kResStages) & 1) ^ 1);
         const uint8_t* row = sRaw + rs * kRawTile + (size_t)tid * a.K * 4;
         const int ng = (a.K + 3) / 4;
@@ -480,7 +492,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
           // groups of 4 k in a per-thread rotated order: conflict-free 16-byte reads
           const int g = g0 < ng ? (g0 + tid) % ng : g0;
           uint4 q = make_uint4(0, 0, 0, 0);
-          if (valid && g0 < ng) q = *reinterpret_cast<const uint4*>(row + g * 16);
+          if (valid && g0 < ng && !(kResDbg & 4)) q = *reinterpret_cast<const uint4*>(row + g * 16);
           uint32_t w[4];
           byte_planes(q.x, q.y, q.z, q.w, w);
           const uint32_t off = tile_off(tid, (g % 8) * 4, kRows);
@@ -488,8 +500,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<uint32_t*>(sA + ((g / 8) * 4 + j) * kATile + off) = w[j];
         }
-        mbar_arrive(&raw_empty[rs]);
-        if (tid == 0 && it + kResRaw < cnt) {
+        if (!(kResDbg & 4)) mbar_arrive(&raw_empty[rs]);
+        if (tid == 0 && it + kResRaw < cnt && !(kResDbg & 4)) {
           mbar_wait(&raw_empty[rs], rph);
           issue_raw(it + kResRaw, rs);
         }
@@ -503,7 +515,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
 #pragma unroll
       for (int g = 0; g < KC * 8; ++g) {
         const int k = g * 4;
-        if (valid && k < a.K) {
+        if (valid && k < a.K && !(kResDbg & 4)) {
           const uint32_t* p = src + (size_t)k * a.n2;
           v[g][0] = __ldg(p);
           v[g][1] = __ldg(p + a.n2);
@@ -569,12 +581,23 @@ __global__ void __launch_bounds__(kResThreads, 1)
           tc_fence_before();
           mbar_arrive(&acc_empty[ab]);   // buffer drained: the next tile's MMAs may start
         }
-        if (!valid) continue;
+        if (!valid || (kResDbg & 1)) continue;
         // Ntw == BN on this path: no per-column guard, and every per-unit mode
         // branch sits outside the column loops so the kCWr folds interleave
         uint32_t y[kCWr];
 #pragma unroll
         for (int e = 0; e < kCWr; ++e) y[e] = fold4<KC>(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
+        if (kResDbg & 2) {
+          if (y[0] == 0x7fffffff && y[kCWr - 1] == 1) a.out[0] = 0;
+          continue;
+        }
+        if (kResDbg & 512) {
+          uint32_t z = 0;
+#pragma unroll
+          for (int e = 0; e < kCWr; ++e) z ^= y[e] * (2 * e + 1);
+          if (z == 0x7fffffff) a.out[0] = 0;
+          continue;
+        }
         if (STAGE == 1) {
           // P[k1 = col][i2 = x] = S * W2[k1][i2]
           const int n2 = a.n2;
