@@ -60,6 +60,7 @@ struct StageArgs {
   int K, KC;             // contraction length, number of 32-chunks (padded)
   int Ntw;               // twiddle columns
   int total_rows;        // batch * R
+  int p_blocked;         // stage 1 (resident kernel): write P in the TS blocked layout
   LimbMap map;
   EpiArgs epi;
 };
@@ -566,6 +567,11 @@ __global__ void __launch_bounds__(kResThreads, 1)
       const int x = valid ? gr % a.R : 0;
       const int prime = a.map.prime[limb];
       const PrimeConst pc = a.pc[prime];
+      // stage 1: this row's P, row-major [k1][i2] or, when the TS stage 2
+      // follows (Ctx::ts_stage2), its blocked [i2/16][k1][16]; column stride ps
+      const int ps = a.p_blocked ? 16 : a.n2;
+      uint32_t* p_row = a.out + ((size_t)limb * a.batch + b) * a.n +
+                        (a.p_blocked ? (size_t)(x >> 4) * a.n1 * 16 + (x & 15) : (size_t)x);
 #pragma unroll 1
       for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += kCWr) {
         uint32_t acc[4][kCWr];
@@ -601,11 +607,11 @@ __global__ void __launch_bounds__(kResThreads, 1)
         if (STAGE == 1) {
           // P[k1 = col][i2 = x] = S * W2[k1][i2]
           const int n2 = a.n2;
-          uint32_t* o = a.out + ((size_t)limb * a.batch + b) * a.n + (size_t)c0 * n2 + x;
+          uint32_t* o = p_row + c0 * ps;
           const uint32_t* w = sW2 + c0 * n2 + x;
 #pragma unroll
           for (int e = 0; e < kCWr; ++e)
-            o[e * n2] = mul_shoup(y[e], w[e * n2], w[a.n + e * n2], pc.q);
+            o[e * ps] = mul_shoup(y[e], w[e * n2], w[a.n + e * n2], pc.q);
           continue;
         }
         // out[n1*k2 + k1], k2 = col, k1 = x
@@ -730,6 +736,10 @@ int launch_stage_any(const Ctx& c, int bn, int kc, const StageArgs& a, int npad,
       case 64 * 8 + 1: return launch_res<STAGE, 64, 1>(c, a, n_limbs, st);
       case 64 * 8 + 2: return launch_res<STAGE, 64, 2>(c, a, n_limbs, st);
     }
+  }
+  if (a.p_blocked) {
+    set_error("blocked P output needs the resident stage-1 kernel");
+    return 2;
   }
   return launch_stage_bn<STAGE>(bn, a, npad, n_limbs, st);
 }
@@ -871,9 +881,10 @@ int build_ntt_tables(Ctx& c) {
   if (c.sms <= 0) c.sms = 148;
   // twiddle-resident tensor-core path for n1, n2 in {128, 256}
   // (its single-correction Montgomery epilogue needs q > 2^20; see ntt_ts.cu)
-  c.use_ts = c.n1 >= 128 && c.n2 <= 256 &&
-             *std::min_element(c.primes.begin(), c.primes.end()) > (1u << 20);
-  if (c.use_ts) return build_ts_tables(c);
+  const bool big_q = *std::min_element(c.primes.begin(), c.primes.end()) > (1u << 20);
+  c.use_ts = c.n1 >= 128 && c.n2 <= 256 && big_q;
+  c.ts_stage2 = c.n1 == 64 && c.n2 == 128 && big_q;
+  if (c.use_ts || c.ts_stage2) return build_ts_tables(c);
   return 0;
 }
 
@@ -908,8 +919,10 @@ int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& m
   a.KC = c.kpad[0] / kKC;
   a.Ntw = c.n1;
   a.total_rows = batch * c.n2;
+  a.p_blocked = c.ts_stage2 ? 1 : 0;
   int rc = launch_stage_any<1>(c, c.bn[0], a.KC, a, c.npad[0], map.n, st);
   if (rc) return rc;
+  if (c.ts_stage2) return launch_ntt_ts_stage2(c, P, out, map, batch, inverse, epi, st);
   // stage 2: columns of W3 (k2), contraction over i2, rows (b, k1)
   a.in = P;
   a.out = out;

@@ -1,4 +1,5 @@
-// Twiddle-resident tensor-core NTT stages (n1, n2 in {128, 256}; N = 2^14..2^16).
+// Twiddle-resident tensor-core NTT stages (n1, n2 in {128, 256}; N = 2^14..2^16;
+// at N = 2^13 stage 2 only, after the resident small-n stage 1: Ctx::ts_stage2).
 //
 // Same math as ntt_tc.cu (TensorFHE's byte-sliced GEMM formulation, ref
 // ntt.py:212-340), re-tiled so the CONSTANT operand never streams:
@@ -873,6 +874,7 @@ int build_ts_tables(Ctx& c) {
   for (int var = 0; var < 5; ++var) {
       const int inv = var < 4 ? var >> 1 : 0, s = var < 4 ? var & 1 : 1;
       const bool ks = var == 4;
+      if (s == 0 && n1 < 128) continue;   // ts_stage2: stage 1 runs on the resident kernel
       const int ntw = s == 0 ? n1 : n2, K = ntw, H = ntw / 128;
       std::vector<uint32_t> tw((size_t)np * ntw * K);  // K words per row (4 planes x K/4)
       for (int p = 0; p < np; ++p) {
@@ -912,6 +914,7 @@ int build_ts_tables(Ctx& c) {
         return 3;
       }
   }
+  if (n1 < 128) return 0;   // ts_stage2: the resident stage 1 applies W2 itself
   // W2 * 2^96 mod q in [prime][i2/16][e][k1] layout: stage 1 multiplies its
   // folded result (S 2^-64) by this with another Montgomery step -> S * W2;
   // the layout makes the epilogue's per-row loads warp-coalesced
@@ -995,10 +998,30 @@ int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap
   if (rc) return rc;
   rc = launch_ts_k<1>(c, c.n1, a, st);
   if (rc) return rc;
+  return launch_ntt_ts_stage2(c, P, out, map, batch, inverse, epi, st);
+}
+
+int launch_ntt_ts_stage2(const Ctx& c, const uint32_t* P, uint32_t* out, const LimbMap& map,
+                         int batch, int inverse, const EpiArgs* epi, cudaStream_t st) {
+  TsArgs a;
+  memset(&a, 0, sizeof(a));
+  a.pc = c.d_pc;
+  a.n = c.n;
+  a.n1 = c.n1;
+  a.n2 = c.n2;
+  a.batch = batch;
+  a.n_limbs = map.n;
+  a.S = 1;
+  static const int dbg = getenv("TFHE_DBG") ? atoi(getenv("TFHE_DBG")) : 0;
+  a.dbg = dbg;
+  a.map = map;
+  if (epi) a.epi = *epi;
+  else a.epi.mode = EPI_STORE;
   // stage 2: rows k2 (n2 twiddle rows), data columns (b, k1)
   a.in = P;
   a.out = out;
-  if ((rc = make_tmap_stage2(c, &a.tmap, P, map.n, batch))) return rc;
+  int rc = make_tmap_stage2(c, &a.tmap, P, map.n, batch);
+  if (rc) return rc;
   a.twa = (epi && epi->mode == EPI_KS_MAC) ? c.d_twa_ks : c.d_twa[inverse][1];
   if (epi && epi->mode == EPI_KS_MAC && inverse) {
     set_error("fused key-switch MAC needs a forward transform");

@@ -90,6 +90,10 @@ struct Ctx {
   // is then y*2^32, the Montgomery form the fused key-switch MAC multiplies with
   uint32_t* d_twa_ks = nullptr;
   bool use_ts = false;
+  // N = 2^13 (n1 = 64, n2 = 128): stage 1 on the resident small-n kernel,
+  // writing P in the TS blocked layout, stage 2 on the TS kernel (K = 128),
+  // whose twiddles live in TMEM -- the resident kernel cannot hold K = 128
+  bool ts_stage2 = false;
   int sms = 148;
   std::vector<PrimeConst> h_pc;
 };
@@ -107,6 +111,9 @@ int launch_ntt_ts_stage1(const Ctx& c, const uint32_t* in, uint32_t* P, const Li
                          int batch, int inverse, cudaStream_t st);
 int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& map, int batch,
                   int inverse, const EpiArgs* epi, void* ws, cudaStream_t st);
+// TS stage 2 alone over the blocked P workspace (see Ctx::ts_stage2)
+int launch_ntt_ts_stage2(const Ctx& c, const uint32_t* P, uint32_t* out, const LimbMap& map,
+                         int batch, int inverse, const EpiArgs* epi, cudaStream_t st);
 
 // kernels (ntt_tc.cu)
 size_t ntt_workspace_bytes(const Ctx& c, int n_limbs, int batch);
