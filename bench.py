@@ -490,6 +490,26 @@ def run_b200(args):
     e2e_ok = bool(torch.equal(back.data, host_in))
     e2e_value = 2 * L * B * e2e_steps * world / e2e_s / 1e3
     bytes_per_call = L * B * N * 4
+    # the e2e ceiling: raw concurrent H2D + D2H copy bandwidth over the same
+    # pinned buffers (64 MiB chunks on two streams)
+    duplex = None
+    if rank == 0:
+        dst_host = back.data if isinstance(back.data, torch.Tensor) else None
+        if dst_host is not None and dst_host.is_pinned():
+            hin, hout = host_in.view(-1), dst_host.view(-1)
+            din = x.view(-1)
+            s_up, s_dn = torch.cuda.Stream(), torch.cuda.Stream()
+            step = 16 << 20   # int32 words per chunk (64 MiB)
+            for rep in range(2):
+                torch.cuda.synchronize()
+                t1 = time.perf_counter()
+                for off in range(0, hin.numel(), step):
+                    with torch.cuda.stream(s_up):
+                        din[off:off + step].copy_(hin[off:off + step], non_blocking=True)
+                    with torch.cuda.stream(s_dn):
+                        hout[off:off + step].copy_(din[off:off + step], non_blocking=True)
+                torch.cuda.synchronize()
+                duplex = 2 * bytes_per_call / (time.perf_counter() - t1) / 1e9
 
     if rank != 0:
         if world > 1:
@@ -530,7 +550,10 @@ def run_b200(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * bytes_per_call,
                 "d2h_bytes_per_step": 2 * bytes_per_call, "steps": e2e_steps,
                 "api": "batched_apply(BatchBuffer(pinned host), 'ntt'/'intt')",
-                "roundtrip_exact": e2e_ok},
+                "roundtrip_exact": e2e_ok,
+                "pcie_duplex_gbs": duplex,
+                "frac_of_pcie_duplex": (4 * bytes_per_call * e2e_steps / e2e_s / 1e9 / duplex)
+                if duplex else None},
         "gpu_launches": 4 * args.steps,
         "clocks": clk.summary(),
     }
