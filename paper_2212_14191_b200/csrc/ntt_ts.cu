@@ -214,7 +214,10 @@ TFHE_DEV uint32_t mont_reduce(uint64_t v, const PrimeConst& pc) {
 // Montgomery rounds: A = C_0..C_3 part (< 2^51), t = A 2^-32 (< 2^30), then
 // u = t + C_4 + C_5 2^8 + C_6 2^16 (< 2^44, built on the ALU pipe) and
 // y = u 2^-32 < q + 2^12.  Four multiplies instead of seven 64-bit ones: the
-// epilogue is bound by the integer-multiply pipe.
+// epilogue is bound by the integer-multiply pipe.  kLazy skips the final
+// correction (y < q + 2^12): a following Montgomery product with a factor < q
+// stays < q 2^32 and corrects once itself.
+template <bool kLazy = false>
 TFHE_DEV uint32_t fold_redc(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t c4,
                             uint32_t c5, uint32_t c6, const PrimeConst& pc) {
   const uint64_t A = (uint64_t)c0 + ((uint64_t)c1 << 8) + ((uint64_t)c2 << 16) + ((uint64_t)c3 << 24);
@@ -231,6 +234,7 @@ TFHE_DEV uint32_t fold_redc(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, 
       : "r"(c4), "r"(c5), "r"(c6), "r"(t));
   const uint32_t m1 = lo * pc.qneg_inv;
   const uint32_t y = (uint32_t)(((((uint64_t)hi << 32) | lo) + (uint64_t)m1 * pc.q) >> 32);
+  if (kLazy) return y;
   return y >= pc.q ? y - pc.q : y;
 }
 
@@ -540,8 +544,11 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
 #pragma unroll
       for (int e = 0; e < kCW; ++e) {
         // y = (sum_s C_s 2^(8s)) * 2^-64 mod q (the twiddles carry the 2^64 back)
-        y[e] = fold_redc(acc[0][e], acc[1][e], acc[2][e], acc[3][e], acc[4][e], acc[5][e],
-                         acc[6][e], pc);
+        // stage 1 (Hadamard) and the key-switch MAC multiply y by a factor < q
+        // in Montgomery form next, so they take it uncorrected
+        y[e] = fold_redc<STAGE == 1 || MODE == EPI_KS_MAC>(acc[0][e], acc[1][e], acc[2][e],
+                                                           acc[3][e], acc[4][e], acc[5][e],
+                                                           acc[6][e], pc);
       }
       if (warp == 4) TS_TRACE(15, i);
       if (kDbg & 2) {
