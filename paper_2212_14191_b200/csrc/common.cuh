@@ -26,6 +26,10 @@ TFHE_DEV uint32_t mul_shoup(uint32_t b, uint32_t w, uint32_t wp, uint32_t q) {
   uint32_t r = w * b - t * q;
   return r >= q ? r - q : r;
 }
+// mul_shoup without the final correction: result in [0, 2q) (q < 2^31)
+TFHE_DEV uint32_t mul_shoup_lazy(uint32_t b, uint32_t w, uint32_t wp, uint32_t q) {
+  return w * b - __umulhi(wp, b) * q;
+}
 // x mod q for x < 2^64 with mu = floor(2^64 / q) (Barrett, one correction
 // suffices because q < 2^31 keeps the quotient error below 2).
 TFHE_DEV uint32_t reduce64(uint64_t x, uint32_t q, uint64_t mu) {

@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
           const uint32_t* w = sW2 + c0 * n2 + x;
 #pragma unroll
           for (int e = 0; e < kCWr; ++e)
-            o[e * ps] = mul_shoup(y[e], w[e * n2], w[a.n + e * n2], pc.q);
+            o[e * ps] = mul_shoup_lazy(y[e], w[e * n2], w[a.n + e * n2], pc.q);   // P in [0, 2q)
           continue;
         }
         // out[n1*k2 + k1], k2 = col, k1 = x

@@ -204,6 +204,13 @@ TFHE_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "mem
 TFHE_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 TFHE_DEV void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// v < q 2^32 -> v 2^-32 mod q in [0, 2q).  Stage 1 leaves P in [0, 2q): stage 2
+// only byte-splits it (any 32-bit value; the fold bounds hold) and the result
+// is exact mod q
+TFHE_DEV uint32_t mont_reduce_lazy(uint64_t v, const PrimeConst& pc) {
+  const uint32_t mq = (uint32_t)v * pc.qneg_inv;
+  return (uint32_t)((v + (uint64_t)mq * pc.q) >> 32);
+}
 TFHE_DEV uint32_t mont_reduce(uint64_t v, const PrimeConst& pc) {
   const uint32_t mq = (uint32_t)v * pc.qneg_inv;
   const uint32_t t = (uint32_t)((v + (uint64_t)mq * pc.q) >> 32);
@@ -561,7 +568,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
         const uint8_t* wt = wstg + buf * kInBuf;
 #pragma unroll
         for (int e = 0; e < kCW; ++e)
-          y[e] = mont_reduce((uint64_t)y[e] * *reinterpret_cast<const uint32_t*>(wt + e * 128 + lane * 4), pc);
+          y[e] = mont_reduce_lazy((uint64_t)y[e] * *reinterpret_cast<const uint32_t*>(wt + e * 128 + lane * 4), pc);
         // blocked P layout [limb][b][i2/16][k1][16]: the warp's rows are 64 B apart
         uint32_t* dst = a.out + (((size_t)limb * a.batch + b) * (a.n2 / kNC) + w.x0 / kNC) * kNC * a.n1 +
                         (size_t)(h * 128 + wq * 32) * kNC + cb;
