@@ -223,11 +223,17 @@ def run_b200(args):
     import torch.distributed as dist
 
     rank, world = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1)
-    local = _env_int("LOCAL_RANK", 0)
+    # TFHE_BENCH_SHARED_GPU=1 (development check only): every rank on cuda:0
+    # with a gloo group, to exercise the N > 1 code path on a one-GPU box
+    shared = os.environ.get("TFHE_BENCH_SHARED_GPU") == "1"
+    local = 0 if shared else _env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
@@ -236,7 +242,7 @@ def run_b200(args):
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if shared else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
