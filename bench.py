@@ -414,10 +414,23 @@ def run_b200(args):
             c0ctx.ntt(x0, q0, out=f0)
             c0ctx.ntt(f0, q0, inverse=True, out=y0)
         ms0 = timed(cfg0, 20)
+        # the same step replayed from a CUDA graph (launch-latency bound: 4 small launches)
+        ms0g = None
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                cfg0()
+            ms0g = timed(graph.replay, 20)
+            del graph
+        except Exception:
+            ms0g = None
         sweep["config0"] = {"workload": "fwd+inv NTT, N=2^12, one 30-bit prime, batch 64 "
                                         "(BASELINE configs[0])",
                             "limb_ntt_kops": 2 * 64 * world / (ms0 / 1e3) / 1e3,
-                            "us_per_step": ms0 * 1e3}
+                            "us_per_step": ms0 * 1e3,
+                            "cuda_graph": None if ms0g is None else {
+                                "limb_ntt_kops": 2 * 64 * world / (ms0g / 1e3) / 1e3,
+                                "us_per_step": ms0g * 1e3}}
         for logn in range(12, 17):
             nn = 1 << logn
             qs = generate_primes(nn, [29, 29])
