@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define TFHE_ABI_VERSION 2
+#define TFHE_ABI_VERSION 3
 #define TFHE_OK 0
 #define TFHE_EINVAL 2
 #define TFHE_ECUDA 3
@@ -127,6 +127,14 @@ int tfhe_keyswitch(TfheCtx* ctx, const uint32_t* d, int level, int batch, const 
 int tfhe_hmult(TfheCtx* ctx, const uint32_t* ct0, const uint32_t* ct1, int level, int batch,
                const uint32_t* rlk, int dnum, uint32_t* out, void* ws, size_t ws_bytes,
                void* stream);
+/* HMULT + relinearisation + rescale in one pipeline: out (2, level, B, n) equals
+ * tfhe_rescale(tfhe_hmult(ct0, ct1)) bit for bit (ref ckks.py:265-274 then
+ * :291-311) with 2*level fewer limb-NTTs -- ModDown's and the rescale's forward
+ * NTTs merge by linearity (capi.cu: moddown_rescale).  level >= 1.
+ * Workspace: tfhe_ckks_workspace_bytes(ctx, level, batch). */
+int tfhe_hmult_rescale(TfheCtx* ctx, const uint32_t* ct0, const uint32_t* ct1, int level,
+                       int batch, const uint32_t* rlk, int dnum, uint32_t* out, void* ws,
+                       size_t ws_bytes, void* stream);
 /* rescale (ckks.py:291-311): (2, level+1, batch, n) -> (2, level, batch, n) */
 int tfhe_rescale(TfheCtx* ctx, const uint32_t* ct, int level, int batch, uint32_t* out, void* ws,
                  size_t ws_bytes, void* stream);

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 #: in-tree build; TFHE_B200_LIB may point at another build of the same ABI
 #: (A/B performance experiments)
 LIB_PATH = os.environ.get("TFHE_B200_LIB") or os.path.join(_HERE, "libtfhe_b200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 EINVAL = 2
 ECUDA = 3
@@ -51,6 +51,8 @@ SIGNATURES = {
                                       _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "tfhe_hmult": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int,
                                   _vp, _vp, ctypes.c_size_t, _vp]),
+    "tfhe_hmult_rescale": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp,
+                                          ctypes.c_int, _vp, _vp, ctypes.c_size_t, _vp]),
     "tfhe_rescale": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp, _vp,
                                     ctypes.c_size_t, _vp]),
     "tfhe_hrotate": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_uint32, _vp,

@@ -234,6 +234,19 @@ class CkksContext(ClientMixin):
                            out=out)
         return CiphertextBatch(data=d, level=c0.level, scale=c0.scale * c1.scale)
 
+    def hmult_rescale_batch(self, c0: CiphertextBatch, c1: CiphertextBatch, rlk, out=None):
+        """`rescale_batch(hmult_batch(c0, c1, rlk))` in one pipeline, bit-identical:
+        ModDown's and the rescale's forward NTTs merge by linearity (2*level
+        fewer limb-NTTs; capi.cu moddown_rescale)."""
+        if c0.level != c1.level or c0.data.shape != c1.data.shape:
+            raise ParameterError("batch operands must match in level and shape")
+        if c0.level < 1:
+            raise ParameterError("no levels left to rescale")
+        q_top = self.params.chain.q[c0.level]
+        d = self.dev.hmult_rescale(c0.data, c1.data, c0.level, self.device_key(rlk),
+                                   self.params.dnum, out=out)
+        return CiphertextBatch(data=d, level=c0.level - 1, scale=c0.scale * c1.scale / q_top)
+
     def rescale_batch(self, cb: CiphertextBatch, out=None):
         if cb.level < 1:
             raise ParameterError("no levels left to rescale")

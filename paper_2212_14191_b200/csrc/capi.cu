@@ -152,14 +152,103 @@ int fill_bconv(const Ctx& c, const std::vector<int>& src, const std::vector<int>
   return 0;
 }
 
+// ModDown fused with the rescale that follows it (tfhe_hmult_rescale).  With
+// top = level, P = prod of the specials, conv_i the base-converted special
+// rows (coefficient domain) and X_i = acc_i P^-1 + base_i:
+//   ModDown_i  = X_i - NTT_i(conv_i) P^-1                     (ckks.py:367-381)
+//   rescale_i  = (ModDown_i - NTT_i(T)) q_top^-1,  T = INTT_top(ModDown_top)
+//                                                             (ckks.py:291-311)
+//              = (X_i - NTT_i(conv_i P^-1 + T)) q_top^-1        (NTT_i is linear mod q_i)
+// so one forward NTT per output row replaces ModDown's and the rescale's
+// (2 level fewer limb-NTTs), bit-identical to rescale(hmult(.)).
+int moddown_rescale(const Ctx& c, const CkksGeom& g, uint32_t* acc, const uint32_t* md_in,
+                    uint32_t* wbuf, uint32_t* top, uint32_t* tcoef, const uint32_t* base,
+                    const int16_t* base_rows, uint32_t* out, int batch, uint32_t* ntt_ws,
+                    size_t ntt_ws_bytes, cudaStream_t st) {
+  const int lv = g.l1 - 1;   // the prime rescale drops
+  const int64_t U = (int64_t)batch * c.n;
+  auto p_inv = [&](int i) {
+    const uint32_t q = c.primes[i];
+    uint64_t pm = 1;
+    for (int k = 0; k < g.K; ++k) pm = pm * (c.primes[g.Lc + k] % q) % q;
+    return invmod(pm, q);
+  };
+  auto md_row = [&](int cmp, int i) { return (int16_t)(g.K > 1 ? cmp * g.nr + i : cmp); };
+  int rc;
+  // 1. ModDown of the top row alone (as the unfused path computes it)
+  LimbMap mt;
+  EpiArgs et;
+  memset(&et, 0, sizeof(et));
+  et.mode = EPI_SUB_SCALE;
+  et.x = acc;
+  et.base = base;
+  mt.n = 2;
+  for (int cmp = 0; cmp < 2; ++cmp) {
+    mt.prime[cmp] = (int16_t)lv;
+    mt.in_row[cmp] = md_row(cmp, lv);
+    mt.out_row[cmp] = (int16_t)cmp;
+    et.x_row[cmp] = (int16_t)(cmp * g.T + lv);
+    et.base_row[cmp] = base ? base_rows[cmp * g.nr + lv] : (int16_t)-1;
+    et.s[cmp] = p_inv(lv);
+    et.s_shoup[cmp] = shoup(et.s[cmp], c.primes[lv]);
+  }
+  if ((rc = launch_ntt(c, md_in, top, mt, batch, 0, &et, ntt_ws, ntt_ws_bytes, st))) return rc;
+  // 2. T = INTT_top(top)
+  LimbMap mi;
+  mi.n = 2;
+  for (int cmp = 0; cmp < 2; ++cmp) {
+    mi.prime[cmp] = (int16_t)lv;
+    mi.in_row[cmp] = mi.out_row[cmp] = (int16_t)cmp;
+  }
+  if ((rc = launch_ntt(c, top, tcoef, mi, batch, 1, nullptr, ntt_ws, ntt_ws_bytes, st))) return rc;
+  if (lv == 0) return 0;
+  // 3. X_i (in place in acc) and W_i = conv_i P^-1 + T mod q_i (row cmp * nr + i of wbuf,
+  //    in place over conv_i when K > 1)
+  MdRsArgs ar;
+  LimbMap mr;
+  EpiArgs er;
+  memset(&er, 0, sizeof(er));
+  er.mode = EPI_SUB_SCALE;
+  er.x = acc;
+  mr.n = 2 * lv;
+  const uint32_t q_top = c.primes[lv];
+  for (int cmp = 0; cmp < 2; ++cmp)
+    for (int i = 0; i < lv; ++i) {
+      const int l = cmp * lv + i;
+      ar.prime[l] = (int16_t)i;
+      ar.acc_row[l] = (int16_t)(cmp * g.T + i);
+      ar.base_row[l] = base ? base_rows[cmp * g.nr + i] : (int16_t)-1;
+      ar.conv_row[l] = md_row(cmp, i);
+      ar.w_row[l] = (int16_t)(cmp * g.nr + i);
+      ar.t_row[l] = (int16_t)cmp;
+      ar.pinv[l] = p_inv(i);
+      ar.pinv_shoup[l] = shoup(ar.pinv[l], c.primes[i]);
+      // 4. out_i = (X_i - NTT_i(W_i)) q_top^-1
+      mr.prime[l] = (int16_t)i;
+      mr.in_row[l] = (int16_t)(cmp * g.nr + i);
+      mr.out_row[l] = (int16_t)l;
+      er.x_row[l] = (int16_t)(cmp * g.T + i);
+      er.base_row[l] = -1;
+      er.s[l] = invmod(q_top, c.primes[i]);
+      er.s_shoup[l] = shoup(er.s[l], c.primes[i]);
+    }
+  if ((rc = launch_md_rescale_prep(c, acc, base, md_in, tcoef, wbuf, ar, 2 * lv, U, st))) return rc;
+  return launch_ntt(c, wbuf, out, mr, batch, 0, &er, ntt_ws, ntt_ws_bytes, st);
+}
+
 // key switch of the local rows d (nr, B, n; chain rows [r0, r0+nr), NTT
 // domain) -> out (2, nr, B, n) [+ add rows base_rows[]].  y_full is the
 // coefficient-domain d over ALL level+1 chain rows (the all-gathered INTT of
 // the limb-partitioned key switch); NULL = compute it here from d, which then
 // must hold every chain row (r0 = 0, nr = level + 1).
+//
+// rs_scratch != NULL fuses the rescale that follows (tfhe_hmult_rescale): out is
+// then (2, level, B, n) = rescale(ModDown(.)) bit for bit, and rs_scratch (>= 2
+// rows, dead after ModUp) holds the top row's coefficient form.
 int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int level, int batch,
                    const uint32_t* key, int dnum, int r0, int nr, uint32_t* out,
-                   const uint32_t* base, const int16_t* base_rows, Carve& cv, cudaStream_t st) {
+                   const uint32_t* base, const int16_t* base_rows, Carve& cv, cudaStream_t st,
+                   uint32_t* rs_scratch = nullptr) {
   const Ctx& c = h->c;
   CkksGeom g = geom(h, level, dnum, r0, nr);
   set_group(g, c, batch);
@@ -169,7 +258,13 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
   const size_t ntt_ws_bytes = ks_ntt_rows(g) * U * 4;
   uint32_t* ntt_ws = cv.take<uint32_t>(ntt_ws_bytes);
   uint32_t* ysp = cv.take<uint32_t>(2 * g.K * U * 4);
-  uint32_t* conv = g.need_conv ? cv.take<uint32_t>(ks_conv_rows(g) * U * 4) : nullptr;
+  // (the fused rescale builds its NTT input W in the conversion rows)
+  uint32_t* conv =
+      g.need_conv || rs_scratch ? cv.take<uint32_t>(ks_conv_rows(g) * U * 4) : nullptr;
+  if (rs_scratch && (y_full || r0 != 0 || g.nr != g.l1 || level < 1)) {
+    set_error("fused rescale needs the unpartitioned key switch at level >= 1");
+    return TFHE_EINVAL;
+  }
   if (!cv.ok) {
     set_error("ckks workspace too small");
     return TFHE_EINVAL;
@@ -346,6 +441,8 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
         return rc;
     md_in = conv;
   }
+  if (rs_scratch) return moddown_rescale(c, g, acc, md_in, conv, y, rs_scratch, base, base_rows,
+                                         out, batch, ntt_ws, ntt_ws_bytes, st);
   LimbMap md;
   EpiArgs ep;
   memset(&ep, 0, sizeof(ep));
@@ -640,6 +737,37 @@ int tfhe_hmult(TfheCtx* h, const uint32_t* ct0, const uint32_t* ct1, int level, 
   for (int l = 0; l < 2 * l1; ++l) rows[l] = (int16_t)l;  // (d0, d1) added to (ksb, ksa)
   return keyswitch_impl(h, dd + 2 * P, nullptr, level, batch, rlk, dnum, 0, l1, out, dd, rows, cv,
                         st);
+}
+
+int tfhe_hmult_rescale(TfheCtx* h, const uint32_t* ct0, const uint32_t* ct1, int level,
+                       int batch, const uint32_t* rlk, int dnum, uint32_t* out, void* ws,
+                       size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_ctx(h)) || (rc = check_level(h, level, batch, dnum ? dnum : -1))) return rc;
+  if (level < 1) {
+    set_error("no levels left to rescale");
+    return TFHE_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int l1 = level + 1;
+  const size_t P = (size_t)l1 * batch * h->c.n;  // elements per component
+  Carve cv{static_cast<uint8_t*>(ws), ws_bytes};
+  uint32_t* dd = cv.take<uint32_t>(3 * P * 4);  // d0 | d1 | d2
+  if (!cv.ok) {
+    set_error("ckks workspace too small");
+    return TFHE_EINVAL;
+  }
+  int16_t rp[kMaxRows];
+  for (int i = 0; i < l1; ++i) rp[i] = (int16_t)i;
+  if ((rc = launch_tensor(h->c, ct0, ct0 + P, ct1, ct1 + P, dd, dd + P, dd + 2 * P, rp, l1,
+                          (int64_t)batch * h->c.n, st)))
+    return rc;
+  int16_t rows[kMaxLimbs];
+  for (int l = 0; l < 2 * l1; ++l) rows[l] = (int16_t)l;
+  // d2 (the key-switch input) is dead after ModUp: its first rows hold the top
+  // row's coefficient form for the fused rescale
+  return keyswitch_impl(h, dd + 2 * P, nullptr, level, batch, rlk, dnum, 0, l1, out, dd, rows, cv,
+                        st, dd + 2 * P);
 }
 
 int tfhe_rescale(TfheCtx* h, const uint32_t* ct, int level, int batch, uint32_t* out, void* ws,

@@ -147,6 +147,34 @@ __global__ void ks_mac_kernel(const uint32_t* __restrict__ x, const uint32_t* __
   }
 }
 
+// fused ModDown + rescale preparation (poly_ops.h: MdRsArgs)
+__global__ void md_rescale_prep_kernel(uint32_t* __restrict__ acc, const uint32_t* __restrict__ base,
+                                       const uint32_t* conv, const uint32_t* __restrict__ t,
+                                       uint32_t* w, const PrimeConst* __restrict__ pcs,
+                                       const __grid_constant__ MdRsArgs ar, int64_t per_row) {
+  const int row = blockIdx.y;
+  const PrimeConst pc = pcs[ar.prime[row]];
+  const uint32_t pi = ar.pinv[row], pis = ar.pinv_shoup[row];
+  uint32_t* xr = acc + ar.acc_row[row] * per_row;
+  const uint32_t* br = ar.base_row[row] >= 0 ? base + ar.base_row[row] * per_row : nullptr;
+  const uint32_t* cr = conv + ar.conv_row[row] * per_row;
+  const uint32_t* tr = t + ar.t_row[row] * per_row;
+  uint32_t* wr = w + ar.w_row[row] * per_row;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+    uint4 x = ld4(xr + i), cv = ld4(cr + i), tv = ld4(tr + i);
+    uint4 b = br ? ld4(br + i) : make_uint4(0, 0, 0, 0);
+    uint4 wv;
+#define TFHE_MDRS(c)                                                                   \
+  x.c = add_mod(mul_shoup(x.c, pi, pis, pc.q), b.c, pc.q);                             \
+  wv.c = add_mod(mul_shoup(cv.c, pi, pis, pc.q), reduce64(tv.c, pc.q, pc.mu), pc.q);
+    TFHE_MDRS(x) TFHE_MDRS(y) TFHE_MDRS(z) TFHE_MDRS(w)
+#undef TFHE_MDRS
+    st4(xr + i, x);
+    st4(wr + i, wv);
+  }
+}
+
 // NTT domain: out[k] = in[((t (2k+1) mod 2n) - 1) / 2]   (kernels.py:77-96)
 __global__ void automorph_ntt_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                      uint32_t t, int log_n, int64_t rows) {
@@ -306,6 +334,19 @@ int launch_ks_mac(const Ctx& c, const uint32_t* x, const uint32_t* kb, const uin
   dim3 g = grid_rows((int64_t)batch * c.n, rows, 256);
   ks_mac_kernel<<<g, 256, 0, st>>>(x, kb, ka, acc_b, acc_a, c.d_pc, ma, batch, c.n, first);
   return check("ks mac kernel");
+}
+
+int launch_md_rescale_prep(const Ctx& c, uint32_t* acc, const uint32_t* base, const uint32_t* conv,
+                           const uint32_t* t, uint32_t* w, const MdRsArgs& ar, int rows,
+                           int64_t per_row, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  if (rows > kMaxRows || per_row % 4) {
+    set_error("md_rescale_prep: too many rows or unaligned rows");
+    return 2;
+  }
+  dim3 g = grid_rows(per_row, rows, 256);
+  md_rescale_prep_kernel<<<g, 256, 0, st>>>(acc, base, conv, t, w, c.d_pc, ar, per_row);
+  return check("md_rescale_prep kernel");
 }
 
 int launch_automorph(const Ctx& c, const uint32_t* in, uint32_t* out, uint32_t t, int ntt_domain,

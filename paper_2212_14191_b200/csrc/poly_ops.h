@@ -35,4 +35,19 @@ int launch_automorph(const Ctx& c, const uint32_t* in, uint32_t* out, uint32_t t
 int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,
                  cudaStream_t st);
 
+// Fused ModDown + rescale preparation, per row l = (component, chain row i < top):
+//   X = acc[acc_row] * P^-1 + base[base_row]     (in place; base_row < 0: none)
+//   W = conv[conv_row] * P^-1 + (T[t_row] mod q_i)   -> w[w_row]  (may be in place)
+// so that NTT_i(W) = NTT_i(conv) P^-1 + NTT_i(T) and
+// (X - NTT_i(W)) q_top^-1 = rescale(ModDown(.)) exactly (see capi.cu).
+struct MdRsArgs {
+  int16_t prime[kMaxRows];
+  int16_t acc_row[kMaxRows], base_row[kMaxRows], conv_row[kMaxRows], t_row[kMaxRows];
+  int16_t w_row[kMaxRows];
+  uint32_t pinv[kMaxRows], pinv_shoup[kMaxRows];
+};
+int launch_md_rescale_prep(const Ctx& c, uint32_t* acc, const uint32_t* base, const uint32_t* conv,
+                           const uint32_t* t, uint32_t* w, const MdRsArgs& ar, int rows,
+                           int64_t per_row, cudaStream_t st);
+
 }  // namespace tfhe

@@ -267,6 +267,17 @@ class DeviceContext:
             _ptr(ws), ws.numel(), _stream(self.device)), "tfhe_hmult")
         return out
 
+    def hmult_rescale(self, ct0, ct1, level, rlk, dnum, out=None):
+        """rescale(hmult(ct0, ct1)) in one native pipeline (bit-identical)."""
+        batch = ct0.shape[2]
+        if out is None:
+            out = self.empty(2, level, batch, self.n)
+        ws = self.ckks_workspace(level, batch)
+        _lib.check(self.lib.tfhe_hmult_rescale(
+            self.handle, _ptr(ct0), _ptr(ct1), level, batch, _ptr(rlk), dnum, _ptr(out),
+            _ptr(ws), ws.numel(), _stream(self.device)), "tfhe_hmult_rescale")
+        return out
+
     def rescale(self, ct, level, out=None):
         batch = ct.shape[2]
         if out is None:

@@ -68,6 +68,13 @@ def _run(kind, level, seed):
     if level >= 1:
         r = ctx.rescale(m)
         out["hmult_rescale"] = np.stack([r.b.rows, r.a.rows])
+        # the fused operator (ModDown's and the rescale's NTTs merged) gives
+        # the same bits, so the golden check of hmult_rescale pins it too
+        fb = ctx.hmult_rescale_batch(ctx.batch_from_ciphertexts([c0]),
+                                     ctx.batch_from_ciphertexts([c1]), rlk)
+        fused = fb.data.cpu().numpy().view(np.uint32)[:, :, 0]
+        assert fb.level == level - 1
+        assert np.array_equal(fused, out["hmult_rescale"]), "fused hmult+rescale"
         r0 = ctx.rescale(c0)
         out["rescale"] = np.stack([r0.b.rows, r0.a.rows])
     h = ctx.hrotate(c0, 1, rk)

@@ -11,12 +11,15 @@ L1, E = p.l_max + 1, p.l_max + 1 + p.k
 key = torch.randint(0, 1 << 26, (p.dnum, 2, E, p.n), dtype=torch.int32, device="cuda")
 c0 = CiphertextBatch(torch.randint(0, 1 << 26, (2, L1, B, p.n), dtype=torch.int32, device="cuda"), p.l_max)
 c1 = CiphertextBatch(torch.randint(0, 1 << 26, (2, L1, B, p.n), dtype=torch.int32, device="cuda"), p.l_max)
+fused = len(sys.argv) > 3 and sys.argv[3] == "fused"
+op = (lambda: ck.hmult_rescale_batch(c0, c1, key)) if fused else \
+    (lambda: ck.rescale_batch(ck.hmult_batch(c0, c1, key)))
 for _ in range(2):
-    ck.rescale_batch(ck.hmult_batch(c0, c1, key))
+    op()
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record()
 for _ in range(3):
-    ck.rescale_batch(ck.hmult_batch(c0, c1, key))
+    op()
 e.record(); torch.cuda.synchronize()
-print(f"{p.n} B={B}: {s.elapsed_time(e)/3:.2f} ms per hmult+rescale batch -> {3*B/(s.elapsed_time(e)/1e3):.1f}/s")
+print(f"{'fused ' if fused else ''}{p.n} B={B}: {s.elapsed_time(e)/3:.2f} ms per hmult+rescale batch -> {3*B/(s.elapsed_time(e)/1e3):.1f}/s")
