@@ -70,7 +70,9 @@ struct StageArgs {
 // Montgomery step (v < q 2^32) replaces the 64-bit Barrett reduction.  With
 // K <= 64 (KC <= 2) every C_i < 4 K 255^2 <= 2^24, so the pairs C_0 + 2^8 C_1
 // and C_2 + 2^8 C_3 fit 32 bits; larger K folds in 64 bits throughout.
-template <int KC>
+// kLazy: the Montgomery result is left in [0, 2q) for a consumer that takes
+// any 32-bit operand (the stage-1 Shoup Hadamard).
+template <int KC, bool kLazy = false>
 TFHE_DEV uint32_t fold4(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const PrimeConst& pc) {
   const uint64_t v =
       KC <= 2 ? (uint64_t)(c0 + (c1 << 8)) + ((uint64_t)(c2 + (c3 << 8)) << 16)
@@ -78,6 +80,7 @@ TFHE_DEV uint32_t fold4(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, cons
   if (pc.pad[0]) {
     const uint32_t m = (uint32_t)v * pc.qneg_inv;
     const uint32_t t = (uint32_t)((v + (uint64_t)m * pc.q) >> 32);
+    if (kLazy) return t;
     return t >= pc.q ? t - pc.q : t;
   }
   return reduce64(v, pc.q, pc.mu);
@@ -592,7 +595,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
         // branch sits outside the column loops so the kCWr folds interleave
         uint32_t y[kCWr];
 #pragma unroll
-        for (int e = 0; e < kCWr; ++e) y[e] = fold4<KC>(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
+        for (int e = 0; e < kCWr; ++e)   // stage 1: the Shoup Hadamard takes y uncorrected
+          y[e] = fold4<KC, STAGE == 1>(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
         if (kResDbg & 2) {
           if (y[0] == 0x7fffffff && y[kCWr - 1] == 1) a.out[0] = 0;
           continue;
