@@ -582,6 +582,7 @@ void tfhe_ctx_destroy(TfheCtx* h) {
   for (int i = 0; i < 2; ++i) {
     for (int s = 0; s < 2; ++s) {
       cudaFree(c.d_tw[i][s]);
+      if (i == 0 && s == 0) cudaFree(c.d_tw_ks);
       cudaFree(c.d_twa[i][s]);
       if (i == 0 && s == 0) cudaFree(c.d_twa_ks);
     }

@@ -86,6 +86,18 @@ TFHE_DEV uint32_t fold4(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, cons
   return reduce64(v, pc.q, pc.mu);
 }
 
+// key-switch MAC product y k mod q: y arrives in Montgomery form (y 2^32, from
+// the 2^64-scaled stage-2 twiddles) for Montgomery primes, else plain (Barrett)
+TFHE_DEV uint32_t mac_mul(uint32_t y, uint32_t k, const PrimeConst& pc) {
+  if (pc.pad[0]) {
+    const uint64_t v = (uint64_t)y * k;
+    const uint32_t m = (uint32_t)v * pc.qneg_inv;
+    const uint32_t t = (uint32_t)((v + (uint64_t)m * pc.q) >> 32);
+    return t >= pc.q ? t - pc.q : t;
+  }
+  return mul_mod(y, k, pc.q, pc.mu);
+}
+
 // Stage-2 epilogue operands of W consecutive output columns col0.. of row
 // (b, x): the accumulator (EPI_KS_MAC, not first) or x and base (EPI_SUB_SCALE).
 // Every load is issued before any of the row's stores: written inline, each
@@ -124,8 +136,8 @@ TFHE_DEV void epi2_store(const StageArgs& a, int limb, int b, int x, int col, ui
   const size_t pos = (size_t)col * a.n1 + x;   // out[n1*k2 + k1], k2 = col, k1 = x
   const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + b) * a.n;
   if (a.epi.mode == EPI_KS_MAC) {
-    const uint32_t tb = mul_mod(y, kb[pos], pc.q, pc.mu);
-    const uint32_t ta = mul_mod(y, ka[pos], pc.q, pc.mu);
+    const uint32_t tb = mac_mul(y, kb[pos], pc);
+    const uint32_t ta = mac_mul(y, ka[pos], pc);
     a.epi.acc_b[orow + pos] = a.epi.first ? tb : add_mod(p0, tb, pc.q);
     a.epi.acc_a[orow + pos] = a.epi.first ? ta : add_mod(p1, ta, pc.q);
     return;
@@ -628,8 +640,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
           uint32_t tb[kCWr], ta[kCWr];
 #pragma unroll
           for (int e = 0; e < kCWr; ++e) {
-            tb[e] = mul_mod(y[e], kb[e * n1], pc.q, pc.mu);
-            ta[e] = mul_mod(y[e], kb[a.n + e * n1], pc.q, pc.mu);
+            tb[e] = mac_mul(y[e], kb[e * n1], pc);
+            ta[e] = mac_mul(y[e], kb[a.n + e * n1], pc);
           }
           if (a.epi.first) {
 #pragma unroll
@@ -787,8 +799,13 @@ int build_ntt_tables(Ctx& c) {
   std::vector<uint8_t> tw;
   std::vector<uint32_t> w2((size_t)np * n), w2s((size_t)np * n);
   std::vector<uint32_t> pw(two_n), T;
-  for (int inv = 0; inv < 2; ++inv) {
-    for (int s = 0; s < 2; ++s) {
+  // variants 0..3: (inv, stage) = (v >> 1, v & 1); variant 4: forward stage 2
+  // with one more 2^32 for the key-switch MAC epilogue (Montgomery primes): the
+  // stage-2 result is then y 2^32, and one Montgomery product per key gives y k
+  for (int var = 0; var < 5; ++var) {
+    {
+      const int inv = var < 4 ? var >> 1 : 0, s = var < 4 ? var & 1 : 1;
+      const bool ks = var == 4;
       const int ntw = s == 0 ? n1 : n2, K = ntw, BN = c.bn[s], KC = c.kpad[s] / kKC;
       tw.assign(c.tw_stride[s] * np, 0);
       T.resize((size_t)ntw * K);
@@ -796,11 +813,12 @@ int build_ntt_tables(Ctx& c) {
         const uint32_t q = c.primes[p];
         const bool mont = q > (1u << 20);   // Montgomery fold (fold4) for this prime
         const uint32_t r32 = powmod_h(2, 32, q);
+        const uint32_t tw_scale = mont ? (ks ? mulmod_h(r32, r32, q) : r32) : 1u;
         uint32_t root = inv ? powmod_h(c.psis[p], q - 2, q) : c.psis[p];
         pw[0] = 1;
         for (uint64_t e = 1; e < two_n; ++e) pw[e] = mulmod_h(pw[e - 1], root, q);
         const uint32_t n_inv = powmod_h(n, q - 2, q);
-        if (inv == 0 && s == 0) {
+        if (var == 0) {
           PrimeConst& k = c.h_pc[p];
           k.q = q;
           k.n_inv = n_inv;
@@ -836,7 +854,7 @@ int build_ntt_tables(Ctx& c) {
             uint32_t t = T[(size_t)cc * K + k];
             for (int j = 0; j < 4; ++j) {
               // V_j = 2^(8j) T (x 2^32 for the Montgomery fold) mod q
-              uint32_t vj = mulmod_h(mont ? mulmod_h(t, r32, q) : t, 1ull << (8 * j), q);
+              uint32_t vj = mulmod_h(mulmod_h(t, tw_scale, q), 1ull << (8 * j), q);
               for (int i = 0; i < 4; ++i) {
                 size_t tile = ((size_t)(ct * KC + kc) * 4 + j) * 4 + i;
                 size_t off = tile * (BN * kKC) + (kr >> 4) * (BN * 16) + (cr >> 3) * 128 +
@@ -846,7 +864,7 @@ int build_ntt_tables(Ctx& c) {
             }
           }
         }
-        if (s == 0) {
+        if (s == 0 && !ks) {
           for (int k1 = 0; k1 < n1; ++k1)
             for (int i2 = 0; i2 < n2; ++i2) {
               uint64_t e = inv ? (2ull * k1 * i2 + k1) : (2ull * k1 * i2 + i2);
@@ -856,12 +874,13 @@ int build_ntt_tables(Ctx& c) {
             }
         }
       }
-      if (cudaMalloc(&c.d_tw[inv][s], tw.size()) != cudaSuccess ||
-          cudaMemcpy(c.d_tw[inv][s], tw.data(), tw.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+      uint8_t** dst = ks ? &c.d_tw_ks : &c.d_tw[inv][s];
+      if (cudaMalloc(dst, tw.size()) != cudaSuccess ||
+          cudaMemcpy(*dst, tw.data(), tw.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
         set_error("twiddle upload failed");
         return 3;
       }
-      if (s == 0) {
+      if (s == 0 && !ks) {
         size_t bytes = w2.size() * 4;
         if (cudaMalloc(&c.d_w2[inv], bytes) != cudaSuccess ||
             cudaMalloc(&c.d_w2s[inv], bytes) != cudaSuccess ||
@@ -930,7 +949,12 @@ int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& m
   // stage 2: columns of W3 (k2), contraction over i2, rows (b, k1)
   a.in = P;
   a.out = out;
-  a.tw = c.d_tw[inverse][1];
+  // the key-switch MAC takes y 2^32 (Montgomery form) from the 2^64 table
+  if (a.epi.mode == EPI_KS_MAC && inverse) {
+    set_error("fused key-switch MAC needs a forward transform");
+    return 2;
+  }
+  a.tw = a.epi.mode == EPI_KS_MAC ? c.d_tw_ks : c.d_tw[inverse][1];
   a.tw_stride = c.tw_stride[1];
   a.R = c.n1;
   a.K = c.n2;

@@ -76,6 +76,7 @@ struct Ctx {
   // device tables
   PrimeConst* d_pc = nullptr;
   uint8_t* d_tw[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [inverse][stage]
+  uint8_t* d_tw_ks = nullptr;   // forward stage 2, x 2^64 (key-switch MAC epilogue)
   size_t tw_stride[2] = {0, 0};                                   // bytes per prime, per stage
   int kpad[2] = {0, 0}, npad[2] = {0, 0}, bn[2] = {0, 0};
   uint32_t* d_w2[2] = {nullptr, nullptr};   // [inverse] (prime, n1*n2) hadamard twiddles
