@@ -136,3 +136,27 @@ def test_level0_ops_vs_oracle(kind, batch):
     got = ctx.hrotate_batch(CiphertextBatch(d(c0), 0), 1, tk).data.cpu().numpy().view(np.uint32)
     rb, ra = O.hrotate(c0[0], c0[1], 1, basis, key, p.chain.q, p.chain.p, p.alpha, p.dnum)
     assert np.array_equal(got[0], rb) and np.array_equal(got[1], ra)
+
+
+@pytest.mark.parametrize("kind,level,batch", [("small", 5, 4), ("set_a", 1, 33),
+                                              ("set_b", 2, 5), ("n16", 3, 3),
+                                              ("p_dnum5", 12, 2)])
+def test_fused_hmult_rescale_batched(kind, level, batch):
+    """The fused HMULT+rescale equals rescale_batch(hmult_batch(.)) bit for bit
+    on multi-member batches (the golden cases above use one member)."""
+    import torch
+    from paper_2212_14191_b200.ckks import CiphertextBatch
+    ctx = _ctx(kind)
+    p = ctx.params
+    rng = np.random.default_rng(900 + level)
+    basis = tuple(p.chain.q[:level + 1])
+    c0 = np.stack([synth.rows(rng, basis, (batch, p.n)) for _ in range(2)])
+    c1 = np.stack([synth.rows(rng, basis, (batch, p.n)) for _ in range(2)])
+    key = synth.switching_key(rng, p.chain.q, p.chain.p, p.n, p.dnum)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()  # noqa
+    tk = d(key)
+    two = ctx.rescale_batch(ctx.hmult_batch(CiphertextBatch(d(c0), level),
+                                            CiphertextBatch(d(c1), level), tk))
+    one = ctx.hmult_rescale_batch(CiphertextBatch(d(c0), level), CiphertextBatch(d(c1), level), tk)
+    assert one.level == two.level == level - 1
+    assert torch.equal(one.data, two.data)
