@@ -267,8 +267,9 @@ def mod_down(x, x_basis, target, specials, threads=None):
     return out
 
 
-def key_switch(d, basis, key, chain_q, chain_p, alpha, dnum, threads=None):
-    """ckks.py:321-352.  d: (level+1, ..., n) NTT domain over `basis`."""
+def key_switch_acc(d, basis, key, chain_q, chain_p, alpha, dnum, threads=None):
+    """ckks.py:321-351: the key switch's inner-product accumulators over
+    ext = basis ++ specials, before ModDown."""
     basis = tuple(basis)
     level = len(basis) - 1
     ext = basis + tuple(chain_p)
@@ -288,6 +289,14 @@ def key_switch(d, basis, key, chain_q, chain_p, alpha, dnum, threads=None):
             ka = ka.reshape(kb.shape)
         acc_b = ele_add(acc_b, hada_mult(raised, kb, ext), ext)
         acc_a = ele_add(acc_a, hada_mult(raised, ka, ext), ext)
+    return acc_b, acc_a
+
+
+def key_switch(d, basis, key, chain_q, chain_p, alpha, dnum, threads=None):
+    """ckks.py:321-352.  d: (level+1, ..., n) NTT domain over `basis`."""
+    basis = tuple(basis)
+    acc_b, acc_a = key_switch_acc(d, basis, key, chain_q, chain_p, alpha, dnum, threads)
+    ext = basis + tuple(chain_p)
     return (mod_down(acc_b, ext, basis, tuple(chain_p), threads),
             mod_down(acc_a, ext, basis, tuple(chain_p), threads))
 
@@ -338,6 +347,50 @@ def hmult(b0, a0, b1, a1, basis, rlk, chain_q, chain_p, alpha, dnum, threads=Non
     d2 = hada_mult(a0, a1, basis)
     ksb, ksa = key_switch(d2, basis, rlk, chain_q, chain_p, alpha, dnum, threads)
     return ele_add(d0, ksb, basis), ele_add(d1, ksa, basis)
+
+
+def hmult_rescale_fused(b0, a0, b1, a1, basis, rlk, chain_q, chain_p, alpha, dnum,
+                        threads=None):
+    """The build's fused HMULT+rescale (capi.cu moddown_rescale) restated, so
+    the CPU suite can check its algebra against rescale(hmult(.)) (ckks.py
+    :265-274 then :291-311): with X_i = acc_i P^-1 + d_i, conv_i the converted
+    special rows and T = INTT_top(ModDown_top + d_top),
+        rescale_i = (X_i - NTT_i(conv_i P^-1 + T)) q_top^-1."""
+    basis = tuple(basis)
+    sp = tuple(chain_p)
+    ext = basis + sp
+    q_top = basis[-1]
+    d0 = hada_mult(b0, b1, basis)
+    d1 = ele_add(hada_mult(a0, b1, basis), hada_mult(a1, b0, basis), basis)
+    d2 = hada_mult(a0, a1, basis)
+    accs = key_switch_acc(d2, basis, rlk, chain_q, chain_p, alpha, dnum, threads)
+    big_p = 1
+    for r in sp:
+        big_p *= r
+    outs = []
+    for acc, dd in zip(accs, (d0, d1)):
+        conv = fast_basis_conv(intt(acc[len(basis):], sp, threads), sp, basis)
+        # the top row's ModDown alone, then its coefficient form
+        qq = np.uint64(q_top)
+        pinv = np.uint64(pow(big_p, -1, q_top))
+        y = ntt(conv[-1:], (q_top,), threads)[0].astype(np.uint64)
+        top = ((acc[len(basis) - 1].astype(np.uint64) + qq - y) % qq * pinv
+               + dd[-1].astype(np.uint64)) % qq
+        t = intt(top[None].astype(np.uint32), (q_top,), threads)[0].astype(np.uint64)
+        w = np.empty((len(basis) - 1,) + acc.shape[1:], dtype=np.uint32)
+        x = np.empty_like(w)
+        for i, q in enumerate(basis[:-1]):
+            qi = np.uint64(q)
+            pi = np.uint64(pow(big_p, -1, q))
+            x[i] = (acc[i].astype(np.uint64) * pi + dd[i].astype(np.uint64)) % qi
+            w[i] = (conv[i].astype(np.uint64) % qi * pi + t % qi) % qi
+        nw = ntt(w, basis[:-1], threads)
+        out = np.empty_like(w)
+        for i, q in enumerate(basis[:-1]):
+            qi = np.uint64(q)
+            out[i] = (x[i].astype(np.uint64) + qi - nw[i]) % qi * np.uint64(pow(q_top, -1, q)) % qi
+        outs.append(out)
+    return outs[0], outs[1]
 
 
 def rescale_poly(c, basis, threads=None):
