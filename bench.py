@@ -136,19 +136,52 @@ class ClockSampler:
 # ----------------------------------------------------------------------------
 
 def cpu_oracle_rate(primes, members, reps=1):
-    """limb-NTT/s of the C oracle (fwd + inv over len(primes) limbs x members)."""
+    """limb-NTT/s of the C oracle port (fwd + inv over len(primes) limbs x
+    members), in place on pre-reduced rows: only the OpenMP C kernel is timed
+    (no numpy upcast / copy / stack glue), every host thread."""
     from oracle import oracle as O
     threads = os.cpu_count() or 1
     O.THREADS = threads
     rng = np.random.default_rng(7)
     x = O.uniform_rows(rng, primes, (members, N))
-    O.ntt(x[:1, :1], primes[:1])           # build tables / warm the library
+    for q in primes:                       # build every prime's tables untimed
+        O._tables(q, N)
+    O.transform_inplace(x[:1, :1].copy(), primes[:1])
     t0 = time.perf_counter()
     for _ in range(reps):
-        f = O.ntt(x, primes)
-        O.intt(f, primes)
+        O.transform_inplace(x, primes)
+        O.transform_inplace(x, primes, inverse=True)
     dt = time.perf_counter() - t0
     return 2 * len(primes) * members * reps / dt, dt, threads
+
+
+def cpu_numpy_butterfly(primes, members_per_task=2, pool_tasks=None):
+    """The reference's own algorithm and cost profile: the numpy butterfly
+    restatement (oracle/butterfly_np.py, ref ntt.py:172-205 via
+    batch.batched_apply) on ONE host core, and over a multiprocessing.Pool of
+    every core mapping independent (limb, member-chunk) tasks (BASELINE.md
+    §2).  Returns {single_core, all_cores} limb-NTT/s with the core counts."""
+    import multiprocessing as mp
+    from oracle import butterfly_np as BF
+    cores = os.cpu_count() or 1
+    q = primes[0]
+    BF._plan(q, N)
+    t0 = time.perf_counter()
+    done = BF.fwd_inv_rows((q, N, members_per_task, 1))
+    one = done / (time.perf_counter() - t0)
+    tasks = [(primes[i % len(primes)], N, members_per_task, 100 + i)
+             for i in range(pool_tasks or 2 * cores)]
+    ctx = mp.get_context("spawn")   # the parent holds a CUDA context: never fork it
+    with ctx.Pool(cores) as pool:
+        pool.map(BF.fwd_inv_rows, tasks[:cores])          # warm: plans built per worker
+        t0 = time.perf_counter()
+        done = sum(pool.map(BF.fwd_inv_rows, tasks))
+        allc = done / (time.perf_counter() - t0)
+    return {"single_core": {"value": one / 1e3, "unit": UNIT, "cores": 1},
+            "all_cores": {"value": allc / 1e3, "unit": UNIT, "cores": cores,
+                          "sample": f"{len(tasks)} tasks x {members_per_task} members fwd+inv "
+                                    f"(N=2^16, p_default primes), Pool({cores})"},
+            "impl": "oracle/butterfly_np.py (numpy uint64 ufuncs, ref ntt.py:172-205)"}
 
 
 def headline_config(L, B, world, plan):
@@ -227,6 +260,9 @@ def run_b200(args):
     # with a gloo group, to exercise the N > 1 code path on a one-GPU box
     shared = os.environ.get("TFHE_BENCH_SHARED_GPU") == "1"
     local = 0 if shared else _env_int("LOCAL_RANK", 0)
+    if not shared and local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs GPU {local}, but only "
+                         f"{torch.cuda.device_count()} are visible (--gpus {world})")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -329,16 +365,44 @@ def run_b200(args):
                                  dtype=torch.int64).to(torch.int32)
         return t
 
-    def ckks_setup(prm, batch):
+    def ckks_setup(prm, batch, key=None):
         ck = CkksContext(prm, device=dev)
         e = tuple(prm.chain.q) + tuple(prm.chain.p)
-        key = rand_rows(e, (prm.dnum, 2, prm.n)).permute(1, 2, 0, 3).contiguous()
+        if key is None:
+            key = rand_rows(e, (prm.dnum, 2, prm.n)).permute(1, 2, 0, 3).contiguous()
         cts = [CiphertextBatch(rand_rows(prm.chain.q, (2, batch, prm.n)).transpose(0, 1)
                                .contiguous(), prm.l_max) for _ in range(2)]
         return ck, key, cts
 
+    # batched NTT batch sweep at the headline chain (BASELINE configs[1]
+    # "batch sweep on 1 B200"; ref cli.py:195-216 --batch-sizes): fwd+inv of
+    # (45, B, 2^16) for B = 1 .. 1024 (12 GiB per buffer at B = 1024)
+    bsweep = None
+    if args.batch_sweep:
+        bsweep = {}
+        bmax = 1024
+        flat = [torch.empty(L * bmax * N, dtype=torch.int32, device=dev) for _ in range(2)]
+        for i, q in enumerate(primes):     # uniform residues per limb, reused by every B
+            flat[0].view(L, bmax, N)[i] = torch.randint(0, q, (bmax, N), generator=g, device=dev,
+                                                        dtype=torch.int64).to(torch.int32)
+        bb = 1
+        while bb <= bmax:
+            xs = flat[0][:L * bb * N].view(L, bb, N)
+            fs = flat[1][:L * bb * N].view(L, bb, N)
+
+            def fwd_inv():
+                ctx.ntt(xs, primes, out=fs)
+                ctx.ntt(fs, primes, inverse=True, out=xs)
+            ms_b = timed(fwd_inv, max(3, min(50, 2048 // bb)))
+            bsweep[str(bb)] = {"limb_ntt_kops": 2 * L * bb * world / (ms_b / 1e3) / 1e3,
+                               "ms_per_step": ms_b}
+            bb *= 2
+        del flat, xs, fs
+        ctx._ws.clear()
+
     # CKKS operators at P-Default (configs[2..4]), same protocol
     hm = None
+    hm_check = None
     if args.hmult_batch > 0:
         Bh = args.hmult_batch
         ck, key, cts = ckks_setup(params, Bh)
@@ -360,7 +424,37 @@ def run_b200(args):
               "hmult_relin_only_per_s": rate(ms_hm_only), "hrotate_per_s": rate(ms_rot),
               "hrotate_ms_per_batch": ms_rot, "rescale_per_s": rate(ms_rs),
               "mixed_ct_per_s": rate(ms_mix), "mixed_ms_per_batch": ms_mix}
+        # parity spot check of the timed HMULT+relin+rescale (member 0) against
+        # the CPU oracle (ckks.py:265-274 then :291-311), rank 0, untimed
+        if args.hmult_check and rank == 0:
+            from oracle import oracle as O
+            O.THREADS = os.cpu_count() or 1
+            t0 = time.perf_counter()
+            got = ck.hmult_rescale_batch(cts[0], cts[1], key).data[:, :, 0].cpu().numpy() \
+                .view(np.uint32)
+            c0h = cts[0].data[:, :, 0].cpu().numpy().view(np.uint32)
+            c1h = cts[1].data[:, :, 0].cpu().numpy().view(np.uint32)
+            kh = key.cpu().numpy().view(np.uint32)
+            basis = tuple(params.chain.q)
+            hb, ha = O.hmult(c0h[0], c0h[1], c1h[0], c1h[1], basis, kh, params.chain.q,
+                             params.chain.p, params.alpha, params.dnum)
+            rb, ra = O.rescale(hb, ha, basis)
+            hm_check = {"member": 0, "exact": bool(np.array_equal(got[0], rb) and
+                                                   np.array_equal(got[1], ra)),
+                        "oracle_s": time.perf_counter() - t0}
+            del kh
+        # HMULT+relin+rescale batch sweep (same key, fresh ciphertexts)
+        hsw = {str(Bh): rate(ms_hm)}
+        for bs in (8, 32):
+            if bs >= Bh:
+                continue
+            _, _, cs = ckks_setup(params, bs, key)
+            ms_b = timed(lambda: ck.hmult_rescale_batch(cs[0], cs[1], key), hsteps)
+            hsw[str(bs)] = bs * world / (ms_b / 1e3)
+            del cs
+        hm["batch_sweep_per_s"] = dict(sorted(hsw.items(), key=lambda kv: int(kv[0])))
         del ck, key, cts
+        ctx._ws.clear()
 
     # dnum-reduced P-Default (alpha = K = 9): ModUp/ModDown are 9-term base
     # conversions on the tensor cores (tfhe_bconv) between the NTTs
@@ -591,19 +685,22 @@ def run_b200(args):
                          "hmult_then_rescale_per_s": hm["hmult_then_rescale_per_s"],
                          "api": "CkksContext.hmult_rescale_batch (fused ModDown+rescale)",
                          "rescale_per_s": hm["rescale_per_s"]}
-        # whole-operator roofline: int8 tensor work of the limb transforms the
-        # fused HMULT+relin+rescale runs (INTT l+1, ModUp (l+1)(l+1+K) incl. the
-        # skipped own-slice raises, ModDown INTT 2K, top-row NTT 2 + INTT 2,
-        # merged ModDown/rescale NTT 2l) -- 2l fewer than ModDown then rescale
-        l1 = L
-        transforms = l1 + l1 * (l1 + len(params.chain.p)) + 2 * len(params.chain.p) + 2 \
-            + 2 + 2 * (l1 - 1)
+        # whole-operator roofline: int8 tensor work of the limb transforms an
+        # HMULT+relin+rescale needs ALGORITHMICALLY (INTT l+1, ModUp raises of
+        # each one-limb slice to the l+K other ext primes, ModDown INTT 2K,
+        # top-row NTT 2 + INTT 2, merged ModDown/rescale NTT 2l); the device
+        # also computes the l+1 own-slice raises it then skips (not counted)
+        l1, K = L, len(params.chain.p)
+        transforms = l1 + l1 * (l1 - 1 + K) + 2 * K + 2 + 2 + 2 * (l1 - 1)
+        computed = transforms + l1
         hm_tops = hm["hmult_kops"] * 1e3 * transforms * ops_per_limb / 1e12
+        line["hmult"]["batch_sweep_per_s"] = hm["batch_sweep_per_s"]
+        line["hmult"]["parity_spot_check"] = hm_check
         line["hmult"]["roofline"] = {
             "bound": "tensor", "achieved": hm_tops, "peak": peak, "unit": "TOPS (int8)",
             "frac": hm_tops / peak,
             "algorithmic": f"{transforms} limb-transforms x {ops_per_limb / 1e9:.3f} G int8-ops "
-                           "per HMULT+relin+rescale"}
+                           f"per HMULT+relin+rescale ({computed} computed)"}
         line["hrotate"] = {"workload": f"HROTATE r=1 (automorphism + keyswitch), N=2^16, {PRESET}"
                                        f", batch {hm['batch_per_gpu']} per GPU (configs[3])",
                            "ops_per_s": hm["hrotate_per_s"],
@@ -618,6 +715,10 @@ def run_b200(args):
         line["p_dnum5"] = d5
     if sweep:
         line["ntt_sweep"] = sweep
+    if bsweep:
+        line["batch_sweep"] = {"workload": f"fwd+inv NTT, N=2^16, {PRESET} chain ({L} limbs), "
+                                           "batch B per GPU (BASELINE configs[1] sweep)",
+                               "unit": UNIT, "by_batch": bsweep}
     if hbm:
         hpeak, hsrc = 6546.6, "fallback (B200_PROFILING.md)"
         try:
@@ -632,12 +733,51 @@ def run_b200(args):
         r, dt, threads = rates
         line["cpu_baseline"] = {
             "value": r / 1e3, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"C oracle (oracle/tfhe_oracle.c), fwd+inv over {L} limbs x "
-                      f"{args.cpu_members} members ({2 * L * args.cpu_members} limb-NTTs) "
-                      f"in {dt:.1f}s"}
+            "sample": f"C oracle (oracle/tfhe_oracle.c, OpenMP, in place), fwd+inv over {L} "
+                      f"limbs x {args.cpu_members} members ({2 * L * args.cpu_members} "
+                      f"limb-NTTs) in {dt:.1f}s"}
+        if args.cpu_numpy:
+            try:
+                line["cpu_baseline"]["python_reference_algorithm"] = cpu_numpy_butterfly(primes)
+            except Exception as exc:   # never lose the bench line to the extra leg
+                line["cpu_baseline"]["python_reference_algorithm"] = {"error": str(exc)[:200]}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def launch_ranks(args):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) with
+    torch.distributed.run on 127.0.0.1, the same command line the driver
+    uses, and pass rank 0's JSON line through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "8"))
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args):
+    """--dry-run: rank plumbing only (no GPU work): every rank joins the
+    process group and rank 0 prints the ranks it sees (tests run it on CPU
+    with gloo)."""
+    import torch.distributed as dist
+    rank, world = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1)
+    ranks = [{"rank": rank, "local_rank": _env_int("LOCAL_RANK", 0), "pid": os.getpid()}]
+    if world > 1:
+        dist.init_process_group("gloo")
+        got = [None] * world
+        dist.all_gather_object(got, ranks[0])
+        ranks = got
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "requested": args.gpus,
+                          "ranks": ranks}), flush=True)
     return 0
 
 
@@ -648,13 +788,21 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--batch", type=int, default=128)
-    ap.add_argument("--hmult-batch", type=int, default=32)
+    ap.add_argument("--hmult-batch", type=int, default=128)
     ap.add_argument("--cpu-members", type=int, default=32)
     ap.add_argument("--set-a-batch", type=int, default=4096)
     ap.add_argument("--hbm-kernels", type=int, default=1)
     ap.add_argument("--dnum5-batch", type=int, default=16)
     ap.add_argument("--sweep", type=int, default=1)
+    ap.add_argument("--batch-sweep", type=int, default=1)
+    ap.add_argument("--hmult-check", type=int, default=1)
+    ap.add_argument("--cpu-numpy", type=int, default=1)
+    ap.add_argument("--dry-run", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args)
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

@@ -131,6 +131,20 @@ def ntt(rows, basis, threads=None) -> np.ndarray:
         if len(basis) else rows.copy()
 
 
+def transform_inplace(rows, basis, inverse: bool = False, threads=None) -> np.ndarray:
+    """In-place per-limb transform of a C-contiguous uint32 (L, ..., n) array
+    whose rows are already reduced mod their prime: the C kernel only, no
+    upcast / copy / stack glue (the CPU-baseline timing path)."""
+    if rows.dtype != np.uint32 or not rows.flags.c_contiguous:
+        raise ValueError("transform_inplace needs a C-contiguous uint32 array")
+    n = rows.shape[-1]
+    per = rows[0].size // n if len(basis) else 0
+    for i, q in enumerate(basis):
+        lib().orc_ntt_rows(_p(rows[i]), per, n.bit_length() - 1, q, _p(_tables(q, n)),
+                           int(inverse), THREADS if threads is None else threads)
+    return rows
+
+
 def intt(rows, basis, threads=None) -> np.ndarray:
     rows = np.asarray(rows, dtype=np.uint32)
     return np.stack([transform_rows(rows[i], q, True, threads) for i, q in enumerate(basis)]) \

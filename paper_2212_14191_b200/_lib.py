@@ -23,6 +23,8 @@ EINVAL = 2
 ECUDA = 3
 
 OP_ADD, OP_SUB, OP_MUL, OP_NEG, OP_SCALAR = 0, 1, 2, 3, 4
+#: widest base conversion one device launch takes (csrc/poly_ops.h kMaxBconvSrc)
+MAX_BCONV_SRC = 16
 
 _u32p = ctypes.POINTER(ctypes.c_uint32)
 _i32p = ctypes.POINTER(ctypes.c_int32)

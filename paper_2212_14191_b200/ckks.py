@@ -21,6 +21,8 @@ chain.q ++ chain.p) are accepted directly too.
 
 from __future__ import annotations
 
+import weakref
+from collections import OrderedDict
 from dataclasses import dataclass
 from fractions import Fraction
 
@@ -102,7 +104,18 @@ class CkksContext(ClientMixin):
                                      n_special=len(params.chain.p), device=device)
         self.table = TwiddleTable(params.n, self.ext_basis)
         self.table._ctx = self.dev
-        self._keys = {}
+        # device copies of host switching keys: a small LRU keyed by the host
+        # object's id, evicted when the host key is garbage-collected
+        self._keys = OrderedDict()
+        self.max_cached_keys = 4
+        # the device path's limits (poly_ops.h): base conversions of at most
+        # kMaxBconvSrc sources, primes below 2^31 (tfhe_ctx_create)
+        if max(params.alpha, len(params.chain.p)) > _lib.MAX_BCONV_SRC:
+            raise ParameterError(
+                f"alpha={params.alpha} / K={len(params.chain.p)}: the device base conversion "
+                f"takes at most {_lib.MAX_BCONV_SRC} source limbs")
+        if max(self.ext_basis) >= 1 << 31:
+            raise ParameterError("the device path needs primes below 2^31")
 
     # -- transforms -----------------------------------------------------------
     def to_ntt(self, poly):
@@ -117,7 +130,8 @@ class CkksContext(ClientMixin):
         if isinstance(swk, torch.Tensor):
             return swk
         hit = self._keys.get(id(swk))
-        if hit is not None and hit[0] is swk:
+        if hit is not None and hit[0]() is swk:
+            self._keys.move_to_end(id(swk))
             return hit[1]
         p = self.params
         if isinstance(swk, SwitchingKey):
@@ -130,7 +144,14 @@ class CkksContext(ClientMixin):
         else:
             arr = np.asarray(swk, dtype=np.uint32)
         t, _ = to_device(arr, self.dev.device)
-        self._keys[id(swk)] = (swk, t)
+        try:
+            ref = weakref.ref(swk)
+            weakref.finalize(swk, self._keys.pop, id(swk), None)
+        except TypeError:   # not weak-referenceable (e.g. a list): do not cache
+            return t
+        self._keys[id(swk)] = (ref, t)
+        while len(self._keys) > self.max_cached_keys:
+            self._keys.popitem(last=False)
         return t
 
     def _ct_tensor(self, ct):
@@ -269,23 +290,47 @@ class CkksContext(ClientMixin):
         """d: (level+1, B, N) NTT domain -> (2, level+1, B, N) = (ksb, ksa)."""
         return self.dev.keyswitch(d, level, self.device_key(swk), self.params.dnum, out=out)
 
-    def hadd_batch(self, c0: CiphertextBatch, c1: CiphertextBatch):
-        rows = self.params.q_basis(c0.level) * 2
-        d = self.dev.eltwise(_lib.OP_ADD, c0.data, c1.data, rows)
-        return CiphertextBatch(data=d, level=c0.level, scale=c0.scale)
+    def _binary_batch(self, op, c0: CiphertextBatch, c1: CiphertextBatch):
+        """ele_add / ele_sub of both components of every member: one launch
+        over the (2 (level+1), B, N) rows, row i mod q_{i mod (level+1)}."""
+        if c0.level != c1.level or c0.data.shape != c1.data.shape:
+            raise ParameterError("batch operands must match in level and shape")
+        if c0.scale != c1.scale:
+            raise ParameterError("ciphertext scales differ")
+        basis = self.params.q_basis(c0.level)
+        l1, B, n = len(basis), c0.batch_size, c0.n
+        if tuple(c0.data.shape) != (2, l1, B, n):
+            raise ParameterError("ciphertext batch must be (2, level+1, B, N)")
+        a = c0.data.reshape(2 * l1, B, n)
+        b = c1.data.reshape(2 * l1, B, n)
+        d = self.dev.eltwise(op, a, b, basis * 2)
+        return CiphertextBatch(data=d.view(2, l1, B, n), level=c0.level, scale=c0.scale)
 
-    def cmult_batch(self, cb: CiphertextBatch, pt):
+    def hadd_batch(self, c0: CiphertextBatch, c1: CiphertextBatch):
+        """hadd (ref `ckks.py:246-250`) of every member."""
+        return self._binary_batch(_lib.OP_ADD, c0, c1)
+
+    def hsub_batch(self, c0: CiphertextBatch, c1: CiphertextBatch):
+        """hsub (ref `ckks.py:252-256`) of every member."""
+        return self._binary_batch(_lib.OP_SUB, c0, c1)
+
+    def cmult_batch(self, cb: CiphertextBatch, pt, pt_scale=None):
         """Plaintext product (ref `ckks.py:258-263`) of every member: pt is a
         (level+1, B, N) NTT-domain tensor (one plaintext per member) or a
-        single `Plaintext` / (level+1, N) tensor shared by the batch."""
+        single `Plaintext` / (level+1, N) tensor shared by the batch.  A raw
+        tensor carries no scale, so `pt_scale` is required with it (the result
+        scale is cb.scale * pt_scale, as the reference's)."""
         basis = self.params.q_basis(cb.level)
         l1, B, n = len(basis), cb.batch_size, cb.n
-        scale = cb.scale
         if isinstance(pt, Plaintext):
             if pt.level != cb.level:
                 raise ParameterError("plaintext level does not match ciphertext")
             scale = cb.scale * pt.scale
             pt = pt.poly.rows
+        else:
+            if pt_scale is None:
+                raise ParameterError("cmult_batch of a raw plaintext tensor needs pt_scale")
+            scale = cb.scale * Fraction(pt_scale)
         t, _ = to_device(pt, self.dev.device)
         if tuple(t.shape) == (l1, n):
             t = t.unsqueeze(1).expand(l1, B, n).contiguous()
@@ -296,7 +341,3 @@ class CkksContext(ClientMixin):
             self.dev.eltwise(_lib.OP_MUL, cb.data[c], t, basis, out=out[c])
         return CiphertextBatch(data=out, level=cb.level, scale=scale)
 
-    def hsub_batch(self, c0: CiphertextBatch, c1: CiphertextBatch):
-        rows = self.params.q_basis(c0.level) * 2
-        d = self.dev.eltwise(_lib.OP_SUB, c0.data, c1.data, rows)
-        return CiphertextBatch(data=d, level=c0.level, scale=c0.scale)

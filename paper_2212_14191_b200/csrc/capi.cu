@@ -3,6 +3,7 @@
 // product / ModDown, hmult, rescale, hrotate) on top of the kernels in
 // ntt_tc.cu and poly_ops.cu.  Everything is stream-ordered; no host syncs.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -101,6 +102,12 @@ void set_group(CkksGeom& g, const Ctx& c, int batch) {
   const size_t cap = (size_t)8 << 30;
   int s_mem = (int)std::max<size_t>(1, cap / (row_bytes * g.T));
   g.S = std::max(1, std::min({g.nslices, kMaxLimbs / g.T, s_mem}));
+  // test knob: TFHE_KS_MAX_S caps the group size so small goldens also run the
+  // multi-group path (every group after the first re-reads the accumulator)
+  if (const char* e = getenv("TFHE_KS_MAX_S")) {
+    const int cap_s = atoi(e);
+    if (cap_s > 0) g.S = std::min(g.S, cap_s);
+  }
 }
 
 // prime index of target t (local chain rows, then specials)

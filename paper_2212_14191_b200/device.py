@@ -109,7 +109,7 @@ class DeviceContext:
         n1, n2 = ctypes.c_int(), ctypes.c_int()
         self.lib.tfhe_ctx_plan(self.handle, ctypes.byref(n1), ctypes.byref(n2))
         self.plan = (n1.value, n2.value)
-        self._ws = None
+        self._ws = {}          # stream handle -> byte workspace
         self._staging = None
 
     def __del__(self):
@@ -151,12 +151,18 @@ class DeviceContext:
             raise ParameterError(f"no twiddles prepared for prime {e.args[0]}") from None
 
     def workspace(self, nbytes: int) -> torch.Tensor:
-        """Cached byte workspace (grown on demand, reused across calls)."""
+        """Byte workspace of the CURRENT stream (grown on demand, reused by the
+        calls stream-ordered behind each other).  Every operator enqueues on
+        the current stream, so ops issued on different streams (threads or
+        `torch.cuda.stream` scopes) get disjoint scratch and cannot race."""
         nbytes = max(int(nbytes), 256)
-        if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = None
-            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        return self._ws
+        key = torch.cuda.current_stream(self.device).cuda_stream
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < nbytes:
+            self._ws.pop(key, None)
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
+        return ws
 
     def empty(self, *shape):
         return torch.empty(shape, dtype=torch.int32, device=self.device)

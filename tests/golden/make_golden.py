@@ -123,6 +123,29 @@ def make_ntt_large(doc):
         json.dump(rec, fh, indent=1)
 
 
+def add_ntt_large_all():
+    """Record every prime of primes_{n} (incl. the 31-bit qs[4]) at 2^13..2^16,
+    keeping the existing records (test_acceptance.py:97-121 sweeps them all)."""
+    with open(os.path.join(HERE, "params.json")) as fh:
+        doc = json.load(fh)
+    path = os.path.join(HERE, "ntt_large.json")
+    with open(path) as fh:
+        rec = json.load(fh)
+    for n in (1 << 13, 1 << 14, 1 << 15, 1 << 16):
+        qs = doc["adhoc"][f"primes_{n}"]["q"]
+        table = RN.TwiddleTable(n, qs)
+        for q in qs:
+            if f"{n}_{q}" in rec:
+                continue
+            x = synth.ntt_rows(n, q, rows=2)
+            f = RN.transform_rows(x, q, table, "butterfly").astype(np.uint32)
+            i = RN.transform_rows(x, q, table, "butterfly", inverse=True).astype(np.uint32)
+            rec[f"{n}_{q}"] = {"fwd": sha(f), "inv": sha(i),
+                               "fwd_head": f[0, :8].tolist(), "inv_head": i[0, :8].tolist()}
+    with open(path, "w") as fh:
+        json.dump(rec, fh, indent=1)
+
+
 def make_kernels(doc):
     n = 64
     basis = tuple(doc["adhoc"]["primes_64"]["q"][:3])
@@ -219,6 +242,15 @@ LARGE_CASES = [
     # dnum-reduced N=2^16 set (alpha = K = 9): 9-term tensor-core base
     # conversions in ModUp and ModDown; level 12 = one full + one ragged slice
     ("p_dnum5_l12", p_dnum5, 12, 26),
+    # the bench's own configuration: P-Default at the top level (45 one-limb
+    # GKS slices, so the device key switch runs several slice groups)
+    ("p_default_l44", p_default, 44, 27),
+    # 31-bit primes through the large-n (n1 >= 128) tensor-core path: the
+    # tightest lazy [0, 2q) intermediates (params.py:17-19)
+    ("n16_31b_l3", lambda: RP.CkksParams.generate(n=1 << 16, l_max=3, k=1, dnum=4, bit_size=31),
+     3, 28),
+    ("n14_31b_l5", lambda: RP.CkksParams.generate(n=1 << 14, l_max=5, k=2, dnum=3, bit_size=31),
+     5, 29),
 ]
 
 
@@ -335,6 +367,9 @@ if __name__ == "__main__":
         doc["presets"]["p_dnum5"] = chain_doc(p_dnum5())
         with open(path, "w") as fh:
             json.dump(doc, fh, indent=1)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "ntt-large-all":
+        add_ntt_large_all()
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "client":
         make_client()

@@ -129,7 +129,7 @@ def test_oracle_ntt_golden(n, ntt_small, golden_params):
 def test_oracle_ntt_golden_large(n, golden_params):
     with open(os.path.join(GOLDEN, "ntt_large.json")) as fh:
         rec = json.load(fh)
-    for q in golden_params["adhoc"][f"primes_{n}"]["q"][:3]:
+    for q in golden_params["adhoc"][f"primes_{n}"]["q"]:   # incl. the 31-bit qs[4]
         x = synth.ntt_rows(n, q, rows=2)
         assert _sha(O.transform_rows(x, q)) == rec[f"{n}_{q}"]["fwd"]
         assert _sha(O.transform_rows(x, q, inverse=True)) == rec[f"{n}_{q}"]["inv"]
@@ -200,6 +200,16 @@ def test_oracle_ckks_golden_n16():
         assert _sha(arr) == rec[op]["sha256"], op
 
 
+def test_oracle_ckks_golden_31bit():
+    """A 31-bit chain (the tightest lazy bounds) at n = 2^14: the oracle
+    reproduces the reference's outputs recorded in ckks_large.json."""
+    with open(os.path.join(GOLDEN, "ckks_large.json")) as fh:
+        rec = json.load(fh)["n14_31b_l5"]
+    p = P.CkksParams.generate(n=1 << 14, l_max=5, k=2, dnum=3, bit_size=31)
+    for op, arr in _oracle_ops(p, 5, 29).items():
+        assert _sha(arr) == rec[op]["sha256"], op
+
+
 def test_oracle_batched_equals_per_member():
     # batched (L, B, n) oracle calls equal the per-member calls (batch.py:78)
     p = P.CkksParams.from_preset("set_a")
@@ -214,3 +224,16 @@ def test_oracle_batched_equals_per_member():
         b1, a1 = O.hmult(c[0][:, m], c[1][:, m], c[2][:, m], c[3][:, m], basis, key, basis,
                          tuple(p.chain.p), p.alpha, p.dnum)
         assert np.array_equal(hb[:, m], b1) and np.array_equal(ha[:, m], a1)
+
+
+@pytest.mark.parametrize("n", [16, 256, 4096])
+def test_numpy_butterfly_restatement_matches_goldens(n, golden_params):
+    """oracle/butterfly_np.py (the numpy restatement bench.py times as the
+    Python reference's cost profile) reproduces the reference's butterfly
+    outputs recorded in ntt_small.npz."""
+    from oracle import butterfly_np as BF
+    small = np.load(os.path.join(GOLDEN, "ntt_small.npz"))
+    for q in golden_params["adhoc"][f"primes_{n}"]["q"]:
+        x = small[f"x_{n}_{q}"]
+        assert np.array_equal(BF.forward(x, q).astype(np.uint32), small[f"fwd_{n}_{q}"])
+        assert np.array_equal(BF.inverse(x, q).astype(np.uint32), small[f"inv_{n}_{q}"])

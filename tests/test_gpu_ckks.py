@@ -23,7 +23,15 @@ SMALL = [("small_full", "small", 5, 11), ("small_l4", "small", 4, 12),
          ("set_a_full", "set_a", 1, 15), ("set_b_full", "set_b", 2, 16)]
 LARGE = [("n16_l3", "n16", 3, 21), ("resnet20_l3", "resnet20", 3, 22),
          ("set_c_full", "set_c", 7, 23), ("set_c_l4", "set_c", 4, 24),
-         ("set_c_l2", "set_c", 2, 25), ("p_dnum5_l12", "p_dnum5", 12, 26)]
+         ("set_c_l2", "set_c", 2, 25), ("p_dnum5_l12", "p_dnum5", 12, 26),
+         # the bench configuration (P-Default, level 44: 45 one-limb slices in
+         # several key-switch groups) and 31-bit chains on the large-n path
+         ("p_default_l44", "p_default", 44, 27), ("n16_31b_l3", "n16_31b", 3, 28),
+         ("n14_31b_l5", "n14_31b", 5, 29)]
+# cases rerun with the key-switch group size capped (TFHE_KS_MAX_S), so the
+# multi-group path (accumulator re-read between groups) meets every shape
+MULTIGROUP = [c for c in LARGE if c[0] in ("n16_l3", "resnet20_l3", "set_c_full", "set_c_l4",
+                                           "p_dnum5_l12", "n14_31b_l5")]
 
 
 def _params(kind):
@@ -32,6 +40,10 @@ def _params(kind):
         return CkksParams.generate(n=256, l_max=5, k=3, dnum=3, bit_size=30)
     if kind == "n16":
         return CkksParams.generate(n=1 << 16, l_max=3, k=1, dnum=4, bit_size=28)
+    if kind == "n16_31b":
+        return CkksParams.generate(n=1 << 16, l_max=3, k=1, dnum=4, bit_size=31)
+    if kind == "n14_31b":
+        return CkksParams.generate(n=1 << 14, l_max=5, k=2, dnum=3, bit_size=31)
     return CkksParams.from_preset(kind)
 
 
@@ -101,15 +113,76 @@ def test_ckks_ops_golden_small(case, kind, level, seed, ckks_small):
         assert np.array_equal(arr, want), (case, op)
 
 
+def _sha(arr):
+    return hashlib.sha256(np.ascontiguousarray(arr, dtype=np.uint32).tobytes()).hexdigest()
+
+
+def _large_rec(case):
+    with open(os.path.join(GOLDEN, "ckks_large.json")) as fh:
+        return json.load(fh)[case]
+
+
 @pytest.mark.parametrize("case,kind,level,seed", LARGE)
 def test_ckks_ops_golden_large(case, kind, level, seed):
-    with open(os.path.join(GOLDEN, "ckks_large.json")) as fh:
-        rec = json.load(fh)[case]
+    rec = _large_rec(case)
     got = _run(kind, level, seed)
     for op, arr in got.items():
-        h = hashlib.sha256(np.ascontiguousarray(arr, dtype=np.uint32).tobytes()).hexdigest()
         assert arr.reshape(-1)[:8].tolist() == rec[op]["head"], (case, op)
-        assert h == rec[op]["sha256"], (case, op)
+        assert _sha(arr) == rec[op]["sha256"], (case, op)
+
+
+@pytest.mark.parametrize("cap", [1, 2, 3])
+@pytest.mark.parametrize("case,kind,level,seed", MULTIGROUP)
+def test_ckks_ops_golden_multigroup(case, kind, level, seed, cap, monkeypatch):
+    """The same goldens with at most `cap` GKS slices per fused key-switch
+    group: groups after the first accumulate onto the stored accumulator
+    (capi.cu keyswitch_impl, init_acc), ragged last groups included."""
+    monkeypatch.setenv("TFHE_KS_MAX_S", str(cap))
+    rec = _large_rec(case)
+    got = _run(kind, level, seed)
+    for op, arr in got.items():
+        assert _sha(arr) == rec[op]["sha256"], (case, op, cap)
+
+
+def test_p_default_l44_batch_vs_golden_and_oracle():
+    """The bench configuration itself: P-Default at level 44 (45 one-limb GKS
+    slices; the key switch runs ceil(45 / S) groups), a 2-member batch through
+    the batched operators.  Member 0 carries the golden inputs and must match
+    the reference's outputs; member 1 is fresh and must match the oracle."""
+    import torch
+    from oracle import oracle as O
+    from paper_2212_14191_b200.ckks import CiphertextBatch
+    ctx = _ctx("p_default")
+    p = ctx.params
+    level = p.l_max
+    ins = synth.ckks_inputs(p.chain.q, p.chain.p, p.n, p.dnum, level, 27)
+    basis = tuple(p.chain.q[:level + 1])
+    rng = np.random.default_rng(2727)
+    m1 = {k: synth.rows(rng, basis, (p.n,)) for k in ("b0", "a0", "b1", "a1")}
+    ct = lambda b, a: np.stack([np.stack([ins[b], m1[b]], 1),   # noqa: E731
+                                np.stack([ins[a], m1[a]], 1)])
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()  # noqa: E731
+    c0 = CiphertextBatch(d(ct("b0", "a0")), level)
+    c1 = CiphertextBatch(d(ct("b1", "a1")), level)
+    rlk, rk = d(ins["rlk"]), d(ins["rotk"])
+    host = lambda t: t.data.cpu().numpy().view(np.uint32) if hasattr(t, "data") \
+        else t.cpu().numpy().view(np.uint32)                   # noqa: E731
+    hr = host(ctx.hmult_rescale_batch(c0, c1, rlk))
+    hm = host(ctx.hmult_batch(c0, c1, rlk))
+    ro = host(ctx.hrotate_batch(c0, 1, rk))
+    ks = host(ctx.key_switch_batch(c0.data[1], level, rlk))
+    rec = _large_rec("p_default_l44")
+    for name, arr in (("hmult_rescale", hr), ("hmult", hm), ("hrotate_1", ro),
+                      ("keyswitch", ks)):
+        assert _sha(arr[:, :, 0]) == rec[name]["sha256"], name
+    hb, ha = O.hmult(m1["b0"], m1["a0"], m1["b1"], m1["a1"], basis, ins["rlk"], p.chain.q,
+                     p.chain.p, p.alpha, p.dnum)
+    assert np.array_equal(hm[0, :, 1], hb) and np.array_equal(hm[1, :, 1], ha), "hmult"
+    rb, ra = O.rescale(hb, ha, basis)
+    assert np.array_equal(hr[0, :, 1], rb) and np.array_equal(hr[1, :, 1], ra), "hmult_rescale"
+    ob, oa = O.hrotate(m1["b0"], m1["a0"], 1, basis, ins["rotk"], p.chain.q, p.chain.p,
+                       p.alpha, p.dnum)
+    assert np.array_equal(ro[0, :, 1], ob) and np.array_equal(ro[1, :, 1], oa), "hrotate"
 
 
 @pytest.mark.parametrize("kind,batch", [("small", 3), ("n16", 2), ("set_c", 1)])

@@ -83,11 +83,39 @@ def test_cmult_batch_vs_oracle():
     ct = np.stack([O.uniform_rows(rng, basis, (3, p.n)) for _ in range(2)])
     pt = O.uniform_rows(rng, basis, (3, p.n))
     d = lambda a: torch.from_numpy(a.view(np.int32)).cuda()  # noqa: E731
-    got = ck.cmult_batch(CiphertextBatch(d(ct), p.l_max), d(pt)).data.cpu().numpy().view(np.uint32)
+    got = ck.cmult_batch(CiphertextBatch(d(ct), p.l_max), d(pt), pt_scale=3).data.cpu().numpy().view(np.uint32)
     for c in range(2):
         assert np.array_equal(got[c], O.hada_mult(ct[c], pt, basis))
     shared = pt[:, 0]
-    got = ck.cmult_batch(CiphertextBatch(d(ct), p.l_max), d(np.ascontiguousarray(shared)))
-    got = got.data.cpu().numpy().view(np.uint32)
+    cb = ck.cmult_batch(CiphertextBatch(d(ct), p.l_max, scale=5), d(np.ascontiguousarray(shared)),
+                        pt_scale=3)
+    assert cb.scale == 15
+    got = cb.data.cpu().numpy().view(np.uint32)
     for c in range(2):
         assert np.array_equal(got[c], O.hada_mult(ct[c], shared[:, None, :], basis))
+
+
+def test_hadd_hsub_batch_vs_oracle():
+    """hadd_batch / hsub_batch reduce every limb of both components mod its
+    own prime (ref `ckks.py:246-256`), and reject mismatched operands."""
+    from oracle import oracle as O
+    from paper_2212_14191_b200.ckks import CiphertextBatch, CkksContext
+    from paper_2212_14191_b200.errors import ParameterError
+    from paper_2212_14191_b200.params import CkksParams
+    p = CkksParams.from_preset("default")
+    ck = CkksContext(p)
+    rng = np.random.default_rng(8)
+    basis = p.q_basis(p.l_max)
+    c0 = np.stack([O.uniform_rows(rng, basis, (3, p.n)) for _ in range(2)])
+    c1 = np.stack([O.uniform_rows(rng, basis, (3, p.n)) for _ in range(2)])
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()  # noqa: E731
+    b0, b1 = CiphertextBatch(d(c0), p.l_max), CiphertextBatch(d(c1), p.l_max)
+    add = ck.hadd_batch(b0, b1).data.cpu().numpy().view(np.uint32)
+    sub = ck.hsub_batch(b0, b1).data.cpu().numpy().view(np.uint32)
+    for c in range(2):
+        assert np.array_equal(add[c], O.ele_add(c0[c], c1[c], basis))
+        assert np.array_equal(sub[c], O.ele_sub(c0[c], c1[c], basis))
+    with pytest.raises(ParameterError):
+        ck.hadd_batch(b0, CiphertextBatch(d(c1[:, :-1]), p.l_max - 1))
+    with pytest.raises(ParameterError):
+        ck.hsub_batch(b0, CiphertextBatch(d(c1), p.l_max, scale=3))

@@ -44,7 +44,9 @@ def test_transform_rows_golden_large(n, golden_params):
     from paper_2212_14191_b200 import ntt
     with open(os.path.join(GOLDEN, "ntt_large.json")) as fh:
         rec = json.load(fh)
-    qs = golden_params["adhoc"][f"primes_{n}"]["q"][:3]
+    # every prime of the sweep, incl. the 31-bit qs[4] where the lazy [0, 2q)
+    # intermediates are tightest (ref test_acceptance.py:97-121)
+    qs = golden_params["adhoc"][f"primes_{n}"]["q"]
     table = ntt.TwiddleTable(n, qs)
     for q in qs:
         x = synth.ntt_rows(n, q, rows=2)
@@ -61,7 +63,7 @@ def test_batched_multilimb_vs_oracle(n, batch):
     import torch
     from paper_2212_14191_b200.device import DeviceContext
     primes = __import__("paper_2212_14191_b200.params", fromlist=["x"]).generate_primes(
-        n, [29, 28, 30, 27, 26])
+        n, [29, 31, 30, 27, 26])
     ctx = DeviceContext.get(n, primes)
     rng = np.random.default_rng(n + batch)
     x = O.uniform_rows(rng, primes, (batch, n))
@@ -100,3 +102,35 @@ def test_batched_apply_host_streaming(n, batch, rows, kind):
     b = batched_apply(f, "intt", table=table)
     bh = b.data.numpy().view(np.uint32) if kind == "pinned" else b.data
     assert np.array_equal(bh, x)
+
+
+@pytest.mark.parametrize("n,batch", [(1 << 12, 5), (1 << 16, 3)])
+def test_batched_apply_eltwise_and_frobenius_vs_oracle(n, batch):
+    """The non-transform kernels of batched_apply (ref batch.py:98-127):
+    hada_mult / ele_add / ele_sub against a second buffer and forbenius_map
+    (NTT-domain automorphism) on device and host buffers, against the oracle."""
+    import torch
+    from paper_2212_14191_b200.batch import BatchBuffer, batched_apply
+    from paper_2212_14191_b200.ntt import TwiddleTable
+    from paper_2212_14191_b200.params import generate_primes
+    primes = generate_primes(n, [31, 29, 28])
+    table = TwiddleTable(n, primes)
+    rng = np.random.default_rng(n + 17 * batch)
+    x = O.uniform_rows(rng, primes, (batch, n))
+    y = O.uniform_rows(rng, primes, (batch, n))
+    want = {"hada_mult": O.hada_mult(x, y, primes), "ele_add": O.ele_add(x, y, primes),
+            "ele_sub": O.ele_sub(x, y, primes)}
+    for kind in ("numpy", "device"):
+        conv = (lambda a: a) if kind == "numpy" else \
+            (lambda a: torch.from_numpy(a.view(np.int32)).cuda())   # noqa: E731
+        back = (lambda a: a) if kind == "numpy" else \
+            (lambda a: a.cpu().numpy().view(np.uint32))             # noqa: E731
+        bx = BatchBuffer(data=conv(x), basis=primes, domain="ntt")
+        by = BatchBuffer(data=conv(y), basis=primes, domain="ntt")
+        for op, w in want.items():
+            got = batched_apply(bx, op, aux=by, table=table)
+            assert np.array_equal(back(got.data), w), (kind, op)
+        for r in (1, 3, -1):
+            t = O.galois_element(r, n)
+            got = batched_apply(bx, "forbenius_map", aux=r, table=table)
+            assert np.array_equal(back(got.data), O.apply_automorphism(x, t, primes)), (kind, r)
