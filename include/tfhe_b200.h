@@ -176,6 +176,14 @@ int tfhe_rescale_part(TfheCtx* ctx, const uint32_t* ct_local, const uint32_t* to
                       int level, int batch, int row_lo, int n_rows, uint32_t* out, void* ws,
                       size_t ws_bytes, void* stream);
 
+/* ---- diagnostics -----------------------------------------------------------
+ * Fault injection for the selftest (ref cli.py:77-87 corrupts the twiddle
+ * tables its backend actually uses): flips one byte of prime `prime`'s
+ * FORWARD twiddle tables on the device (every stage table the context built
+ * for it), so every later forward transform mod that prime is wrong.  Only
+ * for a private context the caller then destroys. */
+int tfhe_debug_corrupt_twiddle(TfheCtx* ctx, int prime);
+
 #ifdef __cplusplus
 }
 #endif

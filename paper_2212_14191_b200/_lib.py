@@ -69,6 +69,7 @@ SIGNATURES = {
                                            ctypes.c_int, _vp, ctypes.c_size_t, _vp]),
     "tfhe_rescale_part": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, _vp, _vp, ctypes.c_size_t, _vp]),
+    "tfhe_debug_corrupt_twiddle": (ctypes.c_int, [_vp, ctypes.c_int]),
 }
 
 _lib = None

@@ -945,6 +945,37 @@ int tfhe_rescale_part(TfheCtx* h, const uint32_t* ct_local, const uint32_t* top_
 
 }  // extern "C"
 
+/* ---- diagnostics --------------------------------------------------------- */
+extern "C" int tfhe_debug_corrupt_twiddle(TfheCtx* h, int prime) {
+  if (check_ctx(h)) return TFHE_EINVAL;
+  Ctx& c = h->c;
+  if (prime < 0 || prime >= c.n_primes) {
+    set_error("prime index out of range");
+    return TFHE_EINVAL;
+  }
+  // byte offsets (in each forward stage table) of this prime's first twiddle
+  // plane byte: small-n tiles [prime][tile...] and TS planes [prime][half][row][plane][K]
+  auto flip = [](void* dev_byte) {
+    uint8_t v = 0;
+    if (cudaMemcpy(&v, dev_byte, 1, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    v ^= 0x01;
+    return cudaMemcpy(dev_byte, &v, 1, cudaMemcpyHostToDevice) == cudaSuccess;
+  };
+  bool ok = true;
+  for (int s = 0; s < 2; ++s)
+    if (c.d_tw[0][s]) ok &= flip(c.d_tw[0][s] + (size_t)prime * c.tw_stride[s]);
+  for (int s = 0; s < 2; ++s) {
+    if (!c.d_twa[0][s]) continue;
+    const size_t ntw = s == 0 ? c.n1 : c.n2;      // rows (= K) of this stage
+    ok &= flip(reinterpret_cast<uint8_t*>(c.d_twa[0][s]) + (size_t)prime * ntw * ntw * 4);
+  }
+  if (!ok) {
+    set_error("twiddle fault injection: device copy failed");
+    return TFHE_ECUDA;
+  }
+  return 0;
+}
+
 /* ---- host-streaming transform (e2e path of batched_apply / transform_rows) -- */
 namespace {
 constexpr int kHostSlots = 3;

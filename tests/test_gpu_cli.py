@@ -119,3 +119,25 @@ def test_hadd_hsub_batch_vs_oracle():
         ck.hadd_batch(b0, CiphertextBatch(d(c1[:, :-1]), p.l_max - 1))
     with pytest.raises(ParameterError):
         ck.hsub_batch(b0, CiphertextBatch(d(c1), p.l_max, scale=3))
+
+
+@pytest.mark.parametrize("n", [256, 1 << 12, 1 << 16])
+def test_device_twiddle_fault_is_detected(n):
+    """tfhe_debug_corrupt_twiddle flips a byte of the DEVICE twiddle tables
+    (small-n tiles and TS planes): transforms mod that prime then disagree
+    with the oracle, other primes and fresh contexts are unaffected."""
+    from oracle import oracle as O
+    from paper_2212_14191_b200 import _lib
+    from paper_2212_14191_b200.device import DeviceContext
+    from paper_2212_14191_b200.params import generate_primes
+    qs = generate_primes(n, [30, 29])
+    bad = DeviceContext(n, qs)           # private: not in the shared cache
+    _lib.check(bad.lib.tfhe_debug_corrupt_twiddle(bad.handle, 0), "corrupt")
+    x = O.uniform_rows(np.random.default_rng(n), qs, (2, n))
+    d = torch.from_numpy(x.view(np.int32)).cuda()
+    got = bad.ntt(d, qs).cpu().numpy().view(np.uint32)
+    want = O.ntt(x, qs)
+    assert not np.array_equal(got[0], want[0])
+    assert np.array_equal(got[1], want[1])
+    good = DeviceContext.get(n, tuple(qs))
+    assert np.array_equal(good.ntt(d, qs).cpu().numpy().view(np.uint32), want)
