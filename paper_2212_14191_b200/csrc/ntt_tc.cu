@@ -908,7 +908,7 @@ int build_ntt_tables(Ctx& c) {
   c.use_ts = c.n1 >= 128 && c.n2 <= 256 && big_q;
   c.ts_stage2 = c.n1 == 64 && c.n2 == 128 && big_q;
   if (c.use_ts || c.ts_stage2) return build_ts_tables(c);
-  return 0;
+  return build_fused_tables(c);
 }
 
 int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& map, int batch,
@@ -919,6 +919,10 @@ int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& m
     return 2;
   }
   if (c.use_ts) return launch_ntt_ts(c, in, out, map, batch, inverse, epi, ws, st);
+  {
+    const int rc = launch_ntt_fused(c, in, out, map, batch, inverse, epi, st);
+    if (rc >= 0) return rc;
+  }
   StageArgs a;
   memset(&a, 0, sizeof(a));
   a.pc = c.d_pc;

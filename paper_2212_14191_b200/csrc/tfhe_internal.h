@@ -95,6 +95,12 @@ struct Ctx {
   // writing P in the TS blocked layout, stage 2 on the TS kernel (K = 128),
   // whose twiddles live in TMEM -- the resident kernel cannot hold K = 128
   bool ts_stage2 = false;
+  // fused single-launch n = 4096 transform (ntt_fused.cu): per [inverse]
+  // 64-point DFT byte-plane tiles, W2 R (Montgomery Hadamard), twists
+  uint8_t* d_fdft[2] = {nullptr, nullptr};
+  uint32_t* d_fw2[2] = {nullptr, nullptr};
+  uint32_t* d_ftw[2] = {nullptr, nullptr};
+  uint32_t* d_ftw_ks = nullptr;
   int sms = 148;
   std::vector<PrimeConst> h_pc;
 };
@@ -115,6 +121,12 @@ int launch_ntt_ts(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap
 // TS stage 2 alone over the blocked P workspace (see Ctx::ts_stage2)
 int launch_ntt_ts_stage2(const Ctx& c, const uint32_t* P, uint32_t* out, const LimbMap& map,
                          int batch, int inverse, const EpiArgs* epi, cudaStream_t st);
+
+// fused n = 4096 transform (ntt_fused.cu): tables (no-op for other shapes)
+// and the launch; -1 = not applicable, run the two-stage kernels
+int build_fused_tables(Ctx& c);
+int launch_ntt_fused(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& map,
+                     int batch, int inverse, const EpiArgs* epi, cudaStream_t st);
 
 // kernels (ntt_tc.cu)
 size_t ntt_workspace_bytes(const Ctx& c, int n_limbs, int batch);
