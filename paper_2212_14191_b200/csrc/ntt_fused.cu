@@ -16,8 +16,8 @@
 // (in the producers, one Montgomery product per element), inverse
 // post-multiplies output column k2 by psi^(-64 k2) n^-1 (in the stage-2
 // epilogue).  So one 64 KB byte-plane table serves both stages and the whole
-// working set fits in shared memory: D tiles 64 KB | A1 32 KB | A2 32 KB |
-// raw ring 2 x 32 KB | W2 16 KB (+ 4 KB of A1 bank-conflict padding).
+// working set fits in shared memory: D tiles 64 KB | A1 2 x 36 KB (padded
+// against bank conflicts) | A2 32 KB | raw 32 KB | W2 17 KB.
 //
 // Work unit = two batch members of one limb (MMA M = 128 rows).
 //   stage 1: D1[(b,i2)][k1] = sum_i1 A'_b[i1][i2] D[k1][i1]   A1 = data planes, MN-major
@@ -27,11 +27,16 @@
 //            A2 row k = i2, one 16-byte store per plane)
 //   stage 2: D2[(b,k1)][k2] = sum_i2 P_b[k1][i2] D[k2][i2]
 //   epi 2:   out[b][k2 n1 + k1] = fold(D2) (x twist) -> fused epilogue modes
-// Roles (16 warps, 128 registers each): 0-2 producers (bulk-copy raw members
-// in, twist, byte split), 3 MMA issuer + TMEM owner, 4-7 stage-1 epilogue (one
-// per TMEM lane quarter, 16-column chunks written to A2 as they fold), 8-15
-// stage-2 epilogue (two per lane quarter, 32 columns each).  TMEM: columns [0,256) stage-1 accumulators, [256,512) stage 2.
+// Roles (16 warps, 128 registers each): 0-2 producers (one bulk copy per unit
+// lands the two raw members; each thread pulls its <= 22 x 16 bytes into
+// registers at once so the slot refills early, then twists / byte-splits into
+// the double-buffered A1), 3 MMA issuer + TMEM owner, 4-11 stage-1 epilogue
+// (two per TMEM lane quarter, 32 columns each in 16-column chunks written to
+// A2 as they fold), 12-15 stage-2 epilogue (one per lane quarter: folds all 64
+// columns first and releases the accumulators, then applies the epilogue
+// mode and stores).  TMEM: columns [0,256) stage-1 accumulators, [256,512) stage 2.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -54,17 +59,27 @@ constexpr int kFA1Bytes = 2 * 4 * kFPlane1;
 constexpr int kFTwBytes = 2 * 4 * 256 * 32;   // (K-step, plane) B tiles of 256 rows x 32 K = 64 KB
 constexpr int kFRawBytes = 2 * kFN * 4;       // one unit's raw u32 data (two members)
 constexpr int kFW2Bytes = kFN * 4;
-constexpr int kFThreads = 512;
+constexpr int kFThreads = 512;               // 16 warps = 4 per SMSP at 128 registers
 constexpr int kFProdWarps = 3;
+constexpr int kFEpi1Warp0 = 4;
+// epilogue warps per TMEM lane quarter: 12 epilogue warps split 2 + 1 (plain
+// transforms: stage 1 has the heavier epilogue) or 1 + 2 (fused epilogue modes:
+// stage 2 streams operands); each warp owns 64 / W columns
+template <int MODE>
+__host__ __device__ constexpr int epi1_per_q() { return MODE == EPI_STORE ? 2 : 1; }
 constexpr int kFMmaWarp = 3;
-constexpr int kFEpi1Warp0 = 4, kFEpi2Warp0 = 8;
-constexpr int kFSmem = kFTwBytes + kFA1Bytes + kFABytes + 2 * kFRawBytes + kFW2Bytes + 2 * 64 * 4 + 32 * 8;
+constexpr int kFItems = 22;                   // ceil(64 warp items / 3 producer warps)
+// W2 R transposed [i2][k1] with a 68-word row pitch: the stage-1 epilogue
+// reads its row's 16 consecutive k1 as four conflict-free 16-byte loads
+constexpr int kFW2Pitch = 68;
+constexpr int kFW2TBytes = 64 * kFW2Pitch * 4;
+constexpr int kFSmem = kFTwBytes + 2 * kFA1Bytes + kFABytes + kFRawBytes + kFW2TBytes + 64 * 4 + 32 * 8;
 
 struct FusedArgs {
   const uint32_t* in;
   uint32_t* out;
   const uint8_t* dft;      // [prime] 64 KB byte-plane tiles of D (direction of the call)
-  const uint32_t* w2m;     // [prime][k1][i2] W2 R mod q (Montgomery Hadamard)
+  const uint32_t* w2m;     // [prime][i2][68-word row: k1] W2 R mod q (Montgomery Hadamard)
   const uint32_t* twist;   // [prime][64]: forward pre-twist (x R or x R^2) / inverse post-twist
   const PrimeConst* pc;
   int batch, upl;          // members; units per limb = ceil(batch / 2)
@@ -72,6 +87,7 @@ struct FusedArgs {
   long long units;
   LimbMap map;
   EpiArgs epi;
+  unsigned long long* trace;   // TFHE_FUSED_TRACE builds only
 };
 
 // sum_i 2^(8i) C_i (C_i < 2^24 for K = 64) -> v 2^-32 mod q, lazy in [0, 2q)
@@ -107,19 +123,46 @@ TFHE_DEV uint32_t mn_off(int j, int m, int k) {
                     (m >> 4) * SBO + (k & 7) * 16 + (m & 15));
 }
 
+// mbarrier wait that suspends the warp (hint: up to ~1 ms) instead of spinning,
+// so waiting roles do not steal issue slots from the working ones
+TFHE_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+      "@!P bra WAITS_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
+
+// timeline probes (-DTFHE_FUSED_TRACE): per-unit event clocks of CTA 0, one
+// lane of the first warp of each role; compiled out otherwise
+#ifdef TFHE_FUSED_TRACE
+constexpr int kFTraceN = 128;
+#define FTRACE(ev, i)                                                               \
+  do {                                                                              \
+    if (blockIdx.x == 0 && lane == 0 && (i) < kFTraceN && (warp == 0 || warp == 3 || \
+                                                          warp == 4 || warp == 8))  \
+      a.trace[(ev) * kFTraceN + (i)] = clock64();                                   \
+  } while (0)
+#else
+#define FTRACE(ev, i) do { } while (0)
+#endif
+
+template <int MODE, bool INV>
 __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sD = smem;
-  uint8_t* sA1 = sD + kFTwBytes;
-  uint8_t* sA2 = sA1 + kFA1Bytes;
+  uint8_t* sA1 = sD + kFTwBytes;                 // [2] buffers
+  uint8_t* sA2 = sA1 + 2 * kFA1Bytes;
   uint8_t* sRaw = sA2 + kFABytes;
-  uint32_t* sW2 = reinterpret_cast<uint32_t*>(sRaw + 2 * kFRawBytes);
-  uint32_t* sTw = sW2 + kFN;                   // 64 twist constants
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sTw + 2 * 64);
-  uint64_t* raw_full = bar + 0;    // [2]
-  uint64_t* raw_empty = bar + 2;   // [2]
-  uint64_t* a1_full = bar + 4;
-  uint64_t* a1_empty = bar + 5;
+  uint32_t* sW2 = reinterpret_cast<uint32_t*>(sRaw + kFRawBytes);   // [i2][68]
+  uint32_t* sTw = sW2 + 64 * kFW2Pitch;        // 64 twist constants
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sTw + 64);
+  uint64_t* raw_full = bar + 0;
+  uint64_t* raw_empty = bar + 1;
+  uint64_t* a1_full = bar + 2;     // [2]
+  uint64_t* a1_empty = bar + 4;    // [2]
   uint64_t* acc1_full = bar + 6;
   uint64_t* acc1_empty = bar + 7;
   uint64_t* a2_full = bar + 8;
@@ -132,26 +175,29 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
   uint64_t* epi2_done = bar + 15;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
+  constexpr int kW1 = epi1_per_q<MODE>(), kW2 = 3 - kW1;   // warps per lane quarter
+  constexpr int kC1 = 64 / kW1, kC2 = 64 / kW2;             // columns per warp
+  constexpr int kFEpi2Warp0 = kFEpi1Warp0 + 4 * kW1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long u0 = a.units * blockIdx.x / gridDim.x;
-  const int cnt = (int)(a.units * (blockIdx.x + 1) / gridDim.x - u0);
+  const int u0 = (int)(a.units * blockIdx.x / gridDim.x);
+  const int cnt = (int)(a.units * (blockIdx.x + 1) / gridDim.x) - u0;
   if (tid == 0) {
+    mbar_init(raw_full, 1);
+    mbar_init(raw_empty, 32 * kFProdWarps);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&raw_full[s], 1);
-      mbar_init(&raw_empty[s], 32 * kFProdWarps);
+      mbar_init(&a1_full[s], 32 * kFProdWarps);
+      mbar_init(&a1_empty[s], 1);
     }
-    mbar_init(a1_full, 32 * kFProdWarps);
-    mbar_init(a1_empty, 1);
     mbar_init(acc1_full, 1);
-    mbar_init(acc1_empty, 128);
-    mbar_init(a2_full, 128);
+    mbar_init(acc1_empty, 128 * kW1);
+    mbar_init(a2_full, 128 * kW1);
     mbar_init(a2_empty, 1);
     mbar_init(acc2_full, 1);
-    mbar_init(acc2_empty, 256);
+    mbar_init(acc2_empty, 128 * kW2);
     mbar_init(tw_full, 1);
     mbar_init(tw_empty, 1);
-    mbar_init(epi1_done, 128);
-    mbar_init(epi2_done, 256);
+    mbar_init(epi1_done, 128 * kW1);
+    mbar_init(epi2_done, 128 * kW2);
     fence_mbar_init();
   }
   if (warp == kFMmaWarp) tmem_alloc<512>(tmem_slot);
@@ -159,146 +205,177 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const bool fwd = !a.inverse;
-  auto limb_of = [&](int it) { return (int)((u0 + it) / a.upl); };
-  auto last_of_limb = [&](int it) { return it + 1 == cnt || limb_of(it + 1) != limb_of(it); };
-
-  if (warp < 4) {
-    if (warp < kFProdWarps) {
-      // ------------------------------------------------------------ producers
-      const int ptid = tid;   // 0..95
-      auto issue_raw = [&](int it, int slot) {
-        const long long g = u0 + it;
-        const int limb = (int)(g / a.upl), pair = (int)(g % a.upl);
-        const int b0 = 2 * pair, nb = min(2, a.batch - b0);
-        const uint32_t bytes = (uint32_t)nb * kFN * 4;
-        mbar_arrive_expect_tx(&raw_full[slot], bytes);
-        bulk_g2s(sRaw + slot * kFRawBytes,
-                 a.in + ((size_t)a.map.in_row[limb] * a.batch + b0) * kFN, bytes, &raw_full[slot]);
-      };
-      if (ptid == 0)
-        for (int it = 0; it < 2 && it < cnt; ++it) issue_raw(it, it);
-      int prev_limb = -1;
-      uint32_t tw_ph = 0;
-      for (int it = 0; it < cnt; ++it) {
-        const int limb = limb_of(it);
-        if (limb != prev_limb) {
-          if (ptid == 0) {
-            if (prev_limb >= 0) {
-              // every MMA and epilogue of the previous limb is done with the tables
-              mbar_wait(tw_empty, tw_ph);
-              mbar_wait(epi1_done, tw_ph);
-              mbar_wait(epi2_done, tw_ph);
-            }
-            const int pr = a.map.prime[limb];
-            mbar_arrive_expect_tx(tw_full, kFTwBytes + kFW2Bytes + 64 * 4);
-            bulk_g2s(sD, a.dft + (size_t)pr * kFTwBytes, kFTwBytes, tw_full);
-            bulk_g2s(sW2, a.w2m + (size_t)pr * kFN, kFW2Bytes, tw_full);
-            bulk_g2s(sTw, a.twist + (size_t)pr * 64, 64 * 4, tw_full);
-          }
-          if (prev_limb >= 0) tw_ph ^= 1;
-          mbar_wait(tw_full, tw_ph);   // the pre-twist constants are resident
-          prev_limb = limb;
-        }
-        const PrimeConst pc = a.pc[a.map.prime[limb]];
-        const int slot = it & 1;
-        mbar_wait(&raw_full[slot], (it >> 1) & 1);
-        if (it >= 1) mbar_wait(a1_empty, (it - 1) & 1);   // MMA1(it-1) has read A1
-        const uint8_t* raw = sRaw + slot * kFRawBytes;
-        // 64 warp items per unit: (member b, 4 rows i1, 32 columns i2); lane ->
-        // (r = lane / 8, c = lane % 8): 16-byte raw reads conflict-free per phase
-        const int r = lane >> 3, c = lane & 7;
-        for (int item = warp; item < 64; item += kFProdWarps) {
-          const int b = item >> 5, ib = (item >> 1) & 15, jb = item & 1;
-          const int i1 = 4 * ib + r, i2 = 32 * jb + 4 * c;
-          uint4 x = *reinterpret_cast<const uint4*>(raw + (size_t)b * kFN * 4 + (i1 * kFn1 + i2) * 4);
-          if (fwd) {
-            const uint32_t t = sTw[i1];   // psi^(64 i1) R (x R again for the key-switch MAC)
-            x.x = mont_lazy(x.x, t, pc);
-            x.y = mont_lazy(x.y, t, pc);
-            x.z = mont_lazy(x.z, t, pc);
-            x.w = mont_lazy(x.w, t, pc);
-          }
-          uint32_t w[4];
-          planes4f(x.x, x.y, x.z, x.w, w);
-          const int m = b * 64 + i2;
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<uint32_t*>(sA1 + mn_off<kFSbo1>(j, m, i1)) = w[j];
-        }
-        fence_proxy_async_smem();
-        mbar_arrive(a1_full);
-        mbar_arrive(&raw_empty[slot]);
-        if (ptid == 0 && it + 2 < cnt) {
-          mbar_wait(&raw_empty[slot], (it >> 1) & 1);
-          issue_raw(it + 2, slot);
-        }
-      }
-    } else {
-      // ------------------------------------------------------------ MMA issuer
-      // one MMA per (K-step, data plane): N = 256 = the four output-byte tiles
-      // V_{j,0..3} side by side, landing in the four accumulators C_0..C_3
-      // (TMEM columns i*64); A MN-major
-      constexpr uint32_t idesc = idesc_i8(kFRows, 256) | (1u << 15);
-      const uint32_t sD_u = smem_u32(sD);
-      auto issue = [&](uint32_t a_base, uint32_t d, uint32_t sbo) {
-#pragma unroll
-        for (int kc = 0; kc < 2; ++kc)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint64_t ad = smem_desc_kmajor(a_base + (kc * 4 + j) * 32 * sbo, 8 * sbo, sbo);
-            const uint64_t bd = smem_desc_kmajor(sD_u + (kc * 4 + j) * 8192, 4096, 128);
-            mma_i8_ss(d, ad, bd, idesc, (kc | j) != 0);
-          }
-      };
-      auto stage2 = [&](int v) {
-        mbar_wait(a2_full, v & 1);
-        if (v >= 1) mbar_wait(acc2_empty, (v - 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          issue(smem_u32(sA2), tmem + 256, 128);
-          mma_commit(a2_empty);
-          mma_commit(acc2_full);
-          if (last_of_limb(v)) mma_commit(tw_empty);
-        }
-        __syncwarp();
-      };
-      int prev_limb = -1;
-      uint32_t tw_ph = 0;
-      int s2_next = 0;   // next unit whose stage 2 is still to issue
-      for (int it = 0; it < cnt; ++it) {
-        const int limb = limb_of(it);
-        if (limb != prev_limb) {
-          // the previous limb's stage 2 goes first: its tables are still resident
-          while (s2_next < it) stage2(s2_next++);
-          if (prev_limb >= 0) tw_ph ^= 1;
-          mbar_wait(tw_full, tw_ph);
-          prev_limb = limb;
-        }
-        mbar_wait(a1_full, it & 1);
-        if (it >= 1) mbar_wait(acc1_empty, (it - 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          issue(smem_u32(sA1), tmem, kFSbo1);
-          mma_commit(a1_empty);
-          mma_commit(acc1_full);
-        }
-        __syncwarp();
-        while (s2_next < it) stage2(s2_next++);
-      }
-      while (s2_next < cnt) stage2(s2_next++);
+  constexpr bool fwd = !INV;
+  // unit position (limb, member pair), advanced incrementally by every role
+  // (no per-unit integer division)
+  struct UPos {
+    int limb, pair;
+  };
+  const UPos p0 = {u0 / a.upl, u0 % a.upl};
+  auto adv = [&](UPos& p) {
+    if (++p.pair == a.upl) {
+      p.pair = 0;
+      ++p.limb;
     }
+  };
+  auto last_of_limb = [&](const UPos& p, int it) { return it + 1 == cnt || p.pair + 1 == a.upl; };
+
+  if (warp < kFProdWarps) {
+    // -------------------------------------------------------------- producers
+    // (thread 0 = warp 0 lane 0 also owns the bulk copies)
+    auto issue_raw = [&](const UPos& p) {
+      const int b0 = 2 * p.pair, nb = min(2, a.batch - b0);
+      const uint32_t bytes = (uint32_t)nb * kFN * 4;
+      mbar_arrive_expect_tx(raw_full, bytes);
+      bulk_g2s(sRaw, a.in + ((size_t)a.map.in_row[p.limb] * a.batch + b0) * kFN, bytes, raw_full);
+    };
+    UPos pos = p0, ahead = p0;
+    if (tid == 0 && cnt > 0) issue_raw(ahead);
+    adv(ahead);
+    // 64 warp items per unit: (member b, 4 rows i1, 32 columns i2); warp w takes
+    // items w + 3k.  lane -> (r = lane / 8, c = lane % 8): the 16-byte raw reads
+    // are conflict-free per 8-lane phase, the padded A1 stores per warp
+    const int r = lane >> 3, c = lane & 7;
+    int prev_limb = -1;
+    uint32_t tw_ph = 0;
+    for (int it = 0; it < cnt; ++it, adv(pos)) {
+      const int limb = pos.limb;
+      mbar_wait(raw_full, it & 1);
+      FTRACE(0, it);
+      uint4 x[kFItems];
+#pragma unroll
+      for (int k = 0; k < kFItems; ++k) {
+        const int item = min(warp + kFProdWarps * k, 63);
+        const int b = item >> 5, ib = (item >> 1) & 15, jb = item & 1;
+        x[k] = *reinterpret_cast<const uint4*>(sRaw + (size_t)b * kFN * 4 +
+                                               ((4 * ib + r) * kFn1 + 32 * jb + 4 * c) * 4);
+      }
+      mbar_arrive(raw_empty);
+      if (tid == 0 && it + 1 < cnt) {
+        mbar_wait(raw_empty, it & 1);   // every producer has its values in registers
+        issue_raw(ahead);
+      }
+      adv(ahead);
+      if (limb != prev_limb) {
+        if (tid == 0) {
+          if (prev_limb >= 0) {
+            // every MMA and epilogue of the previous limb is done with the tables
+            mbar_wait(tw_empty, tw_ph);
+            mbar_wait(epi1_done, tw_ph);
+            mbar_wait(epi2_done, tw_ph);
+          }
+          const int pr = a.map.prime[limb];
+          mbar_arrive_expect_tx(tw_full, kFTwBytes + kFW2TBytes + 64 * 4);
+          bulk_g2s(sD, a.dft + (size_t)pr * kFTwBytes, kFTwBytes, tw_full);
+          bulk_g2s(sW2, a.w2m + (size_t)pr * (kFW2TBytes / 4), kFW2TBytes, tw_full);
+          bulk_g2s(sTw, a.twist + (size_t)pr * 64, 64 * 4, tw_full);
+        }
+        if (prev_limb >= 0) tw_ph ^= 1;
+        mbar_wait(tw_full, tw_ph);   // the pre-twist constants are resident
+        prev_limb = limb;
+      }
+      const PrimeConst pc = a.pc[a.map.prime[limb]];
+      const int buf = it & 1;
+      if (it >= 2) mbar_wait(&a1_empty[buf], ((it >> 1) - 1) & 1);   // MMA1(it-2) read it
+      FTRACE(1, it);
+      uint8_t* dst = sA1 + buf * kFA1Bytes;
+#pragma unroll
+      for (int k = 0; k < kFItems; ++k) {
+        const int item = warp + kFProdWarps * k;
+        if (item >= 64) break;
+        const int b = item >> 5, ib = (item >> 1) & 15, jb = item & 1;
+        const int i1 = 4 * ib + r, m = b * 64 + 32 * jb + 4 * c;
+        uint4 v = x[k];
+        if (fwd) {
+          const uint32_t t = sTw[i1];   // psi^(64 i1) R (x R again for the key-switch MAC)
+          v.x = mont_lazy(v.x, t, pc);
+          v.y = mont_lazy(v.y, t, pc);
+          v.z = mont_lazy(v.z, t, pc);
+          v.w = mont_lazy(v.w, t, pc);
+        }
+        uint32_t w[4];
+        planes4f(v.x, v.y, v.z, v.w, w);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<uint32_t*>(dst + mn_off<kFSbo1>(j, m, i1)) = w[j];
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&a1_full[buf]);
+      FTRACE(2, it);
+    }
+  } else if (warp == kFMmaWarp) {
+    // -------------------------------------------------------------- MMA issuer
+    // one MMA per (K-step, data plane): N = 256 = the four output-byte tiles
+    // V_{j,0..3} side by side, landing in the four accumulators C_0..C_3
+    // (TMEM columns i*64); A MN-major
+    constexpr uint32_t idesc = idesc_i8(kFRows, 256) | (1u << 15);
+    const uint32_t sD_u = smem_u32(sD);
+    auto issue = [&](uint32_t a_base, uint32_t d, uint32_t sbo) {
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t ad = smem_desc_kmajor(a_base + (kc * 4 + j) * 32 * sbo, 8 * sbo, sbo);
+          const uint64_t bd = smem_desc_kmajor(sD_u + (kc * 4 + j) * 8192, 4096, 128);
+          mma_i8_ss(d, ad, bd, idesc, (kc | j) != 0);
+        }
+    };
+    UPos pos2 = p0;   // position of the next stage-2 unit
+    auto stage2 = [&](int v) {
+      mbar_wait(a2_full, v & 1);
+      FTRACE(4, v);
+      if (v >= 1) mbar_wait(acc2_empty, (v - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        issue(smem_u32(sA2), tmem + 256, 128);
+        FTRACE(5, v);
+        mma_commit(a2_empty);
+        mma_commit(acc2_full);
+        if (last_of_limb(pos2, v)) mma_commit(tw_empty);
+      }
+      __syncwarp();
+      adv(pos2);
+    };
+    int prev_limb = -1;
+    uint32_t tw_ph = 0;
+    int s2_next = 0;   // next unit whose stage 2 is still to issue
+    UPos pos = p0;
+    for (int it = 0; it < cnt; ++it, adv(pos)) {
+      const int limb = pos.limb;
+      if (limb != prev_limb) {
+        // the previous limb's stage 2 goes first: its tables are still resident
+        while (s2_next < it) stage2(s2_next++);
+        if (prev_limb >= 0) tw_ph ^= 1;
+        mbar_wait(tw_full, tw_ph);
+        prev_limb = limb;
+      }
+      const int buf = it & 1;
+      mbar_wait(&a1_full[buf], (it >> 1) & 1);
+      if (it >= 1) mbar_wait(acc1_empty, (it - 1) & 1);
+      FTRACE(11, it);
+      tc_fence_after();
+      if (elect_one()) {
+        issue(smem_u32(sA1 + buf * kFA1Bytes), tmem, kFSbo1);
+        FTRACE(3, it);
+        mma_commit(&a1_empty[buf]);
+        mma_commit(acc1_full);
+      }
+      __syncwarp();
+      while (s2_next < it) stage2(s2_next++);
+    }
+    while (s2_next < cnt) stage2(s2_next++);
   } else if (warp < kFEpi2Warp0) {
     // -------------------------------------------------------------- stage-1 epilogue
     // warp -> TMEM lane quarter q (rows 32q..32q+31), all 64 columns k1 in
     // 16-column chunks: fold, Hadamard, byte-split, store into A2
-    const int q = warp & 3;
+    const int q = warp & 3, h = (warp - kFEpi1Warp0) >> 2;   // column slice h of kW1
     const int row = q * 32 + lane, b = row >> 6, i2 = row & 63;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     int prev_limb = -1;
     uint32_t tw_ph = 0;
-    for (int it = 0; it < cnt; ++it) {
-      const int limb = limb_of(it);
+    UPos pos = p0;
+    for (int it = 0; it < cnt; ++it, adv(pos)) {
+      const int limb = pos.limb;
       if (limb != prev_limb) {
         if (prev_limb >= 0) tw_ph ^= 1;
         mbar_wait(tw_full, tw_ph);   // this limb's W2
@@ -306,23 +383,30 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
       }
       const PrimeConst pc = a.pc[a.map.prime[limb]];
       mbar_wait(acc1_full, it & 1);
+      FTRACE(6, it);
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < 64; c0 += 16) {
+      for (int c0 = kC1 * h; c0 < kC1 * h + kC1; c0 += 16) {
         uint32_t acc[4][16];
 #pragma unroll
         for (int i = 0; i < 4; ++i) tmem_ld16(tmem + lane_off + i * 64 + c0, acc[i]);
         tmem_ld_wait();
-        if (c0 == 48) {
+        if (c0 == kC1 * h + kC1 - 16) {
           tc_fence_before();
           mbar_arrive(acc1_empty);   // buffer drained: MMA1(it+1) may start
+        }
+        uint32_t w2[16];
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) {
+          const uint4 t = *reinterpret_cast<const uint4*>(sW2 + i2 * kFW2Pitch + c0 + 4 * e4);
+          w2[4 * e4] = t.x; w2[4 * e4 + 1] = t.y; w2[4 * e4 + 2] = t.z; w2[4 * e4 + 3] = t.w;
         }
         uint32_t p[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           // S = fold (twiddles carry R), P = S W2 (W2 carries R): both lazy [0, 2q)
           const uint32_t s = fold4_mont(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
-          p[e] = mont_lazy(s, sW2[(c0 + e) * 64 + i2], pc);
+          p[e] = mont_lazy(s, w2[e], pc);
         }
         uint32_t pl[4][4];   // [plane][word]
 #pragma unroll
@@ -332,7 +416,8 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
 #pragma unroll
           for (int j = 0; j < 4; ++j) pl[j][e4] = w[j];
         }
-        if (c0 == 0 && it >= 1) mbar_wait(a2_empty, (it - 1) & 1);   // MMA2(it-1) read A2
+        if (c0 == kC1 * h && it >= 1) mbar_wait(a2_empty, (it - 1) & 1);   // MMA2(it-1) read A2
+        if (c0 == kC1 * h) FTRACE(7, it);
         const int m = b * 64 + c0;   // A2 row (b, k1) of the chunk's first k1
 #pragma unroll
         for (int j = 0; j < 4; ++j)
@@ -341,104 +426,118 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
       }
       fence_proxy_async_smem();
       mbar_arrive(a2_full);
-      if (last_of_limb(it)) mbar_arrive(epi1_done);
+      FTRACE(8, it);
+      if (last_of_limb(pos, it)) mbar_arrive(epi1_done);
     }
   } else {
     // -------------------------------------------------------------- stage-2 epilogue
+    // kW2 warps per lane quarter, kC2 columns k2 each: pass 1 folds the
+    // warp's columns of the row (b, k1) into registers and releases the
+    // accumulators (MMA2 of the next unit may start), pass 2 applies the
+    // epilogue mode 8 columns at a time; the row's operands (x / base /
+    // accumulators / key rows) are strided by n1
     const int q = warp & 3, h = (warp - kFEpi2Warp0) >> 2;
     const int row = q * 32 + lane, b = row >> 6, k1 = row & 63;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const int mode = a.epi.mode;
     int prev_limb = -1;
     uint32_t tw_ph = 0;
-    for (int it = 0; it < cnt; ++it) {
-      const long long gu = u0 + it;
-      const int limb = limb_of(it);
+    UPos pos = p0;
+    for (int it = 0; it < cnt; ++it, adv(pos)) {
+      const int limb = pos.limb;
       if (limb != prev_limb) {
         if (prev_limb >= 0) tw_ph ^= 1;
-        mbar_wait(tw_full, tw_ph);   // this limb's post-twist (inverse)
+        if (INV) mbar_wait(tw_full, tw_ph);   // this limb's post-twist
         prev_limb = limb;
       }
       const PrimeConst pc = a.pc[a.map.prime[limb]];
-      const int bm = 2 * (int)(gu % a.upl) + b;   // batch member of this row
+      const int bm = 2 * pos.pair + b;   // batch member of this row
       const bool valid = bm < a.batch;
-      const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + bm) * kFN + k1;
+      const size_t cofs = (size_t)kC2 * h * kFn1;   // the warp's first column k2
+      const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + bm) * kFN + k1 + cofs;
       mbar_wait(acc2_full, it & 1);
+      FTRACE(9, it);
       tc_fence_after();
-#pragma unroll 1
-      for (int c0 = 32 * h; c0 < 32 * h + 32; c0 += 8) {
+      uint32_t y[kC2];
+#pragma unroll
+      for (int cc = 0; cc < kC2; cc += 8) {
         uint32_t acc[4][8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) tmem_ld8(tmem + 256 + lane_off + i * 64 + c0, acc[i]);
-        // epilogue operands (issued before the TMEM wait so the loads overlap it)
-        uint32_t p0[8], p1[8], kb[8], ka[8];
-        const uint32_t* s0 = nullptr;
-        const uint32_t* s1 = nullptr;
-        if (valid) {
-          if (mode == EPI_SUB_SCALE) {
-            s0 = a.epi.x + ((size_t)a.epi.x_row[limb] * a.batch + bm) * kFN + k1;
-            const int br = a.epi.base_row[limb];
-            if (br >= 0) s1 = a.epi.base + ((size_t)br * a.batch + bm) * kFN + k1;
-          } else if (mode == EPI_KS_MAC && !a.epi.first) {
-            s0 = a.epi.acc_b + orow;
-            s1 = a.epi.acc_a + orow;
-          }
+        for (int i = 0; i < 4; ++i) tmem_ld8(tmem + 256 + lane_off + i * 64 + kC2 * h + cc, acc[i]);
+        tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const size_t pos = (size_t)(c0 + e) * kFn1;
-            if (s0) p0[e] = s0[pos];
-            if (s1) p1[e] = s1[pos];
+        for (int e = 0; e < 8; ++e)
+          y[cc + e] = fold4_mont(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);   // lazy
+      }
+      tc_fence_before();
+      mbar_arrive(acc2_empty);   // accumulators drained: MMA2(it+1) may start
+      if (valid) {
+        if (INV) {
+#pragma unroll
+          for (int e4 = 0; e4 < kC2 / 4; ++e4) {   // psi^(-64 k2) n^-1 (R), broadcast reads
+            const uint4 t = *reinterpret_cast<const uint4*>(sTw + kC2 * h + 4 * e4);
+            y[4 * e4] = mont_lazy(y[4 * e4], t.x, pc);
+            y[4 * e4 + 1] = mont_lazy(y[4 * e4 + 1], t.y, pc);
+            y[4 * e4 + 2] = mont_lazy(y[4 * e4 + 2], t.z, pc);
+            y[4 * e4 + 3] = mont_lazy(y[4 * e4 + 3], t.w, pc);
           }
-          if (mode == EPI_KS_MAC) {
-            const size_t kr = (size_t)a.epi.key_row[limb] * kFN + k1;
+        }
+#pragma unroll
+        for (int e = 0; e < kC2; ++e) y[e] = corr(y[e], pc.q);
+        if (MODE == EPI_STORE) {
+          uint32_t* o = a.out + orow;
+#pragma unroll
+          for (int e = 0; e < kC2; ++e) o[e * kFn1] = y[e];
+        } else if (MODE == EPI_SUB_SCALE) {
+          const uint32_t* xs = a.epi.x + ((size_t)a.epi.x_row[limb] * a.batch + bm) * kFN + k1 + cofs;
+          const int br = a.epi.base_row[limb];
+          const uint32_t* bs =
+              br >= 0 ? a.epi.base + ((size_t)br * a.batch + bm) * kFN + k1 + cofs : nullptr;
+          const uint32_t ss = a.epi.s[limb], ssp = a.epi.s_shoup[limb];
+          uint32_t* o = a.out + orow;
+#pragma unroll
+          for (int cc = 0; cc < kC2; cc += 8) {
+            uint32_t xv[8], bv[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              kb[e] = __ldg(a.epi.kb + kr + (size_t)(c0 + e) * kFn1);
-              ka[e] = __ldg(a.epi.ka + kr + (size_t)(c0 + e) * kFn1);
+              xv[e] = xs[(cc + e) * kFn1];
+              if (bs) bv[e] = bs[(cc + e) * kFn1];
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              uint32_t t = mul_shoup(sub_mod(xv[e], y[cc + e], pc.q), ss, ssp, pc.q);
+              if (bs) t = add_mod(bv[e], t, pc.q);
+              o[(cc + e) * kFn1] = t;
+            }
+          }
+        } else {   // EPI_KS_MAC: y arrives as y R (the pre-twist carries R^2)
+          const size_t kr = (size_t)a.epi.key_row[limb] * kFN + k1 + cofs;
+          uint32_t* ob = a.epi.acc_b + orow;
+          uint32_t* oa = a.epi.acc_a + orow;
+          const bool first = a.epi.first != 0;
+#pragma unroll
+          for (int cc = 0; cc < kC2; cc += 8) {
+            uint32_t kb[8], ka[8], pb[8], pa[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              kb[e] = __ldg(a.epi.kb + kr + (cc + e) * kFn1);
+              ka[e] = __ldg(a.epi.ka + kr + (cc + e) * kFn1);
+              if (!first) {
+                pb[e] = ob[(cc + e) * kFn1];
+                pa[e] = oa[(cc + e) * kFn1];
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const uint32_t tb = corr(mont_lazy(y[cc + e], kb[e], pc), pc.q);
+              const uint32_t ta = corr(mont_lazy(y[cc + e], ka[e], pc), pc.q);
+              ob[(cc + e) * kFn1] = first ? tb : add_mod(pb[e], tb, pc.q);
+              oa[(cc + e) * kFn1] = first ? ta : add_mod(pa[e], ta, pc.q);
             }
           }
         }
-        tmem_ld_wait();
-        if (c0 + 8 == 32 * h + 32) {
-          tc_fence_before();
-          mbar_arrive(acc2_empty);   // buffer drained: MMA2(it+1) may start
-        }
-        if (!valid) continue;
-        uint32_t y[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          uint32_t t = fold4_mont(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
-          if (!fwd) t = mont_lazy(t, sTw[c0 + e], pc);   // psi^(-64 k2) n^-1 (R)
-          y[e] = corr(t, pc.q);
-        }
-        uint32_t* o = a.out + orow + (size_t)c0 * kFn1;
-        if (mode == EPI_KS_MAC) {
-          // y arrives as y R (the forward pre-twist carries R^2): one Montgomery
-          // product per key gives y k
-          uint32_t* ob = a.epi.acc_b + orow + (size_t)c0 * kFn1;
-          uint32_t* oa = a.epi.acc_a + orow + (size_t)c0 * kFn1;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const uint32_t tb = corr(mont_lazy(y[e], kb[e], pc), pc.q);
-            const uint32_t ta = corr(mont_lazy(y[e], ka[e], pc), pc.q);
-            ob[e * kFn1] = a.epi.first ? tb : add_mod(p0[e], tb, pc.q);
-            oa[e * kFn1] = a.epi.first ? ta : add_mod(p1[e], ta, pc.q);
-          }
-          continue;
-        }
-        if (mode == EPI_SUB_SCALE) {
-          const uint32_t s = a.epi.s[limb], ss = a.epi.s_shoup[limb];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) y[e] = mul_shoup(sub_mod(p0[e], y[e], pc.q), s, ss, pc.q);
-          if (s1) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) y[e] = add_mod(p1[e], y[e], pc.q);
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e * kFn1] = y[e];
       }
-      if (last_of_limb(it)) mbar_arrive(epi2_done);
+      FTRACE(10, it);
+      if (last_of_limb(pos, it)) mbar_arrive(epi2_done);
     }
   }
 
@@ -471,7 +570,7 @@ int build_fused_tables(Ctx& c) {
     if (q <= (1u << 20)) return 0;   // the fused epilogues use Montgomery folds only
   const int np = c.n_primes;
   std::vector<uint8_t> tiles((size_t)np * kFTwBytes);
-  std::vector<uint32_t> w2((size_t)np * kFN), tw((size_t)np * 64);
+  std::vector<uint32_t> w2((size_t)np * 64 * kFW2Pitch, 0), tw((size_t)np * 64);
   for (int inv = 0; inv < 2; ++inv) {
     for (int p = 0; p < np; ++p) {
       const uint32_t q = c.primes[p];
@@ -505,7 +604,7 @@ int build_fused_tables(Ctx& c) {
       for (int k1 = 0; k1 < 64; ++k1)
         for (int i2 = 0; i2 < 64; ++i2) {
           const int e = inv ? (2 * k1 * i2 + k1) : (2 * k1 * i2 + i2);
-          w2[(size_t)p * kFN + k1 * 64 + i2] = mulmod_f(pw[e % (2 * kFN)], R, q);
+          w2[((size_t)p * 64 + i2) * kFW2Pitch + k1] = mulmod_f(pw[e % (2 * kFN)], R, q);
         }
       // twists: forward pre-twist psi^(64 i1) R; inverse post-twist psi^(-64 k2) n^-1 R
       const uint32_t n_inv = powmod_f(kFN, q - 2, q);
@@ -564,17 +663,43 @@ int launch_ntt_fused(const Ctx& c, const uint32_t* in, uint32_t* out, const Limb
   a.upl = (batch + 1) / 2;
   a.inverse = inverse ? 1 : 0;
   a.units = (long long)a.upl * map.n;
+  if (a.units >= (1ll << 31)) return -1;
   a.map = map;
   if (epi) a.epi = *epi;
   else a.epi.mode = EPI_STORE;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ntt_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem);
-    attr = true;
-  }
   const int grid = (int)std::min<long long>(c.sms, a.units);
   if (grid <= 0) return 0;
-  ntt_fused_kernel<<<grid, kFThreads, kFSmem, st>>>(a);
+#ifdef TFHE_FUSED_TRACE
+  static unsigned long long* tbuf = nullptr;
+  if (!tbuf) cudaMalloc(&tbuf, 16 * kFTraceN * 8);
+  cudaMemsetAsync(tbuf, 0, 16 * kFTraceN * 8, st);
+  a.trace = tbuf;
+#endif
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem);
+    kern<<<grid, kFThreads, kFSmem, st>>>(a);
+  };
+  if (inverse) {
+    if (mode == EPI_SUB_SCALE) go(ntt_fused_kernel<EPI_SUB_SCALE, true>);
+    else go(ntt_fused_kernel<EPI_STORE, true>);
+  } else {
+    if (mode == EPI_SUB_SCALE) go(ntt_fused_kernel<EPI_SUB_SCALE, false>);
+    else if (mode == EPI_KS_MAC) go(ntt_fused_kernel<EPI_KS_MAC, false>);
+    else go(ntt_fused_kernel<EPI_STORE, false>);
+  }
+#ifdef TFHE_FUSED_TRACE
+  {
+    std::vector<unsigned long long> h(16 * kFTraceN);
+    cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost);
+    static int seq = 0;
+    char fn[256];
+    snprintf(fn, sizeof(fn), "gpurun_out/ftrace_%d.bin", seq++);
+    if (FILE* f = fopen(fn, "wb")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
+#endif
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("fused ntt launch: ") + cudaGetErrorString(e));
