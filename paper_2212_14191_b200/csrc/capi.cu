@@ -586,7 +586,7 @@ void tfhe_ctx_destroy(TfheCtx* h) {
     }
   }
   cudaFree(c.d_pc);
-  cudaFree(c.d_ftw_ks);
+  cudaFree(c.d_fw2_ks);
   for (int i = 0; i < 2; ++i) {
     for (int s = 0; s < 2; ++s) {
       cudaFree(c.d_tw[i][s]);
@@ -598,7 +598,6 @@ void tfhe_ctx_destroy(TfheCtx* h) {
     cudaFree(c.d_w2s[i]);
     cudaFree(c.d_fdft[i]);
     cudaFree(c.d_fw2[i]);
-    cudaFree(c.d_ftw[i]);
     cudaFree(c.d_w2r[i]);
     cudaFree(c.d_w2rs[i]);
   }

@@ -11,12 +11,15 @@
 // 64th root of unity) the reference's stage matrices (params.py:198-228) are
 //   forward:  W1[k1][i1] = w^(k1 i1) psi^(64 i1),   W3[i2][k2] = w^(i2 k2)
 //   inverse:  W1[k1][i1] = w^-(k1 i1),              W3[i2][k2] = w^-(i2 k2) psi^(-64 k2) n^-1
-// i.e. both stages are the SAME symmetric 64-point DFT matrix D (w or w^-1)
-// plus a diagonal twist: forward pre-multiplies input row i1 by psi^(64 i1)
-// (in the producers, one Montgomery product per element), inverse
-// post-multiplies output column k2 by psi^(-64 k2) n^-1 (in the stage-2
-// epilogue).  So one 64 KB byte-plane table serves both stages and the whole
-// working set fits in shared memory: D tiles 64 KB | A1 2 x 36 KB (padded
+// i.e. both stages are the same 64-point DFT matrix D (w or w^-1) up to a
+// diagonal twist: forward twists the contraction index (t[k] = psi^(64 k)),
+// inverse the output index (u[c] = psi^(-64 c) n^-1).  Both stages therefore
+// use ONE table T (forward T[c][k] = w^(ck) t[k], inverse T[c][k] = u[c] w^-(ck))
+// and the twist the other stage did not ask for is divided out of the Hadamard
+// table for free: forward W2'[k1][i2] = W2 / t[i2] (stage 2 multiplies column
+// i2 by t), inverse W2' = W2 / u[k1] (stage 1 multiplies row k1 by u).  No
+// per-element twist is computed anywhere, and the whole working set fits in
+// shared memory: D tiles 64 KB | A1 2 x 36 KB (padded
 // against bank conflicts) | A2 32 KB | raw 32 KB | W2 17 KB.
 //
 // Work unit = two batch members of one limb (MMA M = 128 rows).
@@ -73,14 +76,13 @@ constexpr int kFItems = 22;                   // ceil(64 warp items / 3 producer
 // reads its row's 16 consecutive k1 as four conflict-free 16-byte loads
 constexpr int kFW2Pitch = 68;
 constexpr int kFW2TBytes = 64 * kFW2Pitch * 4;
-constexpr int kFSmem = kFTwBytes + 2 * kFA1Bytes + kFABytes + kFRawBytes + kFW2TBytes + 64 * 4 + 32 * 8;
+constexpr int kFSmem = kFTwBytes + 2 * kFA1Bytes + kFABytes + kFRawBytes + kFW2TBytes + 32 * 8;
 
 struct FusedArgs {
   const uint32_t* in;
   uint32_t* out;
   const uint8_t* dft;      // [prime] 64 KB byte-plane tiles of D (direction of the call)
   const uint32_t* w2m;     // [prime][i2][68-word row: k1] W2 R mod q (Montgomery Hadamard)
-  const uint32_t* twist;   // [prime][64]: forward pre-twist (x R or x R^2) / inverse post-twist
   const PrimeConst* pc;
   int batch, upl;          // members; units per limb = ceil(batch / 2)
   int inverse;
@@ -157,8 +159,7 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
   uint8_t* sA2 = sA1 + 2 * kFA1Bytes;
   uint8_t* sRaw = sA2 + kFABytes;
   uint32_t* sW2 = reinterpret_cast<uint32_t*>(sRaw + kFRawBytes);   // [i2][68]
-  uint32_t* sTw = sW2 + 64 * kFW2Pitch;        // 64 twist constants
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sTw + 64);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sW2 + 64 * kFW2Pitch);
   uint64_t* raw_full = bar + 0;
   uint64_t* raw_empty = bar + 1;
   uint64_t* a1_full = bar + 2;     // [2]
@@ -205,7 +206,6 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr bool fwd = !INV;
   // unit position (limb, member pair), advanced incrementally by every role
   // (no per-unit integer division)
   struct UPos {
@@ -265,16 +265,13 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
             mbar_wait(epi2_done, tw_ph);
           }
           const int pr = a.map.prime[limb];
-          mbar_arrive_expect_tx(tw_full, kFTwBytes + kFW2TBytes + 64 * 4);
+          mbar_arrive_expect_tx(tw_full, kFTwBytes + kFW2TBytes);
           bulk_g2s(sD, a.dft + (size_t)pr * kFTwBytes, kFTwBytes, tw_full);
           bulk_g2s(sW2, a.w2m + (size_t)pr * (kFW2TBytes / 4), kFW2TBytes, tw_full);
-          bulk_g2s(sTw, a.twist + (size_t)pr * 64, 64 * 4, tw_full);
         }
         if (prev_limb >= 0) tw_ph ^= 1;
-        mbar_wait(tw_full, tw_ph);   // the pre-twist constants are resident
         prev_limb = limb;
       }
-      const PrimeConst pc = a.pc[a.map.prime[limb]];
       const int buf = it & 1;
       if (it >= 2) mbar_wait(&a1_empty[buf], ((it >> 1) - 1) & 1);   // MMA1(it-2) read it
       FTRACE(1, it);
@@ -285,14 +282,7 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
         if (item >= 64) break;
         const int b = item >> 5, ib = (item >> 1) & 15, jb = item & 1;
         const int i1 = 4 * ib + r, m = b * 64 + 32 * jb + 4 * c;
-        uint4 v = x[k];
-        if (fwd) {
-          const uint32_t t = sTw[i1];   // psi^(64 i1) R (x R again for the key-switch MAC)
-          v.x = mont_lazy(v.x, t, pc);
-          v.y = mont_lazy(v.y, t, pc);
-          v.z = mont_lazy(v.z, t, pc);
-          v.w = mont_lazy(v.w, t, pc);
-        }
+        const uint4 v = x[k];
         uint32_t w[4];
         planes4f(v.x, v.y, v.z, v.w, w);
 #pragma unroll
@@ -439,16 +429,9 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
     const int q = warp & 3, h = (warp - kFEpi2Warp0) >> 2;
     const int row = q * 32 + lane, b = row >> 6, k1 = row & 63;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    int prev_limb = -1;
-    uint32_t tw_ph = 0;
     UPos pos = p0;
     for (int it = 0; it < cnt; ++it, adv(pos)) {
       const int limb = pos.limb;
-      if (limb != prev_limb) {
-        if (prev_limb >= 0) tw_ph ^= 1;
-        if (INV) mbar_wait(tw_full, tw_ph);   // this limb's post-twist
-        prev_limb = limb;
-      }
       const PrimeConst pc = a.pc[a.map.prime[limb]];
       const int bm = 2 * pos.pair + b;   // batch member of this row
       const bool valid = bm < a.batch;
@@ -471,16 +454,6 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
       tc_fence_before();
       mbar_arrive(acc2_empty);   // accumulators drained: MMA2(it+1) may start
       if (valid) {
-        if (INV) {
-#pragma unroll
-          for (int e4 = 0; e4 < kC2 / 4; ++e4) {   // psi^(-64 k2) n^-1 (R), broadcast reads
-            const uint4 t = *reinterpret_cast<const uint4*>(sTw + kC2 * h + 4 * e4);
-            y[4 * e4] = mont_lazy(y[4 * e4], t.x, pc);
-            y[4 * e4 + 1] = mont_lazy(y[4 * e4 + 1], t.y, pc);
-            y[4 * e4 + 2] = mont_lazy(y[4 * e4 + 2], t.z, pc);
-            y[4 * e4 + 3] = mont_lazy(y[4 * e4 + 3], t.w, pc);
-          }
-        }
 #pragma unroll
         for (int e = 0; e < kC2; ++e) y[e] = corr(y[e], pc.q);
         if (MODE == EPI_STORE) {
@@ -570,20 +543,32 @@ int build_fused_tables(Ctx& c) {
     if (q <= (1u << 20)) return 0;   // the fused epilogues use Montgomery folds only
   const int np = c.n_primes;
   std::vector<uint8_t> tiles((size_t)np * kFTwBytes);
-  std::vector<uint32_t> w2((size_t)np * 64 * kFW2Pitch, 0), tw((size_t)np * 64);
+  std::vector<uint32_t> w2((size_t)np * 64 * kFW2Pitch, 0), w2ks;
   for (int inv = 0; inv < 2; ++inv) {
+    if (!inv) w2ks.assign(w2.size(), 0);
     for (int p = 0; p < np; ++p) {
       const uint32_t q = c.primes[p];
       const uint32_t psi = inv ? powmod_f(c.psis[p], q - 2, q) : c.psis[p];
       const uint32_t w = powmod_f(psi, 128, q);   // primitive 64th root (inverse: w^-1)
       const uint32_t R = (uint32_t)(((uint64_t)1 << 32) % q);
-      uint32_t wp[64];
+      const uint32_t n_inv = powmod_f(kFN, q - 2, q);
+      std::vector<uint32_t> pw(2 * kFN);
+      pw[0] = 1;
+      for (int e = 1; e < 2 * kFN; ++e) pw[e] = mulmod_f(pw[e - 1], psi, q);
+      uint32_t wp[64], tw[64], tw_inv[64];
       wp[0] = 1;
       for (int e = 1; e < 64; ++e) wp[e] = mulmod_f(wp[e - 1], w, q);
+      // the twist: forward column twist t[k] = psi^(64 k) of W1; inverse row
+      // twist u[c] = psi^(-64 c) n^-1 of W3 (see the header)
+      for (int k = 0; k < 64; ++k) {
+        tw[k] = inv ? mulmod_f(pw[64 * k], n_inv, q) : pw[64 * k];
+        tw_inv[k] = powmod_f(tw[k], q - 2, q);
+      }
       uint8_t* base = tiles.data() + (size_t)p * kFTwBytes;
       for (int cc = 0; cc < 64; ++cc)        // output column (k1 or k2)
         for (int k = 0; k < 64; ++k) {       // contraction index (i1 or i2)
-          const uint32_t t = mulmod_f(wp[(cc * k) & 63], R, q);   // D[cc][k] R
+          // T[cc][k] R: forward w^(cc k) t[k], inverse u[cc] w^-(cc k)
+          const uint32_t t = mulmod_f(mulmod_f(wp[(cc * k) & 63], tw[inv ? cc : k], q), R, q);
           const int kc = k / 32, kr = k % 32;
           for (int j = 0; j < 4; ++j) {
             const uint32_t vj = mulmod_f(t, 1ull << (8 * j), q);
@@ -597,22 +582,17 @@ int build_fused_tables(Ctx& c) {
             }
           }
         }
-      // W2 R: forward psi^(2 k1 i2 + i2), inverse psi^-(2 k1 i2 + k1) (params.py:198-228)
-      std::vector<uint32_t> pw(2 * kFN);
-      pw[0] = 1;
-      for (int e = 1; e < 2 * kFN; ++e) pw[e] = mulmod_f(pw[e - 1], psi, q);
+      // Hadamard W2 R (forward psi^(2 k1 i2 + i2), inverse psi^-(2 k1 i2 + k1),
+      // params.py:198-228), divided by the twist the shared table adds: stage 2
+      // multiplies by t[i2] (forward), stage 1 by u[k1] (inverse)
       for (int k1 = 0; k1 < 64; ++k1)
         for (int i2 = 0; i2 < 64; ++i2) {
           const int e = inv ? (2 * k1 * i2 + k1) : (2 * k1 * i2 + i2);
-          w2[((size_t)p * 64 + i2) * kFW2Pitch + k1] = mulmod_f(pw[e % (2 * kFN)], R, q);
+          const uint32_t v = mulmod_f(mulmod_f(pw[e % (2 * kFN)], tw_inv[inv ? k1 : i2], q), R, q);
+          w2[((size_t)p * 64 + i2) * kFW2Pitch + k1] = v;
+          // key-switch MAC: one more R, so stage 2 yields y R (Montgomery form)
+          if (!inv) w2ks[((size_t)p * 64 + i2) * kFW2Pitch + k1] = mulmod_f(v, R, q);
         }
-      // twists: forward pre-twist psi^(64 i1) R; inverse post-twist psi^(-64 k2) n^-1 R
-      const uint32_t n_inv = powmod_f(kFN, q - 2, q);
-      for (int k = 0; k < 64; ++k) {
-        uint32_t v = mulmod_f(pw[64 * k], R, q);
-        if (inv) v = mulmod_f(v, n_inv, q);
-        tw[(size_t)p * 64 + k] = v;
-      }
     }
     auto up = [&](void** dst, const void* src, size_t bytes) {
       return cudaMalloc(dst, bytes) == cudaSuccess &&
@@ -620,21 +600,9 @@ int build_fused_tables(Ctx& c) {
     };
     if (!up(reinterpret_cast<void**>(&c.d_fdft[inv]), tiles.data(), tiles.size()) ||
         !up(reinterpret_cast<void**>(&c.d_fw2[inv]), w2.data(), w2.size() * 4) ||
-        !up(reinterpret_cast<void**>(&c.d_ftw[inv]), tw.data(), tw.size() * 4)) {
+        (!inv && !up(reinterpret_cast<void**>(&c.d_fw2_ks), w2ks.data(), w2ks.size() * 4))) {
       set_error("fused ntt table upload failed");
       return 3;
-    }
-    if (!inv) {
-      // key-switch MAC variant of the forward pre-twist: psi^(64 i1) R^2
-      for (int p = 0; p < np; ++p) {
-        const uint32_t q = c.primes[p];
-        const uint32_t R = (uint32_t)(((uint64_t)1 << 32) % q);
-        for (int k = 0; k < 64; ++k) tw[(size_t)p * 64 + k] = mulmod_f(tw[(size_t)p * 64 + k], R, q);
-      }
-      if (!up(reinterpret_cast<void**>(&c.d_ftw_ks), tw.data(), tw.size() * 4)) {
-        set_error("fused ntt table upload failed");
-        return 3;
-      }
     }
   }
   return 0;
@@ -656,8 +624,7 @@ int launch_ntt_fused(const Ctx& c, const uint32_t* in, uint32_t* out, const Limb
   a.in = in;
   a.out = out;
   a.dft = c.d_fdft[inverse ? 1 : 0];
-  a.w2m = c.d_fw2[inverse ? 1 : 0];
-  a.twist = inverse ? c.d_ftw[1] : (mode == EPI_KS_MAC ? c.d_ftw_ks : c.d_ftw[0]);
+  a.w2m = inverse ? c.d_fw2[1] : (mode == EPI_KS_MAC ? c.d_fw2_ks : c.d_fw2[0]);
   a.pc = c.d_pc;
   a.batch = batch;
   a.upl = (batch + 1) / 2;

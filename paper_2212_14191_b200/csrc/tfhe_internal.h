@@ -96,11 +96,11 @@ struct Ctx {
   // whose twiddles live in TMEM -- the resident kernel cannot hold K = 128
   bool ts_stage2 = false;
   // fused single-launch n = 4096 transform (ntt_fused.cu): per [inverse]
-  // 64-point DFT byte-plane tiles, W2 R (Montgomery Hadamard), twists
+  // twisted 64-point DFT byte-plane tiles and the matching Hadamard W2' R
+  // (+ the key-switch MAC variant W2' R^2)
   uint8_t* d_fdft[2] = {nullptr, nullptr};
   uint32_t* d_fw2[2] = {nullptr, nullptr};
-  uint32_t* d_ftw[2] = {nullptr, nullptr};
-  uint32_t* d_ftw_ks = nullptr;
+  uint32_t* d_fw2_ks = nullptr;
   int sms = 148;
   std::vector<PrimeConst> h_pc;
 };
