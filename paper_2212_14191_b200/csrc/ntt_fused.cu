@@ -65,11 +65,19 @@ constexpr int kFW2Bytes = kFN * 4;
 constexpr int kFThreads = 512;               // 16 warps = 4 per SMSP at 128 registers
 constexpr int kFProdWarps = 3;
 constexpr int kFEpi1Warp0 = 4;
+#ifndef TFHE_FUSED_E1_MAC
+#define TFHE_FUSED_E1_MAC 1
+#endif
+#ifndef TFHE_FUSED_E1_SUB
+#define TFHE_FUSED_E1_SUB 1
+#endif
 // epilogue warps per TMEM lane quarter: 12 epilogue warps split 2 + 1 (plain
 // transforms: stage 1 has the heavier epilogue) or 1 + 2 (fused epilogue modes:
 // stage 2 streams operands); each warp owns 64 / W columns
 template <int MODE>
-__host__ __device__ constexpr int epi1_per_q() { return MODE == EPI_STORE ? 2 : 1; }
+__host__ __device__ constexpr int epi1_per_q() {
+  return MODE == EPI_STORE ? 2 : MODE == EPI_KS_MAC ? TFHE_FUSED_E1_MAC : TFHE_FUSED_E1_SUB;
+}
 constexpr int kFMmaWarp = 3;
 constexpr int kFItems = 22;                   // ceil(64 warp items / 3 producer warps)
 // W2 R transposed [i2][k1] with a 68-word row pitch: the stage-1 epilogue
