@@ -587,6 +587,7 @@ void tfhe_ctx_destroy(TfheCtx* h) {
   }
   cudaFree(c.d_pc);
   cudaFree(c.d_fw2_ks);
+  cudaFree(c.d_p3t2ks);
   for (int i = 0; i < 2; ++i) {
     for (int s = 0; s < 2; ++s) {
       cudaFree(c.d_tw[i][s]);
@@ -597,6 +598,10 @@ void tfhe_ctx_destroy(TfheCtx* h) {
     cudaFree(c.d_w2[i]);
     cudaFree(c.d_w2s[i]);
     cudaFree(c.d_fdft[i]);
+    cudaFree(c.d_p3t1[i]);
+    cudaFree(c.d_p3hin[i]);
+    cudaFree(c.d_p3hout[i]);
+    cudaFree(c.d_p3t2[i]);
     cudaFree(c.d_fw2[i]);
     cudaFree(c.d_w2r[i]);
     cudaFree(c.d_w2rs[i]);
@@ -968,6 +973,7 @@ extern "C" int tfhe_debug_corrupt_twiddle(TfheCtx* h, int prime) {
   for (int s = 0; s < 2; ++s)
     if (c.d_tw[0][s]) ok &= flip(c.d_tw[0][s] + (size_t)prime * c.tw_stride[s]);
   if (c.d_fdft[0]) ok &= flip(c.d_fdft[0] + (size_t)prime * 65536);
+  if (c.d_p3t1[0]) ok &= flip(c.d_p3t1[0] + (size_t)prime * 16384);
   for (int s = 0; s < 2; ++s) {
     if (!c.d_twa[0][s]) continue;
     const size_t ntw = s == 0 ? c.n1 : c.n2;      // rows (= K) of this stage

@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
         x[k] = *reinterpret_cast<const uint4*>(sRaw + (size_t)b * kFN * 4 +
                                                ((4 * ib + r) * kFn1 + 32 * jb + 4 * c) * 4);
       }
+      fence_proxy_async_smem();   // raw reads before the next TMA write into the slot
       mbar_arrive(raw_empty);
       if (tid == 0 && it + 1 < cnt) {
         mbar_wait(raw_empty, it & 1);   // every producer has its values in registers

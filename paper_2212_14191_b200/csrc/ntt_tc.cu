@@ -30,6 +30,7 @@
 // owns TMEM and issues the MMAs; a 2-stage mbarrier ring overlaps loads with
 // MMAs.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -516,7 +517,10 @@ __global__ void __launch_bounds__(kResThreads, 1)
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<uint32_t*>(sA + ((g / 8) * 4 + j) * kATile + off) = w[j];
         }
-        if (!(kResDbg & 4)) mbar_arrive(&raw_empty[rs]);
+        if (!(kResDbg & 4)) {
+          fence_proxy_async_smem();   // raw reads before the next bulk copy into the slot
+          mbar_arrive(&raw_empty[rs]);
+        }
         if (tid == 0 && it + kResRaw < cnt && !(kResDbg & 4)) {
           mbar_wait(&raw_empty[rs], rph);
           issue_raw(it + kResRaw, rs);
@@ -907,7 +911,15 @@ int build_ntt_tables(Ctx& c) {
   const bool big_q = *std::min_element(c.primes.begin(), c.primes.end()) > (1u << 20);
   c.use_ts = c.n1 >= 128 && c.n2 <= 256 && big_q;
   c.ts_stage2 = c.n1 == 64 && c.n2 == 128 && big_q;
-  if (c.use_ts || c.ts_stage2) return build_ts_tables(c);
+  if (c.use_ts || c.ts_stage2) {
+    int rc = build_ts_tables(c);
+    if (rc) return rc;
+    if (c.n == 1 << 16 && big_q && !getenv("TFHE_NO_P3")) {
+      if ((rc = build_p3_tables(c))) return rc;
+      c.use_p3 = c.d_p3t1[0] != nullptr;
+    }
+    return 0;
+  }
   return build_fused_tables(c);
 }
 
@@ -918,6 +930,8 @@ int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& m
     set_error("ntt workspace too small");
     return 2;
   }
+  if (c.use_p3 && !(epi && epi->mode == EPI_KS_ACC))
+    return launch_ntt_p3(c, in, out, map, batch, inverse, epi, ws, st);
   if (c.use_ts) return launch_ntt_ts(c, in, out, map, batch, inverse, epi, ws, st);
   {
     const int rc = launch_ntt_fused(c, in, out, map, batch, inverse, epi, st);

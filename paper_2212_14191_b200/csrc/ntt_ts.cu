@@ -127,22 +127,33 @@ TFHE_DEV uint32_t ring_off(int row, int k) {
 // sequence (limb, chunk) and the same ring / accumulator phases.  Chunks of a
 // limb run member-major (c = b * R / kNC + x0 / kNC): a member's columns are
 // contiguous in memory, which measured ~3% faster than grouping the members
-// that share a column block.
+// that share a column block -- except for the fused key-switch epilogue
+// (EPI_KS_ACC), whose key tiles depend on the column block only: there the
+// chunks run column-block-major (c = (x0 / kNC) * batch + b) so consecutive
+// units of a CTA reuse the same S key tiles (L2-resident) across the batch
+// instead of streaming them once per member.
 struct UnitIter {
   int limb, c, b, x0;
   int sl;         // slice within the (limb, chunk) group (EPI_KS_ACC)
   int S;          // slices per group
   int R;          // data columns per member
+  int B;          // batch members (column-block-major order), 0 = member-major
   int s;          // ring slot
   uint32_t rph;   // ring phase parity of slot s
   int ab;         // accumulator buffer
   uint32_t aph;   // accumulator phase parity
-  TFHE_DEV void init(long long g0, int C, int R_, int S_) {
+  TFHE_DEV void init(long long g0, int C, int R_, int S_, int B_ = 0) {
     limb = (int)(g0 / C);
     c = (int)(g0 % C);
     R = R_;
-    b = c * kNC / R;
-    x0 = c * kNC % R;
+    B = B_;
+    if (B) {
+      b = c % B;
+      x0 = c / B * kNC;
+    } else {
+      b = c * kNC / R;
+      x0 = c * kNC % R;
+    }
     sl = 0; S = S_;
     s = 0; rph = 0; ab = 0; aph = 0;
   }
@@ -150,7 +161,9 @@ struct UnitIter {
     if (++sl == S) {
       sl = 0;
       if (++c == C) { c = 0; ++limb; b = 0; x0 = 0; }
-      else if ((x0 += kNC) == R) { x0 = 0; ++b; }
+      else if (B) {
+        if (++b == B) { b = 0; x0 += kNC; }
+      } else if ((x0 += kNC) == R) { x0 = 0; ++b; }
     }
     if (++s == kRing) { s = 0; rph ^= 1; }
     ab ^= 1;
@@ -306,7 +319,7 @@ __global__ void __launch_bounds__(kThreadsTS, 1) ntt_ts_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   UnitIter w;
-  w.init(g0, C, a.R, a.S);
+  w.init(g0, C, a.R, a.S, MODE == EPI_KS_ACC && !(kDbg & 65536) ? a.batch : 0);
   // Each role's register budget is set at the top of its own branch so that
   // ptxas allocates every role's code under the matching setmaxnreg limit.
   if (warp < 4) {
@@ -1050,6 +1063,7 @@ int launch_ntt_ts_stage2(const Ctx& c, const uint32_t* P, uint32_t* out, const L
 int launch_ntt_ts_ks_group(const Ctx& c, const uint32_t* in, void* ws, const LimbMap& s1map,
                            const LimbMap& tmap, int S, int batch, const EpiArgs& epi,
                            cudaStream_t st) {
+  if (c.use_p3) return launch_ntt_p3_ks_group(c, in, ws, s1map, tmap, S, batch, epi, st);
   if (s1map.n != S * tmap.n) {
     set_error("key-switch group: stage-1 map must hold S * T limbs");
     return 2;

@@ -101,6 +101,15 @@ struct Ctx {
   uint8_t* d_fdft[2] = {nullptr, nullptr};
   uint32_t* d_fw2[2] = {nullptr, nullptr};
   uint32_t* d_fw2_ks = nullptr;
+  // three-factor n = 2^16 transform (ntt_p3.cu), per [inverse]: column-pass
+  // 32-point tiles, inner / outer Hadamard tables, row-pass 64-point tiles
+  // (+ the key-switch MAC variant of the forward row tiles)
+  bool use_p3 = false;
+  uint8_t* d_p3t1[2] = {nullptr, nullptr};
+  uint32_t* d_p3hin[2] = {nullptr, nullptr};
+  uint32_t* d_p3hout[2] = {nullptr, nullptr};
+  uint8_t* d_p3t2[2] = {nullptr, nullptr};
+  uint8_t* d_p3t2ks = nullptr;
   int sms = 148;
   std::vector<PrimeConst> h_pc;
 };
@@ -127,6 +136,15 @@ int launch_ntt_ts_stage2(const Ctx& c, const uint32_t* P, uint32_t* out, const L
 int build_fused_tables(Ctx& c);
 int launch_ntt_fused(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& map,
                      int batch, int inverse, const EpiArgs* epi, cudaStream_t st);
+
+// three-factor n = 2^16 transform (ntt_p3.cu)
+int build_p3_tables(Ctx& c);
+int launch_ntt_p3(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& map, int batch,
+                  int inverse, const EpiArgs* epi, void* ws, cudaStream_t st);
+// key-switch group on the p3 plan (same contract as launch_ntt_ts_ks_group)
+int launch_ntt_p3_ks_group(const Ctx& c, const uint32_t* in, void* ws, const LimbMap& s1map,
+                           const LimbMap& tmap, int S, int batch, const EpiArgs& epi,
+                           cudaStream_t st);
 
 // kernels (ntt_tc.cu)
 size_t ntt_workspace_bytes(const Ctx& c, int n_limbs, int batch);
