@@ -62,6 +62,14 @@ int tfhe_ctx_create(int device, int log_n, const uint32_t* primes, const uint32_
 void tfhe_ctx_destroy(TfheCtx* ctx);
 /* n1 x n2 plan actually used (params.build_ntt_plan, params.py:170-175) */
 int tfhe_ctx_plan(const TfheCtx* ctx, int* n1, int* n2);
+/* How the device factors one transform into tensor-core contractions (any
+ * exact factorisation gives the reference's bits): the contraction lengths
+ * k0, k1, k2 of its GEMM stages (k2 = 0 for two stages).  n = 2^16 on the
+ * three-factor plan: (32, 32, 64) -- a 1024-point column transform split
+ * 32 x 32 on chip, then 64-point rows; n = 2^14 / 2^15: (n1, n2, 0) on the
+ * twiddle-resident kernel; n = 4096: (64, 64, 0).  int8 tensor work per
+ * limb-transform = 32 n (k0 + k1 + k2). */
+int tfhe_ctx_transform_plan(const TfheCtx* ctx, int* k0, int* k1, int* k2);
 
 /* ---- transforms --------------------------------------------------------
  * Replaces ntt.transform_rows (ntt.py:347-363), ntt_forward/ntt_inverse

@@ -70,6 +70,9 @@ SIGNATURES = {
     "tfhe_rescale_part": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, _vp, _vp, ctypes.c_size_t, _vp]),
     "tfhe_debug_corrupt_twiddle": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "tfhe_ctx_transform_plan": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int),
+                                               ctypes.POINTER(ctypes.c_int),
+                                               ctypes.POINTER(ctypes.c_int)]),
 }
 
 _lib = None

@@ -616,6 +616,21 @@ int tfhe_ctx_plan(const TfheCtx* h, int* n1, int* n2) {
   return 0;
 }
 
+int tfhe_ctx_transform_plan(const TfheCtx* h, int* k0, int* k1, int* k2) {
+  if (check_ctx(h)) return TFHE_EINVAL;
+  const Ctx& c = h->c;
+  int f[3] = {c.n1, c.n2, 0};
+  if (c.use_p3) {
+    f[0] = 32;
+    f[1] = 32;
+    f[2] = 64;
+  }
+  if (k0) *k0 = f[0];
+  if (k1) *k1 = f[1];
+  if (k2) *k2 = f[2];
+  return 0;
+}
+
 size_t tfhe_ntt_workspace_bytes(const TfheCtx* h, int n_limbs, int batch) {
   return h ? ntt_workspace_bytes(h->c, n_limbs, batch) : 0;
 }

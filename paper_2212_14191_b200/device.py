@@ -109,6 +109,10 @@ class DeviceContext:
         n1, n2 = ctypes.c_int(), ctypes.c_int()
         self.lib.tfhe_ctx_plan(self.handle, ctypes.byref(n1), ctypes.byref(n2))
         self.plan = (n1.value, n2.value)
+        k = [ctypes.c_int() for _ in range(3)]
+        self.lib.tfhe_ctx_transform_plan(self.handle, *[ctypes.byref(v) for v in k])
+        #: contraction lengths of the device factorisation (tfhe_ctx_transform_plan)
+        self.transform_plan = tuple(v.value for v in k)
         self._ws = {}          # stream handle -> byte workspace
         self._staging = None
 
