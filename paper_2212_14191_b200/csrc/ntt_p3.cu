@@ -31,6 +31,7 @@
 //   epilogue writes out[1024 k2 + k1] (coalesced along k1) through the same
 //   fused modes as the other transforms (plain, ModDown/rescale, key-switch MAC).
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -55,7 +56,7 @@ constexpr int kPItems = 22;                      // ceil(64 warp items / 3 produ
 
 
 // ---- pass 1 shared memory: T 16 KB | H' 4 KB | raw 32 KB | A1 2 x (2 tiles) | A2 (2 tiles)
-constexpr int kC1T = 16384, kC1H = 4096;
+constexpr int kC1T = 16384, kC1H = 64 * 32 * 4;   // T | outer twist beta[i2][b2]
 constexpr int kC1A = 2 * kPTile + 16;            // two M tiles (+16 B: tile 1 on other banks)
 constexpr int kC1Smem = kC1T + kC1H + kPRaw + 2 * kC1A + kC1A + 32 * 8;
 // ---- pass 2 shared memory: T2 64 KB | raw 32 KB | A 2 x (2 K-steps)
@@ -65,12 +66,13 @@ constexpr int kC2Smem = kC2T + kPRaw + 2 * kC2A + 32 * 8;
 
 struct ColArgs {
   const uint8_t* tab;      // [prime] 16 KB: T (B operand, 4 planes x 128 rows x 32 K)
-  const uint32_t* hin;     // [prime][b1][a2] H' R
-  const uint32_t* hout;    // [prime][i2][k1] outer Hadamard R
+  const uint32_t* hin;     // [prime][b1][a2][i2] H'[b1][a2] c[i2][b1] R (inner x row part of outer)
+  const uint32_t* hout;    // [prime][i2][b2] beta R (column part of the outer Hadamard)
   uint32_t* P;             // P^T workspace: [limb][member][i2][k1]
   const PrimeConst* pc;
   int batch, units;
   LimbMap map;
+  unsigned long long* trace;   // TFHE_P3_TRACE builds only
   CUtensorMap tmap;        // input viewed as [rows * batch][1024 i1][64 i2], box {8, 256, 1}
 };
 
@@ -112,6 +114,20 @@ TFHE_DEV uint32_t p_off(int kc, int j, int m, int k) {
                     (k & 7) * 16 + (m & 15));
 }
 
+// timeline probes of the column pass (-DTFHE_P3_TRACE): per-unit event clocks
+// of CTA 0, lane 0 of the first warp of each role; compiled out otherwise
+#ifdef TFHE_P3_TRACE
+constexpr int kPTraceN = 128;
+#define PTRACE(ev, i)                                                                \
+  do {                                                                               \
+    if (blockIdx.x == 0 && lane == 0 && (i) < kPTraceN &&                            \
+        (warp == 0 || warp == 3 || warp == 4 || warp == 12))                         \
+      a.trace[(ev) * kPTraceN + (i)] = clock64();                                    \
+  } while (0)
+#else
+#define PTRACE(ev, i) do { } while (0)
+#endif
+
 // ============================================================================ pass 1
 template <bool INV>
 __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_constant__ ColArgs a) {
@@ -135,6 +151,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
   uint64_t* tw_full = bar + 12;
   uint64_t* tw_empty = bar + 13;
   uint64_t* epiA_done = bar + 14;
+  uint64_t* epiB_done = bar + 15;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -156,6 +173,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
     mbar_init(tw_full, 1);
     mbar_init(tw_empty, 1);
     mbar_init(epiA_done, 256);
+    mbar_init(epiB_done, 128);
     fence_mbar_init();
   }
   if (warp == kPMmaWarp) tmem_alloc<512>(tmem_slot);
@@ -202,6 +220,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
     for (int it = 0; it < cnt; ++it, adv(pos)) {
       const int limb = pos.limb;
       mbar_wait(raw_full, it & 1);
+      PTRACE(0, it);
       uint4 x[kPItems];
 #pragma unroll
       for (int k = 0; k < kPItems; ++k) {
@@ -220,18 +239,19 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
         if (tid == 0) {
           if (prev_limb >= 0) {
             mbar_wait(tw_empty, tw_ph);
-            mbar_wait(epiA_done, tw_ph);
+            mbar_wait(epiB_done, tw_ph);
           }
           const int pr = a.map.prime[limb];
           mbar_arrive_expect_tx(tw_full, kC1T + kC1H);
           bulk_g2s(sT, a.tab + (size_t)pr * kC1T, kC1T, tw_full);
-          bulk_g2s(sH, a.hin + (size_t)pr * 1024, kC1H, tw_full);
+          bulk_g2s(sH, a.hout + (size_t)pr * (kC1H / 4), kC1H, tw_full);
         }
         if (prev_limb >= 0) tw_ph ^= 1;
         prev_limb = limb;
       }
       const int buf = it & 1;
       if (it >= 2) mbar_wait(&a1_empty[buf], ((it >> 1) - 1) & 1);
+      PTRACE(1, it);
       uint8_t* dst = sA1 + buf * kC1A;
 #pragma unroll
       for (int k = 0; k < kPItems; ++k) {
@@ -247,6 +267,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
       }
       fence_proxy_async_smem();
       mbar_arrive(&a1_full[buf]);
+      PTRACE(2, it);
     }
   } else if (warp == kPMmaWarp) {
     // -------------------------------------------------------------- MMA issuer
@@ -268,10 +289,12 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
     UPos pos2 = p0;
     auto stageB = [&](int v) {
       mbar_wait(a2_full, v & 1);
+      PTRACE(4, v);
       if (v >= 1) mbar_wait(accB_empty, (v - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
         issue(smem_u32(sA2), tmem + 256);
+        PTRACE(5, v);
         mma_commit(a2_empty);
         mma_commit(accB_full);
         if (last_of_limb(pos2, v)) mma_commit(tw_empty);
@@ -293,9 +316,11 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
       const int buf = it & 1;
       mbar_wait(&a1_full[buf], (it >> 1) & 1);
       if (it >= 1) mbar_wait(accA_empty, (it - 1) & 1);
+      PTRACE(11, it);
       tc_fence_after();
       if (elect_one()) {
         issue(smem_u32(sA1 + buf * kC1A), tmem);
+        PTRACE(3, it);
         mma_commit(&a1_empty[buf]);
         mma_commit(accA_full);
       }
@@ -319,15 +344,21 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
     for (int it = 0; it < cnt; ++it, adv(pos)) {
       if (pos.limb != prev_limb) {
         if (prev_limb >= 0) tw_ph ^= 1;
-        mbar_wait(tw_full, tw_ph);   // this limb's H'
+        mbar_wait(tw_full, tw_ph);   // this limb's tables (the column twist for epi B)
         prev_limb = pos.limb;
       }
-      const PrimeConst pc = a.pc[a.map.prime[pos.limb]];
+      const int pr = a.map.prime[pos.limb];
+      const PrimeConst pc = a.pc[pr];
+      // H''[b1][a2][i2 = 8 cb + t]: lanes read 32-byte runs of 8 consecutive i2
+      const uint32_t* hrow = a.hin + ((size_t)pr * 1024 + a2) * 64 + 8 * pos.cb + t;
       mbar_wait(accA_full, it & 1);
+      PTRACE(6, it);
       tc_fence_after();
 #pragma unroll 1
       for (int g = 0; g < 2; ++g) {
-        uint32_t acc[4][16];
+        uint32_t acc[4][16], hv[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) hv[e] = __ldg(hrow + (size_t)(16 * g + e) * 32 * 64);
 #pragma unroll
         for (int i = 0; i < 4; ++i) tmem_ld16(tmem + lane_off + tau * 128 + i * 32 + 16 * g, acc[i]);
         tmem_ld_wait();
@@ -339,7 +370,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const uint32_t s = fold4_m(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
-          p[e] = mont_l(s, sH[(16 * g + e) * 32 + a2], pc);   // H'[b1][a2] R
+          p[e] = mont_l(s, hv[e], pc);   // H''[b1][a2][i2] R
         }
         uint32_t pl[4][4];
 #pragma unroll
@@ -350,6 +381,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
           for (int j = 0; j < 4; ++j) pl[j][e4] = w[j];
         }
         if (g == 0 && it >= 1) mbar_wait(a2_empty, (it - 1) & 1);
+        if (g == 0) PTRACE(7, it);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           *reinterpret_cast<uint4*>(a2t + p_off(0, j, mb + 16 * g, a2)) =
@@ -357,20 +389,31 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
       }
       fence_proxy_async_smem();
       mbar_arrive(a2_full);
+      PTRACE(8, it);
       if (last_of_limb(pos, it)) mbar_arrive(epiA_done);
     }
   } else {
     // -------------------------------------------------------------- stage-B epilogue
     // warp -> lane quarter q; in M tile tau' its row m' = 32 q + lane is
-    // (column t = 4 tau' + q, b1 = lane); outputs k1 = b1 + 32 b2 take the outer
-    // Hadamard and go to P^T[i2 = 8 cb + t][k1] (coalesced along b1)
+    // (column t = 4 tau' + q, b1 = lane); outputs k1 = b1 + 32 b2 take the
+    // column part beta[i2][b2] of the outer Hadamard (broadcast shared-memory
+    // reads; the row part rode in with the inner Hadamard) and go to
+    // P^T[i2 = 8 cb + t][k1] (coalesced along b1)
     const int q = warp & 3;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    int prev_limb = -1;
+    uint32_t tw_ph = 0;
     UPos pos = p0;
     for (int it = 0; it < cnt; ++it, adv(pos)) {
+      if (pos.limb != prev_limb) {
+        if (prev_limb >= 0) tw_ph ^= 1;
+        mbar_wait(tw_full, tw_ph);   // this limb's beta
+        prev_limb = pos.limb;
+      }
       const int pr = a.map.prime[pos.limb];
       const PrimeConst pc = a.pc[pr];
       mbar_wait(accB_full, it & 1);
+      PTRACE(9, it);
       tc_fence_after();
       uint32_t y[2][32];
 #pragma unroll
@@ -391,11 +434,19 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
 #pragma unroll
       for (int tile = 0; tile < 2; ++tile) {
         const int i2 = 8 * pos.cb + 4 * tile + q;
-        const uint32_t* h = a.hout + ((size_t)pr * kPn2 + i2) * kPn1 + lane;
+        const uint32_t* bt = sH + i2 * 32;
         uint32_t* o = a.P + (((size_t)pos.limb * a.batch + pos.b) * kPn2 + i2) * kPn1 + lane;
 #pragma unroll
-        for (int b2 = 0; b2 < 32; ++b2) o[32 * b2] = mont_l(y[tile][b2], __ldg(h + 32 * b2), pc);
+        for (int b4 = 0; b4 < 8; ++b4) {
+          const uint4 bv = *reinterpret_cast<const uint4*>(bt + 4 * b4);
+          o[32 * (4 * b4)] = mont_l(y[tile][4 * b4], bv.x, pc);
+          o[32 * (4 * b4 + 1)] = mont_l(y[tile][4 * b4 + 1], bv.y, pc);
+          o[32 * (4 * b4 + 2)] = mont_l(y[tile][4 * b4 + 2], bv.z, pc);
+          o[32 * (4 * b4 + 3)] = mont_l(y[tile][4 * b4 + 3], bv.w, pc);
+        }
       }
+      PTRACE(10, it);
+      if (last_of_limb(pos, it)) mbar_arrive(epiB_done);
     }
   }
 
@@ -770,7 +821,7 @@ int build_p3_tables(Ctx& c) {
     if (q <= (1u << 20)) return 0;   // Montgomery folds only
   const int np = c.n_primes;
   std::vector<uint8_t> t1((size_t)np * kC1T), t2((size_t)np * kC2T), t2ks;
-  std::vector<uint32_t> hin((size_t)np * 1024), hout((size_t)np * kPN);
+  std::vector<uint32_t> hin((size_t)np * 1024 * 64), hout((size_t)np * 64 * 32);
   for (int inv = 0; inv < 2; ++inv) {
     if (!inv) t2ks.assign(t2.size(), 0);
     for (int p = 0; p < np; ++p) {
@@ -794,17 +845,26 @@ int build_p3_tables(Ctx& c) {
       pack_tiles(t1.data() + (size_t)p * kC1T, 32, q, [&](int cc, int k) {
         return mulmod_p(mulmod_p(P(4096ull * ((cc * k) & 31)), tw[k], q), R, q);
       });
+      // outer Hadamard (forward psi^((2 k1 + 1) i2), inverse psi^-((2 i2 + 1) k1)),
+      // k1 = b1 + 32 b2, factored as c[i2][b1] beta[i2][b2]:
+      //   forward c = psi^((2 b1 + 1) i2), beta = psi^(64 i2 b2)
+      //   inverse c = psi^-((2 i2 + 1) b1), beta = psi^-(32 (2 i2 + 1) b2)
+      // c scales the stage-B input row (t, b1), so it rides in the inner
+      // Hadamard; beta is applied per output column by the stage-B epilogue
       for (int b1 = 0; b1 < 32; ++b1)
         for (int a2 = 0; a2 < 32; ++a2) {
           // inner Hadamard: forward psi^(64 (2 b1 + 1) a2), inverse psi^-(128 a2 b1)
-          const uint32_t h = inv ? P(128ull * a2 * b1) : P(64ull * (2 * b1 + 1) * a2);
-          hin[(size_t)p * 1024 + b1 * 32 + a2] = mulmod_p(mulmod_p(h, twi[a2], q), R, q);
+          const uint32_t h = mulmod_p(inv ? P(128ull * a2 * b1) : P(64ull * (2 * b1 + 1) * a2),
+                                      twi[a2], q);
+          for (int i2 = 0; i2 < kPn2; ++i2) {
+            const uint32_t cv = inv ? P((2ull * i2 + 1) * b1) : P((2ull * b1 + 1) * i2);
+            hin[(((size_t)p * 32 + b1) * 32 + a2) * 64 + i2] = mulmod_p(mulmod_p(h, cv, q), R, q);
+          }
         }
-      // outer Hadamard [i2][k1]: forward psi^((2 k1 + 1) i2), inverse psi^-((2 i2 + 1) k1)
       for (int i2 = 0; i2 < kPn2; ++i2)
-        for (int k1 = 0; k1 < kPn1; ++k1) {
-          const uint32_t h = inv ? P((2ull * i2 + 1) * k1) : P((2ull * k1 + 1) * i2);
-          hout[((size_t)p * kPn2 + i2) * kPn1 + k1] = mulmod_p(h, R, q);
+        for (int b2 = 0; b2 < 32; ++b2) {
+          const uint32_t bv = inv ? P(32ull * (2 * i2 + 1) * b2) : P(64ull * i2 * b2);
+          hout[((size_t)p * kPn2 + i2) * 32 + b2] = mulmod_p(bv, R, q);
         }
       // pass 2 (64-point rows): forward psi^(2048 k2 i2), inverse
       // psi^-(1024 (2 i2 + 1) k2) n^-1 (row twist on the output k2)
@@ -869,12 +929,31 @@ int launch_p3_col(const Ctx& c, const uint32_t* in, uint32_t* P, const LimbMap& 
   }
   const int grid = (int)std::min<long long>(c.sms, units);
   if (grid <= 0) return 0;
+#ifdef TFHE_P3_TRACE
+  static unsigned long long* tbuf = nullptr;
+  if (!tbuf) cudaMalloc(&tbuf, 16 * kPTraceN * 8);
+  cudaMemsetAsync(tbuf, 0, 16 * kPTraceN * 8, st);
+  a.trace = tbuf;
+#endif
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kC1Smem);
     kern<<<grid, kPThreads, kC1Smem, st>>>(a);
   };
   if (inverse) go(ntt_col_kernel<true>);
   else go(ntt_col_kernel<false>);
+#ifdef TFHE_P3_TRACE
+  {
+    std::vector<unsigned long long> hbuf(16 * kPTraceN);
+    cudaMemcpy(hbuf.data(), tbuf, hbuf.size() * 8, cudaMemcpyDeviceToHost);
+    static int seq = 0;
+    char fn[256];
+    snprintf(fn, sizeof(fn), "gpurun_out/ptrace_%d.bin", seq++);
+    if (FILE* f = fopen(fn, "wb")) {
+      fwrite(hbuf.data(), 8, hbuf.size(), f);
+      fclose(f);
+    }
+  }
+#endif
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("p3 column pass launch: ") + cudaGetErrorString(e));
