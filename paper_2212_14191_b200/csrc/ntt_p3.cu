@@ -56,7 +56,9 @@ constexpr int kPItems = 22;                      // ceil(64 warp items / 3 produ
 
 
 // ---- pass 1 shared memory: T 16 KB | H' 4 KB | raw 32 KB | A1 2 x (2 tiles) | A2 (2 tiles)
-constexpr int kC1T = 16384, kC1H = 64 * 32 * 4;   // T | outer twist beta[i2][b2]
+// T | beta[i2][b2] (column part of the outer Hadamard) | c[i2][33] (row part,
+// padded rows) | H'[b1][a2] (inner Hadamard)
+constexpr int kC1T = 16384, kC1H = 64 * 32 * 4 + 64 * 33 * 4 + 32 * 32 * 4;
 constexpr int kC1A = 2 * kPTile + 16;            // two M tiles (+16 B: tile 1 on other banks)
 constexpr int kC1Smem = kC1T + kC1H + kPRaw + 2 * kC1A + kC1A + 32 * 8;
 // ---- pass 2 shared memory: T2 64 KB | raw 32 KB | A 2 x (2 K-steps)
@@ -66,8 +68,8 @@ constexpr int kC2Smem = kC2T + kPRaw + 2 * kC2A + 32 * 8;
 
 struct ColArgs {
   const uint8_t* tab;      // [prime] 16 KB: T (B operand, 4 planes x 128 rows x 32 K)
-  const uint32_t* hin;     // [prime][b1][a2][i2] H'[b1][a2] c[i2][b1] R (inner x row part of outer)
-  const uint32_t* hout;    // [prime][i2][b2] beta R (column part of the outer Hadamard)
+  const uint32_t* hin;     // unused
+  const uint32_t* hout;    // [prime] beta[i2][b2] R | c[i2][33] R | H'[b1][a2] R (kC1H bytes)
   uint32_t* P;             // P^T workspace: [limb][member][i2][k1]
   const PrimeConst* pc;
   int batch, units;
@@ -239,6 +241,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
         if (tid == 0) {
           if (prev_limb >= 0) {
             mbar_wait(tw_empty, tw_ph);
+            mbar_wait(epiA_done, tw_ph);
             mbar_wait(epiB_done, tw_ph);
           }
           const int pr = a.map.prime[limb];
@@ -349,16 +352,16 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
       }
       const int pr = a.map.prime[pos.limb];
       const PrimeConst pc = a.pc[pr];
-      // H''[b1][a2][i2 = 8 cb + t]: lanes read 32-byte runs of 8 consecutive i2
-      const uint32_t* hrow = a.hin + ((size_t)pr * 1024 + a2) * 64 + 8 * pos.cb + t;
+      // row part c[i2 = 8 cb + t][b1] of the outer Hadamard (padded rows: the 8
+      // columns t of a warp hit 8 banks) and the inner Hadamard H'[b1][a2]
+      const uint32_t* crow = sH + 64 * 32 + (8 * pos.cb + t) * 33;
+      const uint32_t* hcol = sH + 64 * 32 + 64 * 33 + a2;
       mbar_wait(accA_full, it & 1);
       PTRACE(6, it);
       tc_fence_after();
 #pragma unroll 1
       for (int g = 0; g < 2; ++g) {
-        uint32_t acc[4][16], hv[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) hv[e] = __ldg(hrow + (size_t)(16 * g + e) * 32 * 64);
+        uint32_t acc[4][16];
 #pragma unroll
         for (int i = 0; i < 4; ++i) tmem_ld16(tmem + lane_off + tau * 128 + i * 32 + 16 * g, acc[i]);
         tmem_ld_wait();
@@ -370,7 +373,8 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const uint32_t s = fold4_m(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
-          p[e] = mont_l(s, hv[e], pc);   // H''[b1][a2][i2] R
+          const int b1 = 16 * g + e;
+          p[e] = mont_l(mont_l(s, hcol[b1 * 32], pc), crow[b1], pc);   // S H' c
         }
         uint32_t pl[4][4];
 #pragma unroll
@@ -821,7 +825,7 @@ int build_p3_tables(Ctx& c) {
     if (q <= (1u << 20)) return 0;   // Montgomery folds only
   const int np = c.n_primes;
   std::vector<uint8_t> t1((size_t)np * kC1T), t2((size_t)np * kC2T), t2ks;
-  std::vector<uint32_t> hin((size_t)np * 1024 * 64), hout((size_t)np * 64 * 32);
+  std::vector<uint32_t> hin(1), hout((size_t)np * (kC1H / 4));
   for (int inv = 0; inv < 2; ++inv) {
     if (!inv) t2ks.assign(t2.size(), 0);
     for (int p = 0; p < np; ++p) {
@@ -851,20 +855,23 @@ int build_p3_tables(Ctx& c) {
       //   inverse c = psi^-((2 i2 + 1) b1), beta = psi^-(32 (2 i2 + 1) b2)
       // c scales the stage-B input row (t, b1), so it rides in the inner
       // Hadamard; beta is applied per output column by the stage-B epilogue
+      uint32_t* ht = hout.data() + (size_t)p * (kC1H / 4);
+      for (int i2 = 0; i2 < kPn2; ++i2)
+        for (int b2 = 0; b2 < 32; ++b2) {
+          const uint32_t bv = inv ? P(32ull * (2 * i2 + 1) * b2) : P(64ull * i2 * b2);
+          ht[i2 * 32 + b2] = mulmod_p(bv, R, q);
+        }
+      for (int i2 = 0; i2 < kPn2; ++i2)
+        for (int b1 = 0; b1 < 32; ++b1) {
+          const uint32_t cv = inv ? P((2ull * i2 + 1) * b1) : P((2ull * b1 + 1) * i2);
+          ht[64 * 32 + i2 * 33 + b1] = mulmod_p(cv, R, q);
+        }
       for (int b1 = 0; b1 < 32; ++b1)
         for (int a2 = 0; a2 < 32; ++a2) {
           // inner Hadamard: forward psi^(64 (2 b1 + 1) a2), inverse psi^-(128 a2 b1)
           const uint32_t h = mulmod_p(inv ? P(128ull * a2 * b1) : P(64ull * (2 * b1 + 1) * a2),
                                       twi[a2], q);
-          for (int i2 = 0; i2 < kPn2; ++i2) {
-            const uint32_t cv = inv ? P((2ull * i2 + 1) * b1) : P((2ull * b1 + 1) * i2);
-            hin[(((size_t)p * 32 + b1) * 32 + a2) * 64 + i2] = mulmod_p(mulmod_p(h, cv, q), R, q);
-          }
-        }
-      for (int i2 = 0; i2 < kPn2; ++i2)
-        for (int b2 = 0; b2 < 32; ++b2) {
-          const uint32_t bv = inv ? P(32ull * (2 * i2 + 1) * b2) : P(64ull * i2 * b2);
-          hout[((size_t)p * kPn2 + i2) * 32 + b2] = mulmod_p(bv, R, q);
+          ht[64 * 32 + 64 * 33 + b1 * 32 + a2] = mulmod_p(h, R, q);
         }
       // pass 2 (64-point rows): forward psi^(2048 k2 i2), inverse
       // psi^-(1024 (2 i2 + 1) k2) n^-1 (row twist on the output k2)
