@@ -60,7 +60,7 @@ constexpr int kPItems = 22;                      // ceil(64 warp items / 3 produ
 // padded rows) | H'[b1][a2] (inner Hadamard)
 constexpr int kC1T = 16384, kC1H = 64 * 32 * 4 + 64 * 33 * 4 + 32 * 32 * 4;
 constexpr int kC1A = 2 * kPTile + 16;            // two M tiles (+16 B: tile 1 on other banks)
-constexpr int kC1Smem = kC1T + kC1H + kPRaw + 2 * kC1A + kC1A + 32 * 8;
+constexpr int kC1Smem = kC1T + kC1H + kPRaw + 2 * kC1A + 2 * kC1A + 32 * 8;
 // ---- pass 2 shared memory: T2 64 KB | raw 32 KB | A 2 x (2 K-steps)
 constexpr int kC2T = 65536;
 constexpr int kC2A = 2 * kPTile;                 // K = 64: two K-steps of one M tile
@@ -138,23 +138,23 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
   uint32_t* sH = reinterpret_cast<uint32_t*>(smem + kC1T);
   uint8_t* sRaw = smem + kC1T + kC1H;
   uint8_t* sA1 = sRaw + kPRaw;                  // [2] buffers of two M tiles
-  uint8_t* sA2 = sA1 + 2 * kC1A;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sA2 + kC1A);
+  uint8_t* sA2 = sA1 + 2 * kC1A;                // [2] buffers (stage B operand)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sA2 + 2 * kC1A);
   uint64_t* raw_full = bar + 0;
   uint64_t* raw_empty = bar + 1;
   uint64_t* a1_full = bar + 2;     // [2]
   uint64_t* a1_empty = bar + 4;    // [2]
   uint64_t* accA_full = bar + 6;
   uint64_t* accA_empty = bar + 7;
-  uint64_t* a2_full = bar + 8;
-  uint64_t* a2_empty = bar + 9;
   uint64_t* accB_full = bar + 10;
   uint64_t* accB_empty = bar + 11;
   uint64_t* tw_full = bar + 12;
   uint64_t* tw_empty = bar + 13;
   uint64_t* epiA_done = bar + 14;
   uint64_t* epiB_done = bar + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* a2_full = bar + 16;    // [2]
+  uint64_t* a2_empty = bar + 18;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int u0 = (int)((long long)a.units * blockIdx.x / gridDim.x);
@@ -168,8 +168,10 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
     }
     mbar_init(accA_full, 1);
     mbar_init(accA_empty, 256);
-    mbar_init(a2_full, 256);
-    mbar_init(a2_empty, 1);
+    for (int s2 = 0; s2 < 2; ++s2) {
+      mbar_init(&a2_full[s2], 256);
+      mbar_init(&a2_empty[s2], 1);
+    }
     mbar_init(accB_full, 1);
     mbar_init(accB_empty, 128);
     mbar_init(tw_full, 1);
@@ -291,14 +293,15 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
     };
     UPos pos2 = p0;
     auto stageB = [&](int v) {
-      mbar_wait(a2_full, v & 1);
+      const int b2f = v & 1;
+      mbar_wait(&a2_full[b2f], (v >> 1) & 1);
       PTRACE(4, v);
       if (v >= 1) mbar_wait(accB_empty, (v - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        issue(smem_u32(sA2), tmem + 256);
+        issue(smem_u32(sA2 + b2f * kC1A), tmem + 256);
         PTRACE(5, v);
-        mma_commit(a2_empty);
+        mma_commit(&a2_empty[b2f]);
         mma_commit(accB_full);
         if (last_of_limb(pos2, v)) mma_commit(tw_empty);
       }
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
     const int q = warp & 3, tau = (warp - 4) >> 2;
     const int m = 128 * tau + 32 * q + lane, a2 = m >> 3, t = m & 7;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    uint8_t* a2t = sA2 + (t >> 2) * (kPTile + 16);   // stage-B tile of this column
+    uint8_t* a2t0 = sA2 + (t >> 2) * (kPTile + 16);  // stage-B tile of this column (buffer 0)
     const int mb = 32 * (t & 3);                      // its rows m' = mb + b1
     int prev_limb = -1;
     uint32_t tw_ph = 0;
@@ -384,15 +387,15 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
 #pragma unroll
           for (int j = 0; j < 4; ++j) pl[j][e4] = w[j];
         }
-        if (g == 0 && it >= 1) mbar_wait(a2_empty, (it - 1) & 1);
+        if (g == 0 && it >= 2) mbar_wait(&a2_empty[it & 1], ((it >> 1) - 1) & 1);
         if (g == 0) PTRACE(7, it);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          *reinterpret_cast<uint4*>(a2t + p_off(0, j, mb + 16 * g, a2)) =
+          *reinterpret_cast<uint4*>(a2t0 + (it & 1) * kC1A + p_off(0, j, mb + 16 * g, a2)) =
               make_uint4(pl[j][0], pl[j][1], pl[j][2], pl[j][3]);
       }
       fence_proxy_async_smem();
-      mbar_arrive(a2_full);
+      mbar_arrive(&a2_full[it & 1]);
       PTRACE(8, it);
       if (last_of_limb(pos, it)) mbar_arrive(epiA_done);
     }
