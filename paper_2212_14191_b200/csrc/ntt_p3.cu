@@ -653,7 +653,9 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
         tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-          y[cc + e] = corr_q(fold4_m(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc), pc.q);
+          y[cc + e] = MODE == EPI_KS_ACC   // the grouped key switch takes y lazy in [0, 2q)
+                          ? fold4_m(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc)
+                          : corr_q(fold4_m(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc), pc.q);
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
@@ -689,6 +691,8 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
         // read at the group's start (init_acc) and written once at its end.
         // A slice's own target row is skipped (reused unchanged, ckks.py:361-364).
         const size_t arow = ((size_t)a.map.out_row[limb] * a.batch + pos.b) * kPN + pos0;
+        const bool lazy = pc.q < (1u << 30);   // warp-uniform: one prime per unit
+        const uint32_t q2 = 2 * pc.q;
         if (pos.sl == 0) {
           if (a.epi.init_acc[limb]) {
 #pragma unroll
@@ -713,18 +717,29 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
               kbv[e] = __ldg(kb + (cc + e) * kPn1);
               kav[e] = __ldg(ka + (cc + e) * kPn1);
             }
+            if (lazy) {
+              // q < 2^30: the sums stay in [0, 2q) (< 2^31), one unsigned min per add
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              sb[cc + e] = add_mod(sb[cc + e], corr_q(mont_l(y[cc + e], kbv[e], pc), pc.q), pc.q);
-              sa[cc + e] = add_mod(sa[cc + e], corr_q(mont_l(y[cc + e], kav[e], pc), pc.q), pc.q);
+              for (int e = 0; e < 8; ++e) {
+                const uint32_t tb = sb[cc + e] + mont_l(y[cc + e], kbv[e], pc);
+                const uint32_t ta = sa[cc + e] + mont_l(y[cc + e], kav[e], pc);
+                sb[cc + e] = min(tb, tb - q2);
+                sa[cc + e] = min(ta, ta - q2);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                sb[cc + e] = add_mod(sb[cc + e], corr_q(mont_l(y[cc + e], kbv[e], pc), pc.q), pc.q);
+                sa[cc + e] = add_mod(sa[cc + e], corr_q(mont_l(y[cc + e], kav[e], pc), pc.q), pc.q);
+              }
             }
           }
         }
         if (pos.sl + 1 == S) {
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            a.epi.acc_b[arow + (size_t)e * kPn1] = sb[e];
-            a.epi.acc_a[arow + (size_t)e * kPn1] = sa[e];
+            a.epi.acc_b[arow + (size_t)e * kPn1] = corr_q(sb[e], pc.q);   // [0, 2q) -> [0, q)
+            a.epi.acc_a[arow + (size_t)e * kPn1] = corr_q(sa[e], pc.q);
           }
         }
       } else {   // EPI_KS_MAC: y arrives as y R (the table carries R^2)
