@@ -42,6 +42,10 @@ uint32_t powmod(uint64_t b, uint64_t e, uint32_t q) {
 }
 uint32_t invmod(uint64_t a, uint32_t q) { return powmod(a % q, q - 2, q); }
 uint32_t shoup(uint32_t w, uint32_t q) { return (uint32_t)(((uint64_t)w << 32) / q); }
+bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && *e && *e != '0';
+}
 
 // bump allocator over the caller's workspace
 struct Carve {
@@ -252,10 +256,22 @@ int moddown_rescale(const Ctx& c, const CkksGeom& g, uint32_t* acc, const uint32
 // rs_scratch != NULL fuses the rescale that follows (tfhe_hmult_rescale): out is
 // then (2, level, B, n) = rescale(ModDown(.)) bit for bit, and rs_scratch (>= 2
 // rows, dead after ModUp) holds the top row's coefficient form.
+//
+// rot != NULL is the hoisted HROTATE (ckks.py:276-282): d is the
+// UNrotated a (or phi(a) when rot->d_is_phi) and rot->b the unrotated b; phi_t
+// is never materialised.  INTT(phi(a)) = phi_coeff(INTT(a)) is the INTT's own
+// output scatter, the slice rows' MAC gathers phi(a) and folds P phi(b) into
+// acc_b, so ModDown's (acc_b - y) P^-1 = phi(b) + ksb with no addend pass.
+struct RotHoist {
+  uint32_t t;
+  const uint32_t* b;
+  int d_is_phi;   // 1: d already holds phi(a) (planes without the output scatter)
+};
+
 int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int level, int batch,
                    const uint32_t* key, int dnum, int r0, int nr, uint32_t* out,
                    const uint32_t* base, const int16_t* base_rows, Carve& cv, cudaStream_t st,
-                   uint32_t* rs_scratch = nullptr) {
+                   uint32_t* rs_scratch = nullptr, const RotHoist* rot = nullptr) {
   const Ctx& c = h->c;
   CkksGeom g = geom(h, level, dnum, r0, nr);
   set_group(g, c, batch);
@@ -278,6 +294,10 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
   }
   const size_t key_pair = (size_t)2 * (g.Lc + g.K) * c.n;  // elements per (b_j, a_j)
   int rc;
+  if (rot && (!c.use_ts || y_full || rs_scratch || base || (!rot->d_is_phi && !c.use_p3))) {
+    set_error("hoisted rotation: unsupported key-switch configuration");
+    return TFHE_EINVAL;
+  }
 
   // 1. y = INTT(d), every limb of the level  (ModUp's to_coeff, ckks.py:362)
   if (!y_full) {
@@ -288,7 +308,13 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
     LimbMap m;
     m.n = g.l1;
     for (int r = 0; r < g.l1; ++r) m.prime[r] = m.in_row[r] = m.out_row[r] = (int16_t)r;
-    if ((rc = launch_ntt(c, d, y, m, batch, 1, nullptr, ntt_ws, ntt_ws_bytes, st))) return rc;
+    EpiArgs es;   // hoisted rotation: y = phi_coeff(INTT(a)) by the INTT's output scatter
+    memset(&es, 0, sizeof(es));
+    es.mode = EPI_STORE;
+    es.scatter_t = rot && !rot->d_is_phi ? rot->t : 0u;
+    if ((rc = launch_ntt(c, d, y, m, batch, 1, es.scatter_t ? &es : nullptr, ntt_ws, ntt_ws_bytes,
+                         st)))
+      return rc;
     y_full = y;
   }
 
@@ -302,9 +328,23 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
       const int r = g.r0 + t;
       key_off[t] = (int64_t)(r / g.alpha) * key_pair + (int64_t)r * c.n;
     }
-    if ((rc = launch_ks_mac(c, d, key, key + key_pair / 2, acc, acc + g.T * U, row_prime, key_off,
-                            g.nr, batch, 1, st)))
+    if (rot) {
+      // acc_b = phi(a) k_b + P phi(b), acc_a = phi(a) k_a (phi gathered in the MAC)
+      uint32_t pmod[kMaxRows];
+      for (int t = 0; t < g.nr; ++t) {
+        const uint32_t q = c.primes[g.r0 + t];
+        uint64_t pm = 1;
+        for (int k = 0; k < g.K; ++k) pm = pm * (c.primes[g.Lc + k] % q) % q;
+        pmod[t] = (uint32_t)pm;
+      }
+      if ((rc = launch_ks_mac_rot(c, d, rot->b, key, key + key_pair / 2, acc, acc + g.T * U,
+                                  row_prime, key_off, pmod, g.nr, batch, rot->t, !rot->d_is_phi,
+                                  st)))
+        return rc;
+    } else if ((rc = launch_ks_mac(c, d, key, key + key_pair / 2, acc, acc + g.T * U, row_prime,
+                                   key_off, g.nr, batch, 1, st))) {
       return rc;
+    }
     // 2b. groups of S slices: stage 1 for every (slice, target) pair, stage 2
     // accumulates the S slices of each target on chip (EPI_KS_ACC).  A
     // slice's own rows are skipped in the sum (they were reused in 2a).
@@ -866,13 +906,33 @@ int tfhe_hrotate(TfheCtx* h, const uint32_t* ct, int level, int batch, uint32_t 
   const int l1 = level + 1;
   const size_t P = (size_t)l1 * batch * h->c.n;
   Carve cv{static_cast<uint8_t*>(ws), ws_bytes};
+  int16_t rp[kMaxRows];
+  for (int i = 0; i < 2 * l1; ++i) rp[i] = (int16_t)(i % l1);
+  const Ctx& c = h->c;
+  if (c.use_ts && !getenv_flag("TFHE_NO_HOIST")) {
+    // hoisted automorphism: phi(b) folds into the key switch's
+    // slice MAC; phi(a) is the INTT's output scatter on the p3 plan, a gather
+    // of a alone on the TS plans (2^14, 2^15)
+    RotHoist rot{galois_t, ct, 0};
+    const uint32_t* d = ct + P;
+    if (!c.use_p3) {
+      uint32_t* phia = cv.take<uint32_t>(P * 4);
+      if (!cv.ok) {
+        set_error("ckks workspace too small");
+        return TFHE_EINVAL;
+      }
+      if ((rc = launch_automorph(c, ct + P, phia, galois_t, 1, rp, l1, batch, st))) return rc;
+      d = phia;
+      rot.d_is_phi = 1;
+    }
+    return keyswitch_impl(h, d, nullptr, level, batch, key, dnum, 0, l1, out, nullptr, nullptr, cv,
+                          st, nullptr, &rot);
+  }
   uint32_t* phi = cv.take<uint32_t>(2 * P * 4);
   if (!cv.ok) {
     set_error("ckks workspace too small");
     return TFHE_EINVAL;
   }
-  int16_t rp[kMaxRows];
-  for (int i = 0; i < 2 * l1; ++i) rp[i] = (int16_t)(i % l1);
   if ((rc = launch_automorph(h->c, ct, phi, galois_t, 1, rp, 2 * l1, batch, st))) return rc;
   int16_t rows[kMaxLimbs];
   for (int i = 0; i < l1; ++i) {

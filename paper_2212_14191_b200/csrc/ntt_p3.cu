@@ -660,9 +660,21 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
       if (MODE == EPI_STORE) {
-        uint32_t* o = a.out + orow;
+        if (a.epi.scatter_t) {
+          // hoisted HROTATE: the INTT output lands permuted by x -> x^t
+          // (kernels.py:97-107); coefficient i goes to t i mod 2n, negated past n
+          uint32_t* o = a.out + ((size_t)a.map.out_row[limb] * a.batch + pos.b) * kPN;
+          const uint32_t tt = a.epi.scatter_t;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) o[e * kPn1] = y[e];
+          for (int e = 0; e < 32; ++e) {
+            const uint32_t j = (tt * (uint32_t)(pos0 + (size_t)e * kPn1)) & (2 * kPN - 1);
+            o[j & (kPN - 1)] = j >= (uint32_t)kPN ? (y[e] ? pc.q - y[e] : 0u) : y[e];
+          }
+        } else {
+          uint32_t* o = a.out + orow;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e * kPn1] = y[e];
+        }
       } else if (MODE == EPI_SUB_SCALE) {
         const uint32_t* xs = a.epi.x + ((size_t)a.epi.x_row[limb] * a.batch + pos.b) * kPN + pos0;
         const int br = a.epi.base_row[limb];

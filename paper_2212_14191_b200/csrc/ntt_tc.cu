@@ -930,6 +930,10 @@ int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& m
     set_error("ntt workspace too small");
     return 2;
   }
+  if (epi && epi->scatter_t && !(c.use_p3 && inverse && epi->mode == EPI_STORE)) {
+    set_error("output automorphism needs the N = 2^16 inverse transform");
+    return 2;
+  }
   if (c.use_p3 && !(epi && epi->mode == EPI_KS_ACC))
     return launch_ntt_p3(c, in, out, map, batch, inverse, epi, ws, st);
   if (c.use_ts) return launch_ntt_ts(c, in, out, map, batch, inverse, epi, ws, st);

@@ -116,6 +116,7 @@ __global__ void tensor_kernel(const uint32_t* __restrict__ b0, const uint32_t* _
 struct MacArgs {
   int16_t prime[kMaxRows];
   int64_t key_off[kMaxRows];  // element offset of this row's key row (from kb / ka)
+  uint32_t pmod[kMaxRows], pmod_shoup[kMaxRows];   // ks_mac_rot: P mod q_r
 };
 
 // acc_b[r] (+)= x[r] * kb[key_row[r]], acc_a[r] (+)= x[r] * ka[key_row[r]];
@@ -142,6 +143,57 @@ __global__ void ks_mac_kernel(const uint32_t* __restrict__ x, const uint32_t* __
   oa.c = add_mod(oa.c, mul_mod(v.c, wa.c, pc.q, pc.mu), pc.q);
     TFHE_MAC(x) TFHE_MAC(y) TFHE_MAC(z) TFHE_MAC(w)
 #undef TFHE_MAC
+    st4(acc_b + o, ob);
+    st4(acc_a + o, oa);
+  }
+}
+
+// Hoisted HROTATE (ckks.py:276-282): the slice-row MAC of the key switch and
+// the addend phi(b) in one pass, phi never materialised:
+//   acc_b[r] = phi(x)[r] * kb[key_row[r]] + P_r * phi(base)[r]
+//   acc_a[r] = phi(x)[r] * ka[key_row[r]]
+// with phi(v)[k] = v[((t (2k+1) mod 2n) - 1) / 2] (kernels.py:77-85) and P_r
+// the product of the specials mod q_r, so that ModDown's (acc_b - y) P^-1 is
+// phi(b) + ksb bit for bit.  perm_x = 0: x already holds phi(x).
+__global__ void ks_mac_rot_kernel(const uint32_t* __restrict__ x, const uint32_t* __restrict__ base,
+                                  const uint32_t* __restrict__ kb, const uint32_t* __restrict__ ka,
+                                  uint32_t* __restrict__ acc_b, uint32_t* __restrict__ acc_a,
+                                  const PrimeConst* __restrict__ pcs,
+                                  const __grid_constant__ MacArgs ma, int batch, int log_n,
+                                  uint32_t t, int perm_x) {
+  const int row = blockIdx.y;
+  const PrimeConst pc = pcs[ma.prime[row]];
+  const int n = 1 << log_n;
+  const int64_t per_row = (int64_t)batch * n;
+  const int64_t rbase = (int64_t)row * per_row;
+  const uint32_t* kbr = kb + ma.key_off[row];
+  const uint32_t* kar = ka + ma.key_off[row];
+  const uint32_t pm = ma.pmod[row], pms = ma.pmod_shoup[row];
+  const uint32_t mask = (uint32_t)n - 1, half = (t - 1) >> 1;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+    const int64_t o = rbase + i;
+    const int coef = (int)(i & mask);
+    const int64_t mrow = o - coef;   // this member's row start
+    uint32_t src[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) src[e] = (t * (uint32_t)(coef + e) + half) & mask;
+    const uint4 wb = ld4(kbr + coef), wa = ld4(kar + coef);
+    uint4 v, bv;
+    if (perm_x) {
+      v = make_uint4(__ldg(x + mrow + src[0]), __ldg(x + mrow + src[1]), __ldg(x + mrow + src[2]),
+                     __ldg(x + mrow + src[3]));
+    } else {
+      v = ld4(x + o);
+    }
+    bv = make_uint4(__ldg(base + mrow + src[0]), __ldg(base + mrow + src[1]),
+                    __ldg(base + mrow + src[2]), __ldg(base + mrow + src[3]));
+    uint4 ob, oa;
+#define TFHE_MACR(c)                                                               \
+  ob.c = add_mod(mul_mod(v.c, wb.c, pc.q, pc.mu), mul_shoup(bv.c, pm, pms, pc.q), pc.q); \
+  oa.c = mul_mod(v.c, wa.c, pc.q, pc.mu);
+    TFHE_MACR(x) TFHE_MACR(y) TFHE_MACR(z) TFHE_MACR(w)
+#undef TFHE_MACR
     st4(acc_b + o, ob);
     st4(acc_a + o, oa);
   }
@@ -334,6 +386,29 @@ int launch_ks_mac(const Ctx& c, const uint32_t* x, const uint32_t* kb, const uin
   dim3 g = grid_rows((int64_t)batch * c.n, rows, 256);
   ks_mac_kernel<<<g, 256, 0, st>>>(x, kb, ka, acc_b, acc_a, c.d_pc, ma, batch, c.n, first);
   return check("ks mac kernel");
+}
+
+int launch_ks_mac_rot(const Ctx& c, const uint32_t* x, const uint32_t* base, const uint32_t* kb,
+                      const uint32_t* ka, uint32_t* acc_b, uint32_t* acc_a,
+                      const int16_t* row_prime, const int64_t* key_off, const uint32_t* pmod,
+                      int rows, int batch, uint32_t t, int perm_x, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  if (rows > kMaxRows || (t & 1) == 0) {
+    set_error("ks_mac_rot: too many rows or even galois element");
+    return 2;
+  }
+  MacArgs ma;
+  for (int r = 0; r < rows; ++r) {
+    ma.prime[r] = row_prime[r];
+    ma.key_off[r] = key_off[r];
+    const uint32_t q = c.primes[row_prime[r]];
+    ma.pmod[r] = pmod[r] % q;
+    ma.pmod_shoup[r] = (uint32_t)(((uint64_t)ma.pmod[r] << 32) / q);
+  }
+  dim3 g = grid_rows((int64_t)batch * c.n, rows, 256);
+  ks_mac_rot_kernel<<<g, 256, 0, st>>>(x, base, kb, ka, acc_b, acc_a, c.d_pc, ma, batch, c.log_n,
+                                       t & (2u * c.n - 1), perm_x);
+  return check("ks mac rot kernel");
 }
 
 int launch_md_rescale_prep(const Ctx& c, uint32_t* acc, const uint32_t* base, const uint32_t* conv,

@@ -30,6 +30,12 @@ int launch_tensor(const Ctx& c, const uint32_t* b0, const uint32_t* a0, const ui
 int launch_ks_mac(const Ctx& c, const uint32_t* x, const uint32_t* kb, const uint32_t* ka,
                   uint32_t* acc_b, uint32_t* acc_a, const int16_t* row_prime,
                   const int64_t* key_off, int rows, int batch, int first, cudaStream_t st);
+// hoisted HROTATE slice MAC: acc_b = phi_t(x) kb + pmod phi_t(base), acc_a = phi_t(x) ka
+// (NTT-domain phi; perm_x = 0 reads x unpermuted)
+int launch_ks_mac_rot(const Ctx& c, const uint32_t* x, const uint32_t* base, const uint32_t* kb,
+                      const uint32_t* ka, uint32_t* acc_b, uint32_t* acc_a,
+                      const int16_t* row_prime, const int64_t* key_off, const uint32_t* pmod,
+                      int rows, int batch, uint32_t t, int perm_x, cudaStream_t st);
 int launch_automorph(const Ctx& c, const uint32_t* in, uint32_t* out, uint32_t t, int ntt_domain,
                      const int16_t* row_prime, int rows, int batch, cudaStream_t st);
 int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,

@@ -66,6 +66,10 @@ struct EpiArgs {
   int16_t js[kMaxLimbs];    // slice that owns target row l (-1: none) -> skipped
   int16_t init_acc[kMaxLimbs];  // 1: start from acc, 0: start from zero
   int ks_lazy;                  // slice products summed in 64 bits between reductions
+  // EPI_STORE of an inverse transform: != 0 applies the coefficient-domain
+  // automorphism x -> x^t to the output (coefficient i lands at t i mod 2n,
+  // negated past n; kernels.py:97-107) -- the hoisted HROTATE (p3 plan only)
+  uint32_t scatter_t;
 };
 
 struct Ctx {

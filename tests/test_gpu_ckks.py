@@ -233,3 +233,38 @@ def test_fused_hmult_rescale_batched(kind, level, batch):
     one = ctx.hmult_rescale_batch(CiphertextBatch(d(c0), level), CiphertextBatch(d(c1), level), tk)
     assert one.level == two.level == level - 1
     assert torch.equal(one.data, two.data)
+
+
+@pytest.mark.parametrize("kind,level,batch", [("n16", 3, 3), ("set_c", 5, 2),
+                                              ("n14_31b", 5, 2), ("p_dnum5", 6, 2)])
+def test_hoisted_rotation(kind, level, batch, monkeypatch):
+    """HROTATE / HCONJUGATE with the automorphism hoisted into the key switch
+    (phi(b) folded into the slice MAC, phi(a) the INTT's output scatter on the
+    N=2^16 plan) equal the materialised-phi path (TFHE_NO_HOIST) bit for bit,
+    for small and large galois elements, and member 1 equals the oracle's
+    hrotate (ckks.py:276-289)."""
+    import torch
+    from oracle import oracle as O
+    from paper_2212_14191_b200.ckks import CiphertextBatch
+    ctx = _ctx(kind)
+    p = ctx.params
+    rng = np.random.default_rng(1300 + level)
+    basis = tuple(p.chain.q[:level + 1])
+    c0 = np.stack([synth.rows(rng, basis, (batch, p.n)) for _ in range(2)])
+    key = synth.switching_key(rng, p.chain.q, p.chain.p, p.n, p.dnum)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()  # noqa
+    tk = d(key)
+    ct = CiphertextBatch(d(c0), level)
+    for r in (1, 5, p.n // 2 - 3, "conj"):
+        run = ((lambda: ctx.hconjugate_batch(ct, tk)) if r == "conj"
+               else (lambda: ctx.hrotate_batch(ct, r, tk)))
+        hoisted = run().data.clone()
+        monkeypatch.setenv("TFHE_NO_HOIST", "1")
+        plain = run().data
+        monkeypatch.delenv("TFHE_NO_HOIST")
+        assert torch.equal(hoisted, plain), f"hoisted != materialised phi at r={r}"
+        if r == 5:
+            got = hoisted.cpu().numpy().view(np.uint32)
+            ob, oa = O.hrotate(c0[0][:, 1], c0[1][:, 1], r, basis, key, p.chain.q, p.chain.p,
+                               p.alpha, p.dnum)
+            assert np.array_equal(got[0, :, 1], ob) and np.array_equal(got[1, :, 1], oa)
