@@ -58,7 +58,10 @@ constexpr int kPItems = 22;                      // ceil(64 warp items / 3 produ
 // ---- pass 1 shared memory: T 16 KB | H' 4 KB | raw 32 KB | A1 2 x (2 tiles) | A2 (2 tiles)
 // T | beta[i2][b2] (column part of the outer Hadamard) | c[i2][33] (row part,
 // padded rows) | H'[b1][a2] (inner Hadamard)
-constexpr int kC1T = 16384, kC1H = 64 * 32 * 4 + 64 * 33 * 4 + 32 * 32 * 4;
+// H block words: beta[i2][b2] | c[i2][33] R | H'[b1][a2] | beta Shoup | H' Shoup
+constexpr int kHBeta = 0, kHC = 64 * 32, kHIn = kHC + 64 * 33, kHBetaS = kHIn + 32 * 32,
+              kHInS = kHBetaS + 64 * 32, kHWords = kHInS + 32 * 32;
+constexpr int kC1T = 16384, kC1H = kHWords * 4;
 constexpr int kC1A = 2 * kPTile + 16;            // two M tiles (+16 B: tile 1 on other banks)
 constexpr int kC1Smem = kC1T + kC1H + kPRaw + 2 * kC1A + 2 * kC1A + 32 * 8;
 // ---- pass 2 shared memory: T2 64 KB | raw 32 KB | A 2 x (2 K-steps)
@@ -69,7 +72,7 @@ constexpr int kC2Smem = kC2T + kPRaw + 2 * kC2A + 32 * 8;
 struct ColArgs {
   const uint8_t* tab;      // [prime] 16 KB: T (B operand, 4 planes x 128 rows x 32 K)
   const uint32_t* hin;     // unused
-  const uint32_t* hout;    // [prime] beta[i2][b2] R | c[i2][33] R | H'[b1][a2] R (kC1H bytes)
+  const uint32_t* hout;    // [prime] H block (kHWords): beta, c R, H' and Shoup companions
   uint32_t* P;             // P^T workspace: [limb][member][i2][k1]
   const PrimeConst* pc;
   int batch, units;
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
           const int pr = a.map.prime[limb];
           mbar_arrive_expect_tx(tw_full, kC1T + kC1H);
           bulk_g2s(sT, a.tab + (size_t)pr * kC1T, kC1T, tw_full);
-          bulk_g2s(sH, a.hout + (size_t)pr * (kC1H / 4), kC1H, tw_full);
+          bulk_g2s(sH, a.hout + (size_t)pr * kHWords, kC1H, tw_full);
         }
         if (prev_limb >= 0) tw_ph ^= 1;
         prev_limb = limb;
@@ -357,8 +360,9 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
       const PrimeConst pc = a.pc[pr];
       // row part c[i2 = 8 cb + t][b1] of the outer Hadamard (padded rows: the 8
       // columns t of a warp hit 8 banks) and the inner Hadamard H'[b1][a2]
-      const uint32_t* crow = sH + 64 * 32 + (8 * pos.cb + t) * 33;
-      const uint32_t* hcol = sH + 64 * 32 + 64 * 33 + a2;
+      const uint32_t* crow = sH + kHC + (8 * pos.cb + t) * 33;
+      const uint32_t* hcol = sH + kHIn + a2;
+      const uint32_t* hcols = sH + kHInS + a2;
       mbar_wait(accA_full, it & 1);
       PTRACE(6, it);
       tc_fence_after();
@@ -377,7 +381,8 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
         for (int e = 0; e < 16; ++e) {
           const uint32_t s = fold4_m(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
           const int b1 = 16 * g + e;
-          p[e] = mont_l(mont_l(s, hcol[b1 * 32], pc), crow[b1], pc);   // S H' c
+          // S H' (Shoup, lazy [0, 2q)) c (Montgomery, c carries R)
+          p[e] = mont_l(mul_shoup_lazy(s, hcol[b1 * 32], hcols[b1 * 32], pc.q), crow[b1], pc);
         }
         uint32_t pl[4][4];
 #pragma unroll
@@ -441,15 +446,18 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
 #pragma unroll
       for (int tile = 0; tile < 2; ++tile) {
         const int i2 = 8 * pos.cb + 4 * tile + q;
-        const uint32_t* bt = sH + i2 * 32;
+        const uint32_t* bt = sH + kHBeta + i2 * 32;
+        const uint32_t* bts = sH + kHBetaS + i2 * 32;
         uint32_t* o = a.P + (((size_t)pos.limb * a.batch + pos.b) * kPn2 + i2) * kPn1 + lane;
 #pragma unroll
         for (int b4 = 0; b4 < 8; ++b4) {
+          // lazy Shoup products: P^T in [0, 2q) (the row pass only byte-splits it)
           const uint4 bv = *reinterpret_cast<const uint4*>(bt + 4 * b4);
-          o[32 * (4 * b4)] = mont_l(y[tile][4 * b4], bv.x, pc);
-          o[32 * (4 * b4 + 1)] = mont_l(y[tile][4 * b4 + 1], bv.y, pc);
-          o[32 * (4 * b4 + 2)] = mont_l(y[tile][4 * b4 + 2], bv.z, pc);
-          o[32 * (4 * b4 + 3)] = mont_l(y[tile][4 * b4 + 3], bv.w, pc);
+          const uint4 bs = *reinterpret_cast<const uint4*>(bts + 4 * b4);
+          o[32 * (4 * b4)] = mul_shoup_lazy(y[tile][4 * b4], bv.x, bs.x, pc.q);
+          o[32 * (4 * b4 + 1)] = mul_shoup_lazy(y[tile][4 * b4 + 1], bv.y, bs.y, pc.q);
+          o[32 * (4 * b4 + 2)] = mul_shoup_lazy(y[tile][4 * b4 + 2], bv.z, bs.z, pc.q);
+          o[32 * (4 * b4 + 3)] = mul_shoup_lazy(y[tile][4 * b4 + 3], bv.w, bs.w, pc.q);
         }
       }
       PTRACE(10, it);
@@ -855,7 +863,7 @@ int build_p3_tables(Ctx& c) {
     if (q <= (1u << 20)) return 0;   // Montgomery folds only
   const int np = c.n_primes;
   std::vector<uint8_t> t1((size_t)np * kC1T), t2((size_t)np * kC2T), t2ks;
-  std::vector<uint32_t> hin(1), hout((size_t)np * (kC1H / 4));
+  std::vector<uint32_t> hin(1), hout((size_t)np * kHWords);
   for (int inv = 0; inv < 2; ++inv) {
     if (!inv) t2ks.assign(t2.size(), 0);
     for (int p = 0; p < np; ++p) {
@@ -885,23 +893,26 @@ int build_p3_tables(Ctx& c) {
       //   inverse c = psi^-((2 i2 + 1) b1), beta = psi^-(32 (2 i2 + 1) b2)
       // c scales the stage-B input row (t, b1), so it rides in the inner
       // Hadamard; beta is applied per output column by the stage-B epilogue
-      uint32_t* ht = hout.data() + (size_t)p * (kC1H / 4);
+      uint32_t* ht = hout.data() + (size_t)p * kHWords;
+      auto shoup_p = [&](uint32_t w) { return (uint32_t)(((uint64_t)w << 32) / q); };
       for (int i2 = 0; i2 < kPn2; ++i2)
         for (int b2 = 0; b2 < 32; ++b2) {
           const uint32_t bv = inv ? P(32ull * (2 * i2 + 1) * b2) : P(64ull * i2 * b2);
-          ht[i2 * 32 + b2] = mulmod_p(bv, R, q);
+          ht[kHBeta + i2 * 32 + b2] = bv;   // Shoup operand: no R
+          ht[kHBetaS + i2 * 32 + b2] = shoup_p(bv);
         }
       for (int i2 = 0; i2 < kPn2; ++i2)
         for (int b1 = 0; b1 < 32; ++b1) {
           const uint32_t cv = inv ? P((2ull * i2 + 1) * b1) : P((2ull * b1 + 1) * i2);
-          ht[64 * 32 + i2 * 33 + b1] = mulmod_p(cv, R, q);
+          ht[kHC + i2 * 33 + b1] = mulmod_p(cv, R, q);
         }
       for (int b1 = 0; b1 < 32; ++b1)
         for (int a2 = 0; a2 < 32; ++a2) {
           // inner Hadamard: forward psi^(64 (2 b1 + 1) a2), inverse psi^-(128 a2 b1)
           const uint32_t h = mulmod_p(inv ? P(128ull * a2 * b1) : P(64ull * (2 * b1 + 1) * a2),
                                       twi[a2], q);
-          ht[64 * 32 + 64 * 33 + b1 * 32 + a2] = mulmod_p(h, R, q);
+          ht[kHIn + b1 * 32 + a2] = h;   // Shoup operand: no R
+          ht[kHInS + b1 * 32 + a2] = shoup_p(h);
         }
       // pass 2 (64-point rows): forward psi^(2048 k2 i2), inverse
       // psi^-(1024 (2 i2 + 1) k2) n^-1 (row twist on the output k2)

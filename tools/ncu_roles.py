@@ -5,7 +5,7 @@ usage: ncu_roles.py <ncu source csv (sass, one kernel)> <nvdisasm --print-line-i
 Each SASS instruction is attributed to the last kernel-body line (of ntt_ts.cu,
 outside the helper functions) that precedes it, then binned into the roles.
 """
-import csv, re, sys
+import csv, os, re, sys
 from collections import Counter
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]
@@ -29,7 +29,7 @@ for L in open(sys.argv[2]).read().split("\n"):
     if ".text." in L and L.strip().endswith(":"):
         inside = fn in L
     if not inside: continue
-    m = re.search(r'File ".*ntt_ts.cu", line (\d+)', L)
+    m = re.search(r'File ".*' + re.escape(os.environ.get("SRC", "ntt_ts.cu")) + r'", line (\d+)', L)
     if m and int(m.group(1)) >= body_lo: cur = int(m.group(1))
     m = re.search(r'/\*([0-9a-f]{4,})\*/', L)
     if m and cur is not None: off2line[int(m.group(1), 16)] = cur
