@@ -55,15 +55,24 @@ constexpr int kPProdWarps = 3, kPMmaWarp = 3;
 constexpr int kPItems = 22;                      // ceil(64 warp items / 3 producer warps)
 
 
-// ---- pass 1 shared memory: T 16 KB | H' 4 KB | raw 32 KB | A1 2 x (2 tiles) | A2 (2 tiles)
-// T | beta[i2][b2] (column part of the outer Hadamard) | c[i2][33] (row part,
-// padded rows) | H'[b1][a2] (inner Hadamard)
-// H block words: beta[i2][b2] | c[i2][33] R | H'[b1][a2] | beta Shoup | H' Shoup
-constexpr int kHBeta = 0, kHC = 64 * 32, kHIn = kHC + 64 * 33, kHBetaS = kHIn + 32 * 32,
-              kHInS = kHBetaS + 64 * 32, kHWords = kHInS + 32 * 32;
+// ---- pass 1 shared memory: T 16 KB | H block | raw 32 KB | A1 2 x (2 tiles) | A2 kA2Bufs x (2 tiles)
+// H block words: beta[i2][b2] (column part of the outer Hadamard) | its Shoup |
+// H'T[a2][36] (inner Hadamard, transposed) | its Shoup | c[i2][36] (row part of
+// the outer Hadamard) [| its Shoup].  The stage-A epilogue reads H'T and c as
+// 16-byte vectors (4 outputs b1 per load); the 36-word rows put the 4 (H'T) or
+// 8 (c) rows one warp reads on disjoint banks.
+//   TFHE_P3_CSHOUP = 1: c as a Shoup operand (3 fewer IMAD-pipe cycles per
+//   output than Montgomery) -- its table only fits with one stage-B buffer.
+#ifndef TFHE_P3_CSHOUP
+#define TFHE_P3_CSHOUP 0
+#endif
+constexpr int kA2Bufs = TFHE_P3_CSHOUP ? 1 : 2;
+constexpr int kHBeta = 0, kHBetaS = 64 * 32, kHIn = 2 * 64 * 32, kHInS = kHIn + 32 * 36,
+              kHC = kHInS + 32 * 36, kHCS = kHC + 64 * 36,
+              kHWords = kHC + (TFHE_P3_CSHOUP ? 2 : 1) * 64 * 36;
 constexpr int kC1T = 16384, kC1H = kHWords * 4;
 constexpr int kC1A = 2 * kPTile + 16;            // two M tiles (+16 B: tile 1 on other banks)
-constexpr int kC1Smem = kC1T + kC1H + kPRaw + 2 * kC1A + 2 * kC1A + 32 * 8;
+constexpr int kC1Smem = kC1T + kC1H + kPRaw + 2 * kC1A + kA2Bufs * kC1A + 32 * 8;
 // ---- pass 2 shared memory: T2 64 KB | raw 32 KB | A 2 x (2 K-steps)
 constexpr int kC2T = 65536;
 constexpr int kC2A = 2 * kPTile;                 // K = 64: two K-steps of one M tile
@@ -141,8 +150,8 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
   uint32_t* sH = reinterpret_cast<uint32_t*>(smem + kC1T);
   uint8_t* sRaw = smem + kC1T + kC1H;
   uint8_t* sA1 = sRaw + kPRaw;                  // [2] buffers of two M tiles
-  uint8_t* sA2 = sA1 + 2 * kC1A;                // [2] buffers (stage B operand)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sA2 + 2 * kC1A);
+  uint8_t* sA2 = sA1 + 2 * kC1A;                // [kA2Bufs] buffers (stage B operand)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sA2 + kA2Bufs * kC1A);
   uint64_t* raw_full = bar + 0;
   uint64_t* raw_empty = bar + 1;
   uint64_t* a1_full = bar + 2;     // [2]
@@ -296,8 +305,8 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
     };
     UPos pos2 = p0;
     auto stageB = [&](int v) {
-      const int b2f = v & 1;
-      mbar_wait(&a2_full[b2f], (v >> 1) & 1);
+      const int b2f = v % kA2Bufs;
+      mbar_wait(&a2_full[b2f], (v / kA2Bufs) & 1);
       PTRACE(4, v);
       if (v >= 1) mbar_wait(accB_empty, (v - 1) & 1);
       tc_fence_after();
@@ -358,11 +367,13 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
       }
       const int pr = a.map.prime[pos.limb];
       const PrimeConst pc = a.pc[pr];
-      // row part c[i2 = 8 cb + t][b1] of the outer Hadamard (padded rows: the 8
-      // columns t of a warp hit 8 banks) and the inner Hadamard H'[b1][a2]
-      const uint32_t* crow = sH + kHC + (8 * pos.cb + t) * 33;
-      const uint32_t* hcol = sH + kHIn + a2;
-      const uint32_t* hcols = sH + kHInS + a2;
+      // the inner Hadamard H'[b1][a2] and the row part c[i2 = 8 cb + t][b1] of
+      // the outer Hadamard, 4 consecutive b1 per vector load
+      const uint32_t* hrow = sH + kHIn + a2 * 36;
+      const uint32_t* hrows = sH + kHInS + a2 * 36;
+      const uint32_t* crow = sH + kHC + (8 * pos.cb + t) * 36;
+      const uint32_t* crows = sH + kHCS + (8 * pos.cb + t) * 36;
+      (void)crows;
       mbar_wait(accA_full, it & 1);
       PTRACE(6, it);
       tc_fence_after();
@@ -378,11 +389,28 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
         }
         uint32_t p[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const uint32_t s = fold4_m(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
-          const int b1 = 16 * g + e;
-          // S H' (Shoup, lazy [0, 2q)) c (Montgomery, c carries R)
-          p[e] = mont_l(mul_shoup_lazy(s, hcol[b1 * 32], hcols[b1 * 32], pc.q), crow[b1], pc);
+        for (int e4 = 0; e4 < 4; ++e4) {
+          const int b1 = 16 * g + 4 * e4;
+          const uint4 hv = *reinterpret_cast<const uint4*>(hrow + b1);
+          const uint4 hs = *reinterpret_cast<const uint4*>(hrows + b1);
+          const uint4 cv = *reinterpret_cast<const uint4*>(crow + b1);
+          const uint32_t hva[4] = {hv.x, hv.y, hv.z, hv.w}, hsa[4] = {hs.x, hs.y, hs.z, hs.w};
+          const uint32_t cva[4] = {cv.x, cv.y, cv.z, cv.w};
+#if TFHE_P3_CSHOUP
+          const uint4 cs = *reinterpret_cast<const uint4*>(crows + b1);
+          const uint32_t csa[4] = {cs.x, cs.y, cs.z, cs.w};
+#endif
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = 4 * e4 + u;
+            const uint32_t s = fold4_m(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
+            const uint32_t sh = mul_shoup_lazy(s, hva[u], hsa[u], pc.q);   // S H', [0, 2q)
+#if TFHE_P3_CSHOUP
+            p[e] = mul_shoup_lazy(sh, cva[u], csa[u], pc.q);               // c: Shoup
+#else
+            p[e] = mont_l(sh, cva[u], pc);                                 // c: Montgomery (c R)
+#endif
+          }
         }
         uint32_t pl[4][4];
 #pragma unroll
@@ -392,15 +420,15 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
 #pragma unroll
           for (int j = 0; j < 4; ++j) pl[j][e4] = w[j];
         }
-        if (g == 0 && it >= 2) mbar_wait(&a2_empty[it & 1], ((it >> 1) - 1) & 1);
+        if (g == 0 && it >= kA2Bufs) mbar_wait(&a2_empty[it % kA2Bufs], ((it / kA2Bufs) - 1) & 1);
         if (g == 0) PTRACE(7, it);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          *reinterpret_cast<uint4*>(a2t0 + (it & 1) * kC1A + p_off(0, j, mb + 16 * g, a2)) =
+          *reinterpret_cast<uint4*>(a2t0 + (it % kA2Bufs) * kC1A + p_off(0, j, mb + 16 * g, a2)) =
               make_uint4(pl[j][0], pl[j][1], pl[j][2], pl[j][3]);
       }
       fence_proxy_async_smem();
-      mbar_arrive(&a2_full[it & 1]);
+      mbar_arrive(&a2_full[it % kA2Bufs]);
       PTRACE(8, it);
       if (last_of_limb(pos, it)) mbar_arrive(epiA_done);
     }
@@ -904,15 +932,20 @@ int build_p3_tables(Ctx& c) {
       for (int i2 = 0; i2 < kPn2; ++i2)
         for (int b1 = 0; b1 < 32; ++b1) {
           const uint32_t cv = inv ? P((2ull * i2 + 1) * b1) : P((2ull * b1 + 1) * i2);
-          ht[kHC + i2 * 33 + b1] = mulmod_p(cv, R, q);
+#if TFHE_P3_CSHOUP
+          ht[kHC + i2 * 36 + b1] = cv;   // Shoup operand: no R
+          ht[kHCS + i2 * 36 + b1] = shoup_p(cv);
+#else
+          ht[kHC + i2 * 36 + b1] = mulmod_p(cv, R, q);   // Montgomery operand
+#endif
         }
       for (int b1 = 0; b1 < 32; ++b1)
         for (int a2 = 0; a2 < 32; ++a2) {
           // inner Hadamard: forward psi^(64 (2 b1 + 1) a2), inverse psi^-(128 a2 b1)
           const uint32_t h = mulmod_p(inv ? P(128ull * a2 * b1) : P(64ull * (2 * b1 + 1) * a2),
                                       twi[a2], q);
-          ht[kHIn + b1 * 32 + a2] = h;   // Shoup operand: no R
-          ht[kHInS + b1 * 32 + a2] = shoup_p(h);
+          ht[kHIn + a2 * 36 + b1] = h;   // Shoup operand (no R), transposed
+          ht[kHInS + a2 * 36 + b1] = shoup_p(h);
         }
       // pass 2 (64-point rows): forward psi^(2048 k2 i2), inverse
       // psi^-(1024 (2 i2 + 1) k2) n^-1 (row twist on the output k2)
