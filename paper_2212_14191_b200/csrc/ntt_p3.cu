@@ -73,10 +73,14 @@ constexpr int kHBeta = 0, kHBetaS = 64 * 32, kHIn = 2 * 64 * 32, kHInS = kHIn + 
 constexpr int kC1T = 16384, kC1H = kHWords * 4;
 constexpr int kC1A = 2 * kPTile + 16;            // two M tiles (+16 B: tile 1 on other banks)
 constexpr int kC1Smem = kC1T + kC1H + kPRaw + 2 * kC1A + kA2Bufs * kC1A + 32 * 8;
-// ---- pass 2 shared memory: T2 64 KB | raw 32 KB | A 2 x (2 K-steps)
+// ---- pass 2 shared memory: T2 64 KB | raw kRawSlots x 32 KB | A 2 x (2 K-steps)
+#ifndef TFHE_P3_RAWSLOTS
+#define TFHE_P3_RAWSLOTS 2
+#endif
+constexpr int kRawSlots = TFHE_P3_RAWSLOTS;
 constexpr int kC2T = 65536;
 constexpr int kC2A = 2 * kPTile;                 // K = 64: two K-steps of one M tile
-constexpr int kC2Smem = kC2T + kPRaw + 2 * kC2A + 32 * 8;
+constexpr int kC2Smem = kC2T + kRawSlots * kPRaw + 2 * kC2A + 32 * 8;
 
 struct ColArgs {
   const uint8_t* tab;      // [prime] 16 KB: T (B operand, 4 planes x 128 rows x 32 K)
@@ -506,11 +510,11 @@ template <int MODE>
 __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_constant__ RowArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sT = smem;
-  uint8_t* sRaw = smem + kC2T;
-  uint8_t* sA = sRaw + kPRaw;                    // [2] buffers of two K-steps
+  uint8_t* sRaw = smem + kC2T;                  // [kRawSlots] raw tiles (TMA ring)
+  uint8_t* sA = sRaw + kRawSlots * kPRaw;        // [2] buffers of two K-steps
   uint64_t* bar = reinterpret_cast<uint64_t*>(sA + 2 * kC2A);
-  uint64_t* raw_full = bar + 0;
-  uint64_t* raw_empty = bar + 1;
+  uint64_t* raw_full = bar + 12;   // [kRawSlots]
+  uint64_t* raw_empty = bar + 14;  // [kRawSlots]
   uint64_t* a_full = bar + 2;      // [2]
   uint64_t* a_empty = bar + 4;     // [2]
   uint64_t* acc_full = bar + 6;    // [2]
@@ -525,8 +529,10 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
   const int ge = (int)((long long)a.units * (blockIdx.x + 1) / gridDim.x);
   const int u0 = gb * a.S, cnt = (ge - gb) * a.S;
   if (tid == 0) {
-    mbar_init(raw_full, 1);
-    mbar_init(raw_empty, 32 * kPProdWarps);
+    for (int s = 0; s < kRawSlots; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], 32 * kPProdWarps);
+    }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&a_full[s], 32 * kPProdWarps);
       mbar_init(&a_empty[s], 1);
@@ -568,37 +574,41 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
 
   if (warp < kPProdWarps) {
     // -------------------------------------------------------------- producers
-    auto issue_raw = [&](const UPos& p) {
-      mbar_arrive_expect_tx(raw_full, kPRaw);
+    auto issue_raw = [&](const UPos& p, int slot) {
+      mbar_arrive_expect_tx(&raw_full[slot], kPRaw);
       const int prow = MODE == EPI_KS_ACC ? p.sl * a.map.n + p.limb : a.map.in_row[p.limb];
       const int row = (prow * a.batch + p.b) * kPn2;
-      tma_load_2d(sRaw, &a.tmap, 128 * p.kb, row, raw_full);
+      tma_load_2d(sRaw + slot * kPRaw, &a.tmap, 128 * p.kb, row, &raw_full[slot]);
     };
-    UPos pos = p0, ahead = p0;
-    if (tid == 0 && cnt > 0) issue_raw(ahead);
-    adv(ahead);
+    UPos pos = p0, ahead = p0;   // kRawSlots raw tiles in flight: ahead = unit it + kRawSlots
+    for (int s = 0; s < kRawSlots; ++s) {
+      if (tid == 0 && s < cnt) issue_raw(ahead, s);
+      adv(ahead);
+    }
     // raw word (k = i2, m = k1 local) at 128 k + m; 64 warp items (4 k rows, 32 m)
     const int r = lane >> 3, c = lane & 7;
     int prev_limb = -1;
     uint32_t tw_ph = 0;
     for (int it = 0; it < cnt; ++it, adv(pos)) {
       const int limb = pos.limb;
-      mbar_wait(raw_full, it & 1);
+      const int slot = it % kRawSlots;
+      mbar_wait(&raw_full[slot], (it / kRawSlots) & 1);
       uint4 x[kPItems];
+      const uint8_t* raw = sRaw + slot * kPRaw;
 #pragma unroll
       for (int k = 0; k < kPItems; ++k) {
         const int item = min(warp + kPProdWarps * k, 63);
         const int ib = item >> 2, jb = item & 3;
-        x[k] = *reinterpret_cast<const uint4*>(sRaw + ((4 * ib + r) * 128 + 32 * jb + 4 * c) * 4);
+        x[k] = *reinterpret_cast<const uint4*>(raw + ((4 * ib + r) * 128 + 32 * jb + 4 * c) * 4);
       }
       // the generic-proxy reads of the raw tile must be ordered before the
       // next TMA (async-proxy) write into it: without this fence the refill
       // was observed to land under still-pending reads
       fence_proxy_async_smem();
-      mbar_arrive(raw_empty);
-      if (tid == 0 && it + 1 < cnt) {
-        mbar_wait(raw_empty, it & 1);
-        issue_raw(ahead);
+      mbar_arrive(&raw_empty[slot]);
+      if (tid == 0 && it + kRawSlots < cnt) {
+        mbar_wait(&raw_empty[slot], (it / kRawSlots) & 1);
+        issue_raw(ahead, slot);
       }
       adv(ahead);
       if (limb != prev_limb) {
