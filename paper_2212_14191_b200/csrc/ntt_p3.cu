@@ -687,6 +687,36 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
       const int k1 = 128 * pos.kb + 32 * q + lane;
       const size_t pos0 = (size_t)32 * h * kPn1 + k1;   // the warp's first output position
       const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + pos.b) * kPN + pos0;
+      // EPI_KS_ACC: this slice's key rows (none for the slice's own target row);
+      // the first 8 columns are requested before the accumulator wait and each
+      // later chunk one chunk ahead, so the L2 latency overlaps the fold / MAC
+      const bool use_key = MODE == EPI_KS_ACC && a.epi.j0 + pos.sl != a.epi.js[limb];
+      const uint32_t* kbp = nullptr;
+      uint32_t kbv[2][8], kav[2][8];
+      if (use_key) {
+        kbp = a.epi.key + (size_t)(a.epi.j0 + pos.sl) * a.epi.key_pair +
+              (size_t)a.epi.key_row[limb] * kPN + pos0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          kbv[0][e] = __ldg(kbp + e * kPn1);
+          kav[0][e] = __ldg(kbp + a.epi.key_pair / 2 + e * kPn1);
+        }
+      }
+      if (MODE == EPI_KS_ACC && pos.sl == 0) {
+        // a group's first slice: its accumulator rows (or zero), requested before
+        // the accumulator wait too (the previous group's sums are already stored)
+        if (a.epi.init_acc[limb]) {
+          const size_t arow = ((size_t)a.map.out_row[limb] * a.batch + pos.b) * kPN + pos0;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            sb[e] = a.epi.acc_b[arow + (size_t)e * kPn1];
+            sa[e] = a.epi.acc_a[arow + (size_t)e * kPn1];
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) sb[e] = sa[e] = 0;
+        }
+      }
       mbar_wait(&acc_full[buf], (it >> 1) & 1);
       tc_fence_after();
       uint32_t y[32];
@@ -751,44 +781,32 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
         const size_t arow = ((size_t)a.map.out_row[limb] * a.batch + pos.b) * kPN + pos0;
         const bool lazy = pc.q < (1u << 30);   // warp-uniform: one prime per unit
         const uint32_t q2 = 2 * pc.q;
-        if (pos.sl == 0) {
-          if (a.epi.init_acc[limb]) {
+        if (use_key) {
+          const uint32_t* kap = kbp + a.epi.key_pair / 2;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              sb[e] = a.epi.acc_b[arow + (size_t)e * kPn1];
-              sa[e] = a.epi.acc_a[arow + (size_t)e * kPn1];
-            }
-          } else {
+          for (int ch = 0; ch < 4; ++ch) {
+            const int cur = ch & 1, cc = 8 * ch;
+            if (ch < 3) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) sb[e] = sa[e] = 0;
-          }
-        }
-        if (a.epi.j0 + pos.sl != a.epi.js[limb]) {
-          const uint32_t* kb = a.epi.key + (size_t)(a.epi.j0 + pos.sl) * a.epi.key_pair +
-                               (size_t)a.epi.key_row[limb] * kPN + pos0;
-          const uint32_t* ka = kb + a.epi.key_pair / 2;
-#pragma unroll
-          for (int cc = 0; cc < 32; cc += 8) {
-            uint32_t kbv[8], kav[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              kbv[e] = __ldg(kb + (cc + e) * kPn1);
-              kav[e] = __ldg(ka + (cc + e) * kPn1);
+              for (int e = 0; e < 8; ++e) {
+                kbv[cur ^ 1][e] = __ldg(kbp + (cc + 8 + e) * kPn1);
+                kav[cur ^ 1][e] = __ldg(kap + (cc + 8 + e) * kPn1);
+              }
             }
             if (lazy) {
               // q < 2^30: the sums stay in [0, 2q) (< 2^31), one unsigned min per add
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                const uint32_t tb = sb[cc + e] + mont_l(y[cc + e], kbv[e], pc);
-                const uint32_t ta = sa[cc + e] + mont_l(y[cc + e], kav[e], pc);
+                const uint32_t tb = sb[cc + e] + mont_l(y[cc + e], kbv[cur][e], pc);
+                const uint32_t ta = sa[cc + e] + mont_l(y[cc + e], kav[cur][e], pc);
                 sb[cc + e] = min(tb, tb - q2);
                 sa[cc + e] = min(ta, ta - q2);
               }
             } else {
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                sb[cc + e] = add_mod(sb[cc + e], corr_q(mont_l(y[cc + e], kbv[e], pc), pc.q), pc.q);
-                sa[cc + e] = add_mod(sa[cc + e], corr_q(mont_l(y[cc + e], kav[e], pc), pc.q), pc.q);
+                sb[cc + e] = add_mod(sb[cc + e], corr_q(mont_l(y[cc + e], kbv[cur][e], pc), pc.q), pc.q);
+                sa[cc + e] = add_mod(sa[cc + e], corr_q(mont_l(y[cc + e], kav[cur][e], pc), pc.q), pc.q);
               }
             }
           }
