@@ -37,6 +37,8 @@
 #include <cstring>
 #include <string>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "poly_ops.h"
 #include "tfhe_internal.h"
@@ -66,7 +68,16 @@ struct BconvTcArgs {
   int64_t per_row;     // batch * n coefficients per row
   int64_t tiles;       // ceil(per_row / 128)
   int KC, nchunks;
+  int use_tmap;        // 1: one TMA tensor load per tile (per_row % 128 == 0)
+  CUtensorMap tmap;    // sources viewed as [n_src][per_row], box {128, n_src}
 };
+
+// st.global predicated on `p` (keeps a warp-uniform skip a predicate, not a branch)
+TFHE_DEV void st_global_if(uint32_t* ptr, uint32_t v, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.u32 [%0], %1;\n\t}"
+               ::"l"(ptr), "r"(v), "r"((uint32_t)p)
+               : "memory");
+}
 
 // offset of (row r, byte k) inside a K-major SWIZZLE_NONE tile of `rows` x 32 bytes
 TFHE_DEV uint32_t tile_off_bc(int r, int k, int rows) {
@@ -147,7 +158,7 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
     }
     for (int b = 0; b < 4; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 32 * kEpiWarpsBC);
+      mbar_init(&acc_empty[b], 32 * kEpiWarpsBC / 2);   // one epilogue group per buffer
     }
     fence_mbar_init();
   }
@@ -182,6 +193,10 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
       const int64_t x0 = (t_lo + it) * kRowsBC;
       const uint32_t cnt = (uint32_t)std::min<int64_t>(kRowsBC, a.per_row - x0);
       mbar_arrive_expect_tx(&raw_full[slot], cnt * 4 * nsrc);
+      if (a.use_tmap) {   // every source row of the tile in one tensor load
+        tma_load_2d(sRaw + slot * kRawTileBC, &a.tmap, (int)x0, 0, &raw_full[slot]);
+        return;
+      }
       for (int s = 0; s < nsrc; ++s)
         bulk_g2s(sRaw + slot * kRawTileBC + s * kRowsBC * 4, a.in + (int64_t)s * a.per_row + x0,
                  cnt * 4, &raw_full[slot]);
@@ -224,10 +239,12 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
     }
   } else if (warp < 4 + kEpiWarpsBC) {
     // ---------------------------------------------------------------- epilogue
-    // warp 4 + 4h + g reads TMEM lane group g (rows 32g..32g+31) and the
-    // targets [16h, 16h + 16) of each 32-target chunk.  The fold
-    // v = sum_i 2^(8i) C_i (< 2^48) is reduced by one Montgomery step
-    // (R = 2^32, compensated in the constant operand: V_j carries 2^32).
+    // Two groups of 4 warps take alternate (tile, chunk) units u (group h: u
+    // odd / even, TMEM buffers {h, h + 2}), so two chunks drain at once; warp
+    // 4 + 4h + g reads TMEM lane group g (rows 32g..32g+31) and all 32 targets
+    // of its chunk in two halves.  The fold v = sum_i 2^(8i) C_i (< 2^48) is
+    // reduced by one Montgomery step (R = 2^32, compensated in the constant
+    // operand: V_j carries 2^32).
     const int g = (warp - 4) & 3, h = (warp - 4) >> 2, r = g * 32 + (tid & 31);
     const uint32_t lane_base = tmem + ((uint32_t)(g * 32) << 16);
     int u = 0;
@@ -235,34 +252,43 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
       const int64_t x = (t_lo + it) * kRowsBC + r;
       const bool valid = x < a.per_row;
       for (int ch = 0; ch < nch; ++ch, ++u) {
+        if ((u & 1) != h) continue;
         const int buf = u & 3;
         mbar_wait(&acc_full[buf], (u >> 2) & 1);
         tc_fence_after();
-        uint32_t c[4][16];
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t c[4][16];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) tmem_ld16(lane_base + buf * 128 + i * kChunk + h * 16, c[i]);
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(&acc_empty[buf]);
-        const int tb = ch * kChunk + h * 16;
-        if (!valid || tb >= ba.n_dst) continue;
-        const uint32_t skip = sSkip[tb >> 4];
-        uint32_t qv[16], qi[16];
+          for (int i = 0; i < 4; ++i) tmem_ld16(lane_base + buf * 128 + i * kChunk + hh * 16, c[i]);
+          tmem_ld_wait();
+          if (hh == 1) {
+            tc_fence_before();
+            mbar_arrive(&acc_empty[buf]);
+          }
+          const int tb = ch * kChunk + hh * 16;
+          if (!valid || tb >= ba.n_dst) continue;
+          const uint32_t skip = sSkip[tb >> 4];
+          uint32_t qv[16], qi[16];
 #pragma unroll
-        for (int e = 0; e < 16; e += 4) {
-          const uint4 q4 = *reinterpret_cast<const uint4*>(sQ + tb + e);
-          const uint4 i4 = *reinterpret_cast<const uint4*>(sQinv + tb + e);
-          qv[e] = q4.x; qv[e + 1] = q4.y; qv[e + 2] = q4.z; qv[e + 3] = q4.w;
-          qi[e] = i4.x; qi[e + 1] = i4.y; qi[e + 2] = i4.z; qi[e + 3] = i4.w;
-        }
-        uint32_t* o = a.out + (int64_t)tb * a.per_row + x;
+          for (int e = 0; e < 16; e += 4) {
+            const uint4 q4 = *reinterpret_cast<const uint4*>(sQ + tb + e);
+            const uint4 i4 = *reinterpret_cast<const uint4*>(sQinv + tb + e);
+            qv[e] = q4.x; qv[e + 1] = q4.y; qv[e + 2] = q4.z; qv[e + 3] = q4.w;
+            qi[e] = i4.x; qi[e + 1] = i4.y; qi[e + 2] = i4.z; qi[e + 3] = i4.w;
+          }
+          // predicated stores down the target rows (skip = copies stored by the
+          // producers, and padding): no per-output branch or 64-bit multiply
+          uint32_t* o = a.out + (int64_t)tb * a.per_row + x;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const uint32_t lo = c[0][e] + (c[1][e] << 8), hi = c[2][e] + (c[3][e] << 8);
-          const uint64_t f = (uint64_t)lo + ((uint64_t)hi << 16);
-          const uint32_t m = (uint32_t)f * qi[e];
-          const uint32_t w = (uint32_t)((f + (uint64_t)m * qv[e]) >> 32);
-          if (!((skip >> e) & 1)) o[(int64_t)e * a.per_row] = w >= qv[e] ? w - qv[e] : w;
+          for (int e = 0; e < 16; ++e) {
+            const uint32_t lo = c[0][e] + (c[1][e] << 8), hi = c[2][e] + (c[3][e] << 8);
+            const uint64_t f = (uint64_t)lo + ((uint64_t)hi << 16);
+            const uint32_t m = (uint32_t)f * qi[e];
+            const uint32_t w = (uint32_t)((f + (uint64_t)m * qv[e]) >> 32);
+            st_global_if(o, w >= qv[e] ? w - qv[e] : w, ((skip >> e) & 1) == 0);
+            o += a.per_row;
+          }
         }
       }
     }
@@ -386,6 +412,31 @@ int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArg
   a.tiles = (a.per_row + kRowsBC - 1) / kRowsBC;
   a.KC = (4 * ba.n_src + 31) / 32;
   a.nchunks = (ba.n_dst + kChunk - 1) / kChunk;
+  a.use_tmap = 0;
+  if (a.per_row % kRowsBC == 0) {
+    typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+      cudaDriverEntryPointQueryResult qr;
+      void* p = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) ==
+              cudaSuccess &&
+          qr == cudaDriverEntryPointSuccess)
+        fn = reinterpret_cast<EncodeFn>(p);
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)a.per_row, (cuuint64_t)ba.n_src};
+    cuuint64_t strides[1] = {(cuuint64_t)a.per_row * 4};
+    cuuint32_t box[2] = {(cuuint32_t)kRowsBC, (cuuint32_t)ba.n_src};
+    cuuint32_t es[2] = {1, 1};
+    if (fn && fn(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(in), dims,
+                 strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      a.use_tmap = 1;
+  }
   const int smem = 4 * kMaxChunks * kMaxKC * kBTileBC + kAStages * kMaxKC * kATileBC +
                    kRawBC * kRawTileBC + kMaxBconvDst * (4 + 4 + 4) + kMaxBconvDst / 16 * 4 +
                    (2 * kAStages + 8 + 2 * kRawBC) * 8 + 16;
