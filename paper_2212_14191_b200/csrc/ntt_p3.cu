@@ -101,6 +101,7 @@ struct RowArgs {
   int batch, units;
   int S;                   // EPI_KS_ACC: slices per (target, member, row block) group, else 1;
                            // the P^T row of (slice s, limb l) is s * map.n + l
+  int strided;             // group g of CTA c: c + k * gridDim.x (limb-synchronous CTAs)
   LimbMap map;             // in_row = P^T workspace row
   EpiArgs epi;
   CUtensorMap tmap;        // P^T viewed as [rows * batch * 64 i2][1024 k1], box {128, 64}
@@ -524,10 +525,15 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // a.units counts slice groups (S units each); whole groups per CTA
-  const int gb = (int)((long long)a.units * blockIdx.x / gridDim.x);
-  const int ge = (int)((long long)a.units * (blockIdx.x + 1) / gridDim.x);
-  const int u0 = gb * a.S, cnt = (ge - gb) * a.S;
+  // a.units counts slice groups (S units each); whole groups per CTA, either a
+  // contiguous range or (a.strided) groups blockIdx.x + k * gridDim.x, so that
+  // all CTAs work on the same limb at a time and its per-limb epilogue operand
+  // (the switching-key rows, shared by every member) stays L2-resident
+  const int gstep = a.strided ? (int)gridDim.x : 1;
+  const int gb = a.strided ? (int)blockIdx.x : (int)((long long)a.units * blockIdx.x / gridDim.x);
+  const int ng = a.strided ? (a.units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x
+                           : (int)((long long)a.units * (blockIdx.x + 1) / gridDim.x) - gb;
+  const int cnt = ng * a.S;
   if (tid == 0) {
     for (int s = 0; s < kRawSlots; ++s) {
       mbar_init(&raw_full[s], 1);
@@ -551,25 +557,21 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
   // unit = (limb, member, row block kb of 128 k1, slice sl): sl fastest (S = 1
   // unless the grouped key-switch epilogue sums S slices per output)
   struct UPos {
-    int limb, b, kb, sl;
+    int limb, b, kb, sl, g;
   };
   const int S = a.S;
-  const int g0 = u0 / S;
   const int upl = a.batch * 8;
-  const UPos p0 = {g0 / upl, (g0 % upl) >> 3, g0 & 7, u0 % S};
+  const UPos p0 = {gb / upl, (gb % upl) >> 3, gb & 7, 0, gb};
   auto adv = [&](UPos& p) {
     if (++p.sl < S) return;
     p.sl = 0;
-    if (++p.kb == 8) {
-      p.kb = 0;
-      if (++p.b == a.batch) {
-        p.b = 0;
-        ++p.limb;
-      }
-    }
+    p.g += gstep;
+    p.limb = p.g / upl;
+    p.b = (p.g % upl) >> 3;
+    p.kb = p.g & 7;
   };
   auto last_of_limb = [&](const UPos& p, int it) {
-    return it + 1 == cnt || (p.sl + 1 == S && p.kb == 7 && p.b + 1 == a.batch);
+    return it + 1 == cnt || (p.sl + 1 == S && (p.g + gstep) / upl != p.limb);
   };
 
   if (warp < kPProdWarps) {
@@ -1116,6 +1118,11 @@ int launch_p3_row(const Ctx& c, const uint32_t* P, uint32_t* out, const LimbMap&
   const int grid = (int)std::min<long long>(c.sms, groups);
   if (grid <= 0) return 0;
   a.units = (int)groups;   // the kernel splits groups, then expands them by S
+  // the key-switch epilogues read per-limb key rows shared by every member:
+  // limb-synchronous CTAs keep them in L2 (contiguous ranges put every limb in
+  // flight at once -- 1.75x DRAM read amplification at P-Default)
+  static const int strided_env = getenv("TFHE_P3_STRIDED") ? atoi(getenv("TFHE_P3_STRIDED")) : -1;
+  a.strided = strided_env >= 0 ? strided_env : (mode == EPI_KS_ACC || mode == EPI_KS_MAC);
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kC2Smem);
     kern<<<grid, kRowThreads, kC2Smem, st>>>(a);
