@@ -95,15 +95,20 @@ CkksGeom geom(const TfheCtx* h, int level, int dnum, int r0 = 0, int nr = -1) {
   return g;
 }
 
-// slices per key-switch group: bounded by the launch limb map and by an
-// 8 GiB cap on the (S * T, batch, n) stage-1 workspace
+// slices per key-switch group: bounded by the launch limb map and by a cap on
+// the (S * T, batch, n) stage-1 workspace (default 24 GiB of the 180 GB HBM,
+// TFHE_KS_WS_GIB overrides): every group after the first re-reads and
+// re-writes the (2, T, batch, n) accumulator, so fewer, larger groups save
+// HBM traffic (P-Default at B = 128: S = 11, 5 groups, instead of S = 5, 9)
 void set_group(CkksGeom& g, const Ctx& c, int batch) {
   if (!c.use_ts) {
     g.S = 1;
     return;
   }
   const size_t row_bytes = (size_t)batch * c.n * 4;
-  const size_t cap = (size_t)8 << 30;
+  static const size_t cap_gib = getenv("TFHE_KS_WS_GIB") ? (size_t)atoi(getenv("TFHE_KS_WS_GIB"))
+                                                        : (size_t)24;
+  const size_t cap = std::max<size_t>(cap_gib, 1) << 30;
   int s_mem = (int)std::max<size_t>(1, cap / (row_bytes * g.T));
   g.S = std::max(1, std::min({g.nslices, kMaxLimbs / g.T, s_mem}));
   // test knob: TFHE_KS_MAX_S caps the group size so small goldens also run the

@@ -79,6 +79,9 @@ constexpr int kC1Smem = kC1T + kC1H + kPRaw + 2 * kC1A + kA2Bufs * kC1A + 32 * 8
 #endif
 constexpr int kRawSlots = TFHE_P3_RAWSLOTS;
 constexpr int kC2T = 65536;
+// grouped key-switch row pass: warpgroup 0 (producers + MMA) gives registers to
+// the two epilogue warpgroups (128 * 128 + 256 * 184 <= 384 * 168)
+constexpr int kRowRegsLow = 128, kRowRegsEpi = 184;
 constexpr int kC2A = 2 * kPTile;                 // K = 64: two K-steps of one M tile
 constexpr int kC2Smem = kC2T + kRawSlots * kPRaw + 2 * kC2A + 32 * 8;
 
@@ -575,6 +578,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
   };
 
   if (warp < kPProdWarps) {
+    if (MODE == EPI_KS_ACC) reg_dealloc<kRowRegsLow>();
     // -------------------------------------------------------------- producers
     auto issue_raw = [&](const UPos& p, int slot) {
       mbar_arrive_expect_tx(&raw_full[slot], kPRaw);
@@ -641,6 +645,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
       mbar_arrive(&a_full[buf]);
     }
   } else if (warp == kPMmaWarp) {
+    if (MODE == EPI_KS_ACC) reg_dealloc<kRowRegsLow>();
     // -------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = idesc_i8(128, 256) | (1u << 15);   // A MN-major
     const uint32_t sT_u = smem_u32(sT);
@@ -673,7 +678,145 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
       }
       __syncwarp();
     }
-  } else if (warp < 12) {
+  } else if (MODE == EPI_KS_ACC && warp < 12) {
+    reg_alloc<kRowRegsEpi>();
+    // -------------------------------------------------- grouped key-switch epilogue
+    // warp -> (lane quarter q, column half h) as below.  y arrives as y R (the
+    // table carries R^2); the S slices of a (target, member, row block) sum in
+    // registers (lazy in [0, 2q) for q < 2^30), the accumulator row is read at
+    // the group's start (init_acc, L2-prefetched one group ahead) and written
+    // once at its end; a slice's own target row is skipped (reused unchanged,
+    // ckks.py:361-364).  Fold and MAC run per 8-column chunk while the TMEM
+    // buffer is held, so the key rows stream through a 3-chunk register ring
+    // two chunks ahead -- across unit boundaries -- and their L2 latency hides
+    // behind two chunks of fold / MAC work.
+    const int q = warp & 3, h = (warp - 4) >> 2;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const size_t half = (size_t)a.epi.key_pair / 2;
+    auto key_ptr = [&](const UPos& p) -> const uint32_t* {
+      if (a.epi.j0 + p.sl == a.epi.js[p.limb]) return nullptr;
+      const size_t p0_ = (size_t)32 * h * kPn1 + 128 * p.kb + 32 * q + lane;
+      return a.epi.key + (size_t)(a.epi.j0 + p.sl) * a.epi.key_pair +
+             (size_t)a.epi.key_row[p.limb] * kPN + p0_;
+    };
+    auto acc_row = [&](const UPos& p) -> size_t {
+      return ((size_t)a.map.out_row[p.limb] * a.batch + p.b) * kPN + (size_t)32 * h * kPn1 +
+             128 * p.kb + 32 * q + lane;
+    };
+    uint32_t sb[32], sa[32];
+    // key ring: chunk ch of a unit lives in buffer ch % kKR; after its MAC the
+    // buffer is refilled with chunk ch + kKR (this unit's, else the next
+    // unit's) -- kKR chunks of lookahead, static register indices (the ring
+    // period divides the chunks per unit, so no register rotation is needed)
+    constexpr int kKC = 8, kKR = 4, kCPU = 32 / kKC;
+    static_assert(kCPU % kKR == 0, "ring period must divide the chunks per unit");
+    uint32_t kb[kKR][kKC], ka[kKR][kKC];
+    auto load_keys = [&](const uint32_t* kp, int ch, uint32_t (&b)[kKC], uint32_t (&c)[kKC]) {
+      if (kp) {
+#pragma unroll
+        for (int e = 0; e < kKC; ++e) {
+          b[e] = __ldg(kp + (kKC * ch + e) * kPn1);
+          c[e] = __ldg(kp + half + (kKC * ch + e) * kPn1);
+        }
+      }
+    };
+    UPos pos = p0;
+    const uint32_t* kp_cur = cnt > 0 ? key_ptr(p0) : nullptr;
+    const uint32_t* kp_nxt = nullptr;
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) load_keys(kp_cur, r, kb[r], ka[r]);
+    for (int it = 0; it < cnt; ++it, adv(pos)) {
+      const int limb = pos.limb;
+      const PrimeConst pc = a.pc[a.map.prime[limb]];
+      const int buf = it & 1;
+      const size_t arow = acc_row(pos);
+      if (pos.sl == 0) {
+        if (a.epi.init_acc[limb]) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            sb[e] = a.epi.acc_b[arow + (size_t)e * kPn1];
+            sa[e] = a.epi.acc_a[arow + (size_t)e * kPn1];
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) sb[e] = sa[e] = 0;
+        }
+        // the next group's accumulator rows: HBM -> L2 while this group runs
+        if (it + S < cnt) {
+          UPos ng = pos;
+          for (int k = 0; k < S; ++k) adv(ng);
+          if (a.epi.init_acc[ng.limb]) {
+            const size_t nrow = acc_row(ng);
+#pragma unroll 4
+            for (int e = 0; e < 32; ++e) {
+              prefetch_l2(a.epi.acc_b + nrow + (size_t)e * kPn1);
+              prefetch_l2(a.epi.acc_a + nrow + (size_t)e * kPn1);
+            }
+          }
+        }
+      }
+      kp_nxt = nullptr;
+      if (it + 1 < cnt) {
+        UPos nx = pos;
+        adv(nx);
+        kp_nxt = key_ptr(nx);
+      }
+      const bool lazy = pc.q < (1u << 30);   // warp-uniform: one prime per unit
+      const uint32_t q2 = 2 * pc.q;
+      mbar_wait(&acc_full[buf], (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int ch = 0; ch < kCPU; ++ch) {
+        const int rb = ch % kKR;
+        uint32_t y[kKC];
+#pragma unroll
+        for (int hf = 0; hf < kKC / 4; ++hf) {
+          uint32_t acc[4][4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            tmem_ld4(tmem + buf * 256 + lane_off + i * 64 + 32 * h + kKC * ch + 4 * hf, acc[i]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            y[4 * hf + e] = fold4_m(acc[0][e], acc[1][e], acc[2][e], acc[3][e], pc);
+        }
+        if (ch == kCPU - 1) {
+          tc_fence_before();
+          mbar_arrive(&acc_empty[buf]);
+        }
+        if (kp_cur) {
+          if (lazy) {
+#pragma unroll
+            for (int e = 0; e < kKC; ++e) {
+              const uint32_t tb = sb[kKC * ch + e] + mont_l(y[e], kb[rb][e], pc);
+              const uint32_t ta = sa[kKC * ch + e] + mont_l(y[e], ka[rb][e], pc);
+              sb[kKC * ch + e] = min(tb, tb - q2);
+              sa[kKC * ch + e] = min(ta, ta - q2);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < kKC; ++e) {
+              sb[kKC * ch + e] =
+                  add_mod(sb[kKC * ch + e], corr_q(mont_l(y[e], kb[rb][e], pc), pc.q), pc.q);
+              sa[kKC * ch + e] =
+                  add_mod(sa[kKC * ch + e], corr_q(mont_l(y[e], ka[rb][e], pc), pc.q), pc.q);
+            }
+          }
+        }
+        // refill: chunk ch + kKR of this unit, or chunk ch + kKR - kCPU of the next
+        if (ch + kKR < kCPU) load_keys(kp_cur, ch + kKR, kb[rb], ka[rb]);
+        else load_keys(kp_nxt, ch + kKR - kCPU, kb[rb], ka[rb]);
+      }
+      if (pos.sl + 1 == S) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          a.epi.acc_b[arow + (size_t)e * kPn1] = corr_q(sb[e], pc.q);   // [0, 2q) -> [0, q)
+          a.epi.acc_a[arow + (size_t)e * kPn1] = corr_q(sa[e], pc.q);
+        }
+      }
+      kp_cur = kp_nxt;
+    }
+  } else if (MODE != EPI_KS_ACC && warp < 12) {
     // -------------------------------------------------------------- epilogue
     // warp -> (lane quarter q, column half h): row k1 = 128 kb + 32 q + lane,
     // columns k2 in [32 h, 32 h + 32); fold all 32 first, release the
