@@ -36,6 +36,8 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <vector>
+#include <cstdio>
 
 #include <cuda.h>
 
@@ -56,10 +58,25 @@ constexpr int kEpiWarpsBC = 8;
 constexpr int kMmaWarpBC = 4 + kEpiWarpsBC;
 constexpr int kThreadsBC = 32 * (kMmaWarpBC + 1);
 constexpr int kATileBC = kRowsBC * 32;           // 4 KB per K-step
-constexpr int kBTileBC = kChunk * 32;            // 1 KB per (i, chunk, K-step)
-constexpr int kRawBC = 6;                        // raw input tiles in flight (TMA ring)
+constexpr int kPairN = 256;                      // MMA N: two chunks x 4 planes x 32 targets
+constexpr int kMaxPairs = kMaxChunks / 2;
+constexpr int kBTileBC = kPairN * 32;            // 8 KB per (chunk pair, K-step)
+constexpr int kRawBC = 8;                       // raw input tiles in flight (TMA ring)
 constexpr int kMaxSrcBC = 16;
 constexpr int kRawTileBC = kMaxSrcBC * kRowsBC * 4;   // 8 KB: 128 coefficients x 16 sources
+constexpr int kStageWords = 2 * 2 * kChunk * kRowsBC;   // 64 KB: per epilogue group 2 x [32][128]
+
+// timeline probes (-DTFHE_BC_TRACE): per-tile event clocks of CTA 0, lane 0
+#ifdef TFHE_BC_TRACE
+constexpr int kBTraceN = 128;
+#define BTRACE(ev, i)                                                              \
+  do {                                                                             \
+    if (blockIdx.x == 0 && (tid & 31) == 0 && (i) < kBTraceN)                      \
+      a.trace[(ev) * kBTraceN + (i)] = clock64();                                  \
+  } while (0)
+#else
+#define BTRACE(ev, i) do { } while (0)
+#endif
 
 struct BconvTcArgs {
   const uint32_t* in;
@@ -69,7 +86,13 @@ struct BconvTcArgs {
   int64_t tiles;       // ceil(per_row / 128)
   int KC, nchunks;
   int use_tmap;        // 1: one TMA tensor load per tile (per_row % 128 == 0)
+  int use_tstore;      // 1: outputs leave through shared memory by TMA tensor stores
   CUtensorMap tmap;    // sources viewed as [n_src][per_row], box {128, n_src}
+  CUtensorMap omap;    // targets viewed as [n_dst][per_row], box {128, 32}
+  uint32_t* copy_flag; // tensor-store mode: set to copy_gen if a copy source is non-canonical
+  uint32_t copy_gen;
+  uint32_t copy_src_mask;   // sources some target copies through
+  unsigned long long* trace;   // TFHE_BC_TRACE builds only
 };
 
 // st.global predicated on `p` (keeps a warp-uniform skip a predicate, not a branch)
@@ -89,17 +112,19 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KC = a.KC, nch = a.nchunks;
   uint8_t* sB = smem;                                              // [i][chunk][kc] tiles
-  uint8_t* sA = sB + 4 * kMaxChunks * kMaxKC * kBTileBC;           // [stage][kc] tiles
+  uint8_t* sA = sB + kMaxPairs * kMaxKC * kBTileBC;                // [stage][kc] tiles
   uint8_t* sRaw = sA + kAStages * kMaxKC * kATileBC;               // [slot][src][128] u32
-  uint32_t* sQ = reinterpret_cast<uint32_t*>(sRaw + kRawBC * kRawTileBC);  // per target
+  uint32_t* sStage = reinterpret_cast<uint32_t*>(sRaw + kRawBC * kRawTileBC);  // [grp][2][32][128]
+  uint32_t* sQ = sStage + kStageWords;                             // per target
   uint32_t* sQinv = sQ + kMaxBconvDst;                             // -q^-1 mod 2^32
   int* sCopy = reinterpret_cast<int*>(sQinv + kMaxBconvDst);      // copy list: t | s << 16
-  uint32_t* sSkip = reinterpret_cast<uint32_t*>(sCopy + kMaxBconvDst);  // per 16 targets
+  int* sCopyLo = sCopy + kMaxBconvDst;                             // per chunk: first copy
+  uint32_t* sSkip = reinterpret_cast<uint32_t*>(sCopyLo + 8);      // per 16 targets
   uint64_t* a_full = reinterpret_cast<uint64_t*>(sSkip + kMaxBconvDst / 16);
   uint64_t* a_empty = a_full + kAStages;
   uint64_t* acc_full = a_empty + kAStages;
-  uint64_t* acc_empty = acc_full + 4;
-  uint64_t* raw_full = acc_empty + 4;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* raw_full = acc_empty + 2;
   uint64_t* raw_empty = raw_full + kRawBC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + kRawBC);
 
@@ -107,7 +132,7 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
 
   // constant operand: B_i[4s + j][t] = byte i of (2^(8j+32) F[s][t] mod p_t)
   // (the 2^32 is the Montgomery factor the epilogue's REDC removes)
-  for (int w = tid; w < 4 * kMaxChunks * kMaxKC * kBTileBC / 4; w += blockDim.x)
+  for (int w = tid; w < kMaxPairs * kMaxKC * kBTileBC / 4; w += blockDim.x)
     reinterpret_cast<uint32_t*>(sB)[w] = 0;
   __syncthreads();
   for (int e = tid; e < ba.n_src * ba.n_dst; e += blockDim.x) {
@@ -121,7 +146,8 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
       const int k = 4 * s + j, kc = k >> 5;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        sB[((i * kMaxChunks + ch) * kMaxKC + kc) * kBTileBC + tile_off_bc(tr, k & 31, kChunk)] =
+        sB[((ch >> 1) * kMaxKC + kc) * kBTileBC +
+           tile_off_bc((ch & 1) * 128 + i * kChunk + tr, k & 31, kPairN)] =
             (uint8_t)(v >> (8 * i));
     }
   }
@@ -143,9 +169,14 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
     sSkip[tid] = m;
   }
   if (tid == 0) {
+    // copy list in target order, and each chunk's range of it
     int k = 0;
-    for (int t = 0; t < ba.n_dst; ++t)
-      if (ba.copy_from[t] >= 0) sCopy[k++] = t | (ba.copy_from[t] << 16);
+    for (int ch = 0; ch <= kMaxChunks; ++ch) {
+      sCopyLo[ch] = k;
+      if (ch == kMaxChunks) break;
+      for (int t = ch * kChunk; t < (ch + 1) * kChunk && t < ba.n_dst; ++t)
+        if (ba.copy_from[t] >= 0) sCopy[k++] = t | (ba.copy_from[t] << 16);
+    }
   }
   if (tid == 0) {
     for (int s = 0; s < kAStages; ++s) {
@@ -156,9 +187,9 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], 128);
     }
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 32 * kEpiWarpsBC / 2);   // one epilogue group per buffer
+      mbar_init(&acc_empty[b], 32 * kEpiWarpsBC);   // both epilogue groups
     }
     fence_mbar_init();
   }
@@ -203,23 +234,43 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
     };
     if (tid == 0)
       for (int it = 0; it < kRawBC && it < n_tiles; ++it) issue(it);
+    bool noncanon = false;
     for (int it = 0; it < n_tiles; ++it) {
       const int st = it % kAStages, slot = it % kRawBC;
       if (it >= kAStages) mbar_wait(&a_empty[st], ((it / kAStages) & 1) ^ 1);
+      if (warp == 0) BTRACE(0, it);
       mbar_wait(&raw_full[slot], (it / kRawBC) & 1);
+      if (warp == 0) BTRACE(1, it);
       const int64_t x = (t_lo + it) * kRowsBC + r;
       const bool valid = x < a.per_row;
       const uint32_t* raw = reinterpret_cast<const uint32_t*>(sRaw + slot * kRawTileBC);
-      uint32_t y[kMaxSrcBC];
+      // branch-free: all 16 source rows are read (rows >= nsrc hold stale data)
+      // and the padding sources have qhat_inv = 0, q = 1, so their y is 0;
+      // rows past per_row are clipped at the store
+      uint32_t xv[kMaxSrcBC], y[kMaxSrcBC];
 #pragma unroll
-      for (int s = 0; s < kMaxSrcBC; ++s)
-        y[s] = (valid && s < nsrc) ? mul_shoup(raw[s * kRowsBC + r], hs[s], hss[s], qs[s]) : 0;
-      // targets that are source primes copy the source row through (rns.py:140-142)
-      if (valid)
+      for (int s = 0; s < kMaxSrcBC; ++s) xv[s] = raw[s * kRowsBC + r];
+#pragma unroll
+      for (int s = 0; s < kMaxSrcBC; ++s) y[s] = mul_shoup(xv[s], hs[s], hss[s], qs[s]);
+      // tensor-store mode computes a copy target as y_s (Q/q_s) mod q_s = a_s mod q_s
+      // (the conversion factors of a target that is source s are (Q/q_s) and 0):
+      // a copy only if a_s < q_s -- flag non-canonical copy sources for the fixup
+      if (a.copy_src_mask && valid) {
+#pragma unroll
+        for (int s = 0; s < kMaxSrcBC; ++s)
+          noncanon |= ((a.copy_src_mask >> s) & 1) && xv[s] >= qs[s];
+      }
+      // targets that are source primes copy the source row through (rns.py:140-142):
+      // per thread here, or row copies after the kernel (tensor-store mode)
+      if (!a.use_tstore && valid) {
         for (int c = 0; c < n_copy; ++c) {
           const int e = sCopy[c];
           a.out[(int64_t)(e & 0xFFFF) * a.per_row + x] = raw[(e >> 16) * kRowsBC + r];
         }
+      }
+#ifdef TFHE_BC_TRACE_P
+      if (warp == 0) BTRACE(13, it);
+#endif
       mbar_arrive(&raw_empty[slot]);
       uint8_t* tile = sA + st * kMaxKC * kATileBC;
 #pragma unroll
@@ -229,14 +280,20 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
         *reinterpret_cast<uint4*>(tile + (k >> 5) * kATileBC + tile_off_bc(r, k & 31, kRowsBC)) =
             make_uint4(y[s0], y[s0 + 1], y[s0 + 2], y[s0 + 3]);
       }
+#ifdef TFHE_BC_TRACE_P
+      if (warp == 0) BTRACE(14, it);
+#endif
       fence_proxy_async_smem();
       mbar_arrive(&a_full[st]);
+      if (warp == 0) BTRACE(2, it);
       // refill this raw slot once every producer thread has read it
       if (tid == 0 && it + kRawBC < n_tiles) {
         mbar_wait(&raw_empty[slot], (it / kRawBC) & 1);
         issue(it + kRawBC);
+        BTRACE(12, it);
       }
     }
+    if (noncanon) *a.copy_flag = a.copy_gen;   // same value from every writer
   } else if (warp < 4 + kEpiWarpsBC) {
     // ---------------------------------------------------------------- epilogue
     // Two groups of 4 warps take alternate (tile, chunk) units u (group h: u
@@ -244,31 +301,46 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
     // 4 + 4h + g reads TMEM lane group g (rows 32g..32g+31) and all 32 targets
     // of its chunk in two halves.  The fold v = sum_i 2^(8i) C_i (< 2^48) is
     // reduced by one Montgomery step (R = 2^32, compensated in the constant
-    // operand: V_j carries 2^32).
+    // operand: V_j carries 2^32).  Tensor-store mode: results go to a
+    // [32 target][128 coefficient] staging tile (double-buffered per group)
+    // and one TMA tensor store per chunk writes the box (rows past n_dst and
+    // coefficients past per_row clipped); a copy target's column computes
+    // a_s mod q_s, i.e. the copy for canonical inputs (fixup kernel otherwise).
     const int g = (warp - 4) & 3, h = (warp - 4) >> 2, r = g * 32 + (tid & 31);
     const uint32_t lane_base = tmem + ((uint32_t)(g * 32) << 16);
-    int u = 0;
+    uint32_t* stage0 = sStage + h * 2 * kChunk * kRowsBC;
+    const int npairs = (nch + 1) >> 1;
+    int v = 0, k = 0;
     for (int it = 0; it < n_tiles; ++it) {
-      const int64_t x = (t_lo + it) * kRowsBC + r;
+      const int64_t x0 = (t_lo + it) * kRowsBC;
+      const int64_t x = x0 + r;
       const bool valid = x < a.per_row;
-      for (int ch = 0; ch < nch; ++ch, ++u) {
-        if ((u & 1) != h) continue;
-        const int buf = u & 3;
-        mbar_wait(&acc_full[buf], (u >> 2) & 1);
+      for (int cp = 0; cp < npairs; ++cp, ++v) {
+        // unit v = (tile, chunk pair): group h drains chunk 2 cp + h
+        const int buf = v & 1, ch = 2 * cp + h;
+        mbar_wait(&acc_full[buf], (v >> 1) & 1);
+        if (ch >= nch) {   // odd last pair: nothing to drain, release at once
+          mbar_arrive(&acc_empty[buf]);
+          continue;
+        }
+        uint32_t* stg = stage0 + (k & 1) * kChunk * kRowsBC;
+        if (g == 0) BTRACE(6 + 3 * h, it);
         tc_fence_after();
+        if (a.use_tstore) named_bar(1 + h, 128);   // this staging buffer's last store has read it
 #pragma unroll 1
         for (int hh = 0; hh < 2; ++hh) {
           uint32_t c[4][16];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) tmem_ld16(lane_base + buf * 128 + i * kChunk + hh * 16, c[i]);
+          for (int i = 0; i < 4; ++i)
+            tmem_ld16(lane_base + buf * kPairN + h * 128 + i * kChunk + hh * 16, c[i]);
           tmem_ld_wait();
           if (hh == 1) {
             tc_fence_before();
             mbar_arrive(&acc_empty[buf]);
+            if (g == 0) BTRACE(7 + 3 * h, it);
           }
           const int tb = ch * kChunk + hh * 16;
-          if (!valid || tb >= ba.n_dst) continue;
-          const uint32_t skip = sSkip[tb >> 4];
+          if (tb >= ba.n_dst) continue;
           uint32_t qv[16], qi[16];
 #pragma unroll
           for (int e = 0; e < 16; e += 4) {
@@ -277,49 +349,86 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
             qv[e] = q4.x; qv[e + 1] = q4.y; qv[e + 2] = q4.z; qv[e + 3] = q4.w;
             qi[e] = i4.x; qi[e + 1] = i4.y; qi[e + 2] = i4.z; qi[e + 3] = i4.w;
           }
-          // predicated stores down the target rows (skip = copies stored by the
-          // producers, and padding): no per-output branch or 64-bit multiply
-          uint32_t* o = a.out + (int64_t)tb * a.per_row + x;
+          uint32_t w[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             const uint32_t lo = c[0][e] + (c[1][e] << 8), hi = c[2][e] + (c[3][e] << 8);
             const uint64_t f = (uint64_t)lo + ((uint64_t)hi << 16);
             const uint32_t m = (uint32_t)f * qi[e];
-            const uint32_t w = (uint32_t)((f + (uint64_t)m * qv[e]) >> 32);
-            st_global_if(o, w >= qv[e] ? w - qv[e] : w, ((skip >> e) & 1) == 0);
-            o += a.per_row;
+            const uint32_t v = (uint32_t)((f + (uint64_t)m * qv[e]) >> 32);
+            w[e] = v >= qv[e] ? v - qv[e] : v;
+          }
+          if (a.use_tstore) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) stg[(hh * 16 + e) * kRowsBC + r] = w[e];
+          } else if (valid) {
+            // per-thread stores down the target rows (skip = copies and padding)
+            const uint32_t skip = sSkip[tb >> 4];
+            uint32_t* o = a.out + (int64_t)tb * a.per_row + x;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              st_global_if(o, w[e], ((skip >> e) & 1) == 0);
+              o += a.per_row;
+            }
           }
         }
+        if (a.use_tstore) {
+          // copy targets of this chunk: the source row from the raw slot (the
+          // producers' raw_full wait ordered the TMA fill; re-waited here)
+#ifndef TFHE_BC_TRACE_P
+          if (g == 0) BTRACE(13 + h, it);
+#endif
+          fence_proxy_async_smem();   // generic-proxy staging writes -> TMA reads
+          named_bar(1 + h, 128);
+#ifndef TFHE_BC_TRACE_P
+          if (g == 0) BTRACE(15, it);
+#endif
+          if (g == 0 && (tid & 31) == 0) {
+            tma_store_2d(&a.omap, stg, (int)x0, ch * kChunk);
+            bulk_commit();
+            bulk_wait_read<1>();   // the other staging buffer is free for the next chunk
+          }
+          __syncwarp();
+        }
+        if (g == 0) BTRACE(8 + 3 * h, it);
+        ++k;
       }
     }
+    if (g == 0 && (tid & 31) == 0 && a.use_tstore) bulk_wait_all();
   } else {
     // ---------------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc = idesc_i8(kRowsBC, kChunk);
+    // one MMA per (tile, chunk pair, K-step): N = 256 covers both chunks'
+    // four byte-plane accumulators side by side (n = 128 c + 32 i + t)
+    constexpr uint32_t idesc2 = idesc_i8(kRowsBC, kPairN), idesc1 = idesc_i8(kRowsBC, kPairN / 2);
     const bool leader = elect_one();
-    int u = 0;
+    const int npairs = (nch + 1) >> 1;
+    int v = 0;
     for (int it = 0; it < n_tiles; ++it) {
       const int st = it % kAStages;
       mbar_wait(&a_full[st], (it / kAStages) & 1);
+      BTRACE(3, it);
       tc_fence_after();
       const uint32_t aBase = smem_u32(sA + st * kMaxKC * kATileBC);
-      for (int ch = 0; ch < nch; ++ch, ++u) {
-        const int buf = u & 3;
-        if (u >= 4) mbar_wait(&acc_empty[buf], ((u >> 2) & 1) ^ 1);
+      for (int cp = 0; cp < npairs; ++cp, ++v) {
+        const int buf = v & 1;
+        if (v >= 2) mbar_wait(&acc_empty[buf], ((v >> 1) & 1) ^ 1);
+        BTRACE(4 + (cp & 1), it);
         tc_fence_after();
         if (leader) {
+          const uint32_t id = 2 * cp + 1 < nch ? idesc2 : idesc1;
           for (int kc = 0; kc < KC; ++kc) {
             const uint64_t adesc = smem_desc_kmajor(aBase + kc * kATileBC, kRowsBC * 16, 128);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint32_t bAddr =
-                  smem_u32(sB + ((i * kMaxChunks + ch) * kMaxKC + kc) * kBTileBC);
-              const uint64_t bdesc = smem_desc_kmajor(bAddr, kChunk * 16, 128);
-              mma_i8_ss(tmem + buf * 128 + i * kChunk, adesc, bdesc, idesc, kc != 0);
-            }
+            const uint64_t bdesc =
+                smem_desc_kmajor(smem_u32(sB + (cp * kMaxKC + kc) * kBTileBC), kPairN * 16, 128);
+            mma_i8_ss(tmem + buf * kPairN, adesc, bdesc, id, kc != 0);
           }
           mma_commit(&acc_full[buf]);
         }
         __syncwarp();
+#ifdef TFHE_BC_TRACE_M
+        mbar_wait(&acc_full[buf], (v >> 1) & 1);   // trace only: MMA completion latency
+        BTRACE(5, it);
+#endif
       }
       if (leader) mma_commit(&a_empty[st]);
       __syncwarp();
@@ -383,10 +492,27 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Copy-through fixup of the tensor-store mode: runs after bconv_tc_kernel and
+// does nothing unless that launch flagged a non-canonical copy source (then
+// the copy targets get the raw source rows, rns.py:140-142).
+__global__ void __launch_bounds__(256)
+    bconv_copy_fixup_kernel(const uint32_t* __restrict__ flag, uint32_t gen,
+                            const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                            const __grid_constant__ BconvArgs ba, int64_t per_row) {
+  if (*flag != gen) return;
+  for (int t = 0; t < ba.n_dst; ++t) {
+    const int s = ba.copy_from[t];
+    if (s < 0) continue;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per_row;
+         i += (int64_t)gridDim.x * blockDim.x)
+      out[(int64_t)t * per_row + i] = in[(int64_t)s * per_row + i];
+  }
+}
+
 }  // namespace
 
 int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,
-                 cudaStream_t st) {
+                 cudaStream_t st, bool exact_copies) {
   if (ba.n_dst <= 0) return 0;
   if (ba.n_src < 1 || ba.n_src > 4 * kMaxKC * 2 || ba.n_dst > kMaxBconvDst) {
     set_error("base conversion: 1..16 sources and at most 128 targets");
@@ -405,6 +531,7 @@ int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArg
     return 0;
   }
   BconvTcArgs a;
+  memset(&a, 0, sizeof(a));
   a.in = in;
   a.out = out;
   a.pc = c.d_pc;
@@ -437,16 +564,87 @@ int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArg
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
       a.use_tmap = 1;
   }
-  const int smem = 4 * kMaxChunks * kMaxKC * kBTileBC + kAStages * kMaxKC * kATileBC +
-                   kRawBC * kRawTileBC + kMaxBconvDst * (4 + 4 + 4) + kMaxBconvDst / 16 * 4 +
-                   (2 * kAStages + 8 + 2 * kRawBC) * 8 + 16;
+  a.use_tstore = 0;
+  if (a.use_tmap && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    // (encoder fetched above with the input map; per_row % 128 == 0 there)
+    typedef CUresult (*EncodeFn2)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    cudaDriverEntryPointQueryResult qr;
+    void* pfn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &pfn, cudaEnableDefault, &qr) ==
+            cudaSuccess && qr == cudaDriverEntryPointSuccess) {
+      cuuint64_t od[2] = {(cuuint64_t)a.per_row, (cuuint64_t)ba.n_dst};
+      cuuint64_t os[1] = {(cuuint64_t)a.per_row * 4};
+      cuuint32_t ob[2] = {(cuuint32_t)kRowsBC, (cuuint32_t)kChunk};
+      cuuint32_t oe[2] = {1, 1};
+      if (reinterpret_cast<EncodeFn2>(pfn)(&a.omap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, od, os,
+                                           ob, oe, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                           CU_TENSOR_MAP_SWIZZLE_NONE,
+                                           CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        a.use_tstore = 1;
+    }
+  }
+  if (getenv("TFHE_BC_NO_TSTORE")) a.use_tstore = 0;
+  // copy-through bookkeeping (tensor-store mode, callers that read the copies)
+  a.copy_src_mask = 0;
+  if (a.use_tstore && exact_copies) {
+    for (int t = 0; t < ba.n_dst; ++t)
+      if (ba.copy_from[t] >= 0) a.copy_src_mask |= 1u << ba.copy_from[t];
+    if (a.copy_src_mask) {
+      static uint32_t* flags[64] = {nullptr};
+      static uint32_t gen = 0;
+      uint32_t*& f = flags[c.dev & 63];
+      if (!f) {
+        if (cudaMalloc(&f, 4) != cudaSuccess || cudaMemset(f, 0, 4) != cudaSuccess) {
+          set_error("bconv copy flag allocation failed");
+          return 3;
+        }
+      }
+      if (++gen == 0) ++gen;
+      a.copy_flag = f;
+      a.copy_gen = gen;
+    }
+  }
+  const int smem = kMaxPairs * kMaxKC * kBTileBC + kAStages * kMaxKC * kATileBC +
+                   kRawBC * kRawTileBC + kStageWords * 4 + kMaxBconvDst * (4 + 4 + 4) +
+                   8 * 4 +
+                   kMaxBconvDst / 16 * 4 +
+                   (2 * kAStages + 4 + 2 * kRawBC) * 8 + 16;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(bconv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   const int grid = (int)std::min<int64_t>(a.tiles, c.sms);
+#ifdef TFHE_BC_TRACE
+  static unsigned long long* tbuf = nullptr;
+  if (!tbuf) cudaMalloc(&tbuf, 16 * kBTraceN * 8);
+  cudaMemsetAsync(tbuf, 0, 16 * kBTraceN * 8, st);
+  a.trace = tbuf;
+#endif
   bconv_tc_kernel<<<grid, kThreadsBC, smem, st>>>(a, ba);
+  // tensor-store mode: copy targets (rns.py:140-142) equal a_s mod q_s, the
+  // copy itself unless the input was non-canonical -- then the fixup copies
+  if (a.copy_src_mask) {
+    bconv_copy_fixup_kernel<<<c.sms * 4, 256, 0, st>>>(a.copy_flag, a.copy_gen, in, out, ba,
+                                                        a.per_row);
+  }
+#ifdef TFHE_BC_TRACE
+  {
+    std::vector<unsigned long long> hb(16 * kBTraceN);
+    cudaMemcpy(hb.data(), tbuf, hb.size() * 8, cudaMemcpyDeviceToHost);
+    static int seq = 0;
+    char fn[256];
+    snprintf(fn, sizeof(fn), "gpurun_out/btrace_%d.bin", seq++);
+    if (FILE* f = fopen(fn, "wb")) {
+      fwrite(hb.data(), 8, hb.size(), f);
+      fclose(f);
+    }
+  }
+#endif
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("bconv_tc launch: ") + cudaGetErrorString(e));

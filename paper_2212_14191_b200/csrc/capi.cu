@@ -385,15 +385,18 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
       for (int sl = 0; sl < S; ++sl) {
         const int j = j0 + sl, lo = j * g.alpha, hi = std::min(lo + g.alpha, g.l1);
         if (group_conv) {
-          // fast_basis_conv of the slice to every target prime (slice primes
-          // are copied through) into conv rows [sl*T, sl*T+T)
+          // fast_basis_conv of the slice to every target prime into conv rows
+          // [sl*T, sl*T+T); the slice's own rows (copies in rns.py:140-142)
+          // are never read -- the inner product skips them -- so they are
+          // left as don't-care values
           std::vector<int> src, dst;
           for (int q = lo; q < hi; ++q) src.push_back(q);
           for (int t = 0; t < g.T; ++t) dst.push_back(tprime(g, t));
           BconvArgs ba;
           if ((rc = fill_bconv(c, src, dst, ba))) return rc;
           if ((rc = launch_bconv(c, y_full + (size_t)lo * U, conv + (size_t)sl * g.T * U, ba,
-                                 batch, st)))
+                                 batch, st,
+                                 /*exact_copies=*/false)))
             return rc;
         }
         for (int t = 0; t < g.T; ++t) {

@@ -38,8 +38,10 @@ int launch_ks_mac_rot(const Ctx& c, const uint32_t* x, const uint32_t* base, con
                       int rows, int batch, uint32_t t, int perm_x, cudaStream_t st);
 int launch_automorph(const Ctx& c, const uint32_t* in, uint32_t* out, uint32_t t, int ntt_domain,
                      const int16_t* row_prime, int rows, int batch, cudaStream_t st);
+// exact_copies = false: rows of targets that are source primes may be left
+// with don't-care values (callers that never read them)
 int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,
-                 cudaStream_t st);
+                 cudaStream_t st, bool exact_copies = true);
 
 // Fused ModDown + rescale preparation, per row l = (component, chain row i < top):
 //   X = acc[acc_row] * P^-1 + base[base_row]     (in place; base_row < 0: none)

@@ -74,6 +74,37 @@ def test_bconv_tensor_core_vs_oracle(n, batch, n_src, n_dst, shared):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("n,batch,n_src,n_dst,shared,bad", [
+    (1 << 12, 7, 9, 54, 3, "one"), (1 << 12, 7, 9, 54, 3, "none"), (1 << 14, 4, 4, 40, 4, "all"),
+    (1 << 16, 2, 9, 54, 9, "one")])
+def test_bconv_copy_through_non_canonical(n, batch, n_src, n_dst, shared, bad):
+    """rns.py:140-142 copies a shared prime's row as is, even residues >= q
+    (RnsPolynomial does not enforce the bound).  The tensor-store kernel
+    computes copies as a mod q and a fixup launch restores the raw rows when a
+    copy source was non-canonical: bit-exact either way."""
+    from paper_2212_14191_b200.device import DeviceContext
+    from paper_2212_14191_b200.params import generate_primes
+    widths = [30] * 10 + [29] * 50 + [28] * 50 + [27] * 40
+    primes = generate_primes(n, widths[:n_src + n_dst])
+    src = primes[:n_src]
+    dst = list(primes[n_src:n_src + n_dst - shared]) + list(src[:shared])   # copies last
+    ctx = DeviceContext.get(n, tuple(primes[:n_src + n_dst]))
+    rng = np.random.default_rng(7 * n + n_src)
+    x = O.uniform_rows(rng, src, (batch, n))
+    if bad == "one":
+        x[1, batch - 1, n - 3] = 0xFFFFFFF0          # one residue >= q in a copy source
+    elif bad == "all":
+        x[:shared] |= np.uint32(1 << 31)             # every copy-source residue >= q
+    out = ctx.bconv(torch.from_numpy(x.view(np.int32)).cuda(), src, dst)
+    got = out.cpu().numpy().view(np.uint32)
+    want = O.fast_basis_conv(x, tuple(src), tuple(dst))
+    assert np.array_equal(got, want)
+    # the next launch (canonical input) must not see a stale fixup flag
+    x2 = O.uniform_rows(rng, src, (batch, n))
+    got2 = ctx.bconv(torch.from_numpy(x2.view(np.int32)).cuda(), src, dst).cpu().numpy()
+    assert np.array_equal(got2.view(np.uint32), O.fast_basis_conv(x2, tuple(src), tuple(dst)))
+
+
 @pytest.mark.parametrize("n,t", [(1 << 16, 5), (1 << 16, 25), (1 << 16, 63), (1 << 16, 5 + (1 << 16)),
                                  (1 << 12, 5), (1 << 13, 61), (1 << 16, 625), (1 << 16, (1 << 17) - 1)])
 def test_ntt_automorphism_vs_oracle(n, t):
