@@ -18,21 +18,33 @@
 // Montgomery step (V_j pre-scaled by 2^32) plus a conditional subtraction
 // gives the canonical result -- bit-identical to the reference.
 //
-// K = 4*alpha bytes (one 32-byte MMA K-step for alpha <= 8, two for <= 16);
-// targets are processed in chunks of 32 (N = 32): a chunk is 4 MMAs into
-// 4 x 32 TMEM columns, and TMEM holds 4 chunk buffers (512 columns).
-// Persistent, warp-specialised CTA (one per SM):
-//   warps 0-3  producers: source segments arrive by bulk copy (TMA engine)
-//              kRawBC tiles ahead; y_s = a_s * qhat_inv (Shoup), 16-byte
-//              st.shared of 4 sources per row into the K-major A ring
-//   warps 4-11 epilogue: TMEM -> fold -> Montgomery mod p_t -> coalesced stores
-//              (two warps per TMEM lane group, each half of a target chunk)
-//   warp 12    TMEM owner; one elected lane issues the MMAs
-// The kernel is HBM-bound for small alpha (alpha*4 bytes read, T*4 written
-// per coefficient); the tensor cores remove the alpha*T mul-mods per
-// coefficient that bound the CUDA-core form at large alpha.  Tiny
-// conversions (alpha <= 4, alpha * T <= 32) take an element-wise fast path
-// (bconv_small_kernel) instead of mostly-padding MMA tiles.
+// K = 4*alpha bytes (one 32-byte MMA K-step for alpha <= 8, two for <= 16).
+// Targets come in chunks of 32, and one MMA (M = 128 coefficients, N = 256)
+// covers a chunk PAIR: its B operand holds both chunks' four byte planes
+// side by side (n = 128 c + 32 i + t), so a tile costs KC MMAs per pair;
+// TMEM holds two pair buffers (2 x 256 columns).
+// Persistent, warp-specialised CTA (one per SM, 21 warps, <= 96 registers):
+//   warps 0-3   producers: source rows arrive by one TMA tensor load per tile
+//               kRawBC tiles ahead; y_s = a_s * qhat_inv (Shoup), 16-byte
+//               st.shared of 4 sources per row into the K-major A ring
+//   warps 4-19  epilogue: group h (8 warps) drains chunk h of the pair, warp
+//               (lane quarter g, half hh) 16 targets of 32 rows: TMEM -> fold
+//               -> Montgomery mod p_t -> [32 target][128 coefficient] staging
+//               tile in shared memory (double-buffered per group), written by
+//               ONE TMA tensor store per chunk (rows past n_dst and
+//               coefficients past per_row clipped by the tensor map)
+//   warp 20     TMEM owner; one elected lane issues the MMAs
+// Copy targets (a target that is source prime s, rns.py:140-142) have the
+// factors (Q/q_s) mod q_s and 0, so their column computes a_s mod q_s: the
+// copy itself for canonical residues.  Producers flag non-canonical copy
+// sources and a fixup launch then copies the raw rows (bit-exact for any u32
+// input); callers that never read the copies (the key switch skips a slice's
+// own rows) pass exact_copies = false.
+// The kernel is HBM-bound by design (alpha*4 bytes read, T*4 written per
+// coefficient); the tensor cores remove the alpha*T mul-mods per coefficient
+// that bound the CUDA-core form.  Tiny conversions (alpha <= 4, alpha * T <=
+// 32) take an element-wise fast path (bconv_small_kernel) instead of
+// mostly-padding MMA tiles.  Timeline probes: -DTFHE_BC_TRACE.
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -54,7 +66,7 @@ constexpr int kAStages = 4;
 constexpr int kChunk = 32;           // targets per MMA (N)
 constexpr int kMaxChunks = kMaxBconvDst / kChunk;
 constexpr int kMaxKC = 2;            // 32-byte K-steps (alpha <= 16)
-constexpr int kEpiWarpsBC = 8;
+constexpr int kEpiWarpsBC = 16;         // 2 chunks x 2 target halves x 4 lane quarters
 constexpr int kMmaWarpBC = 4 + kEpiWarpsBC;
 constexpr int kThreadsBC = 32 * (kMmaWarpBC + 1);
 constexpr int kATileBC = kRowsBC * 32;           // 4 KB per K-step
@@ -120,7 +132,10 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
   int* sCopy = reinterpret_cast<int*>(sQinv + kMaxBconvDst);      // copy list: t | s << 16
   int* sCopyLo = sCopy + kMaxBconvDst;                             // per chunk: first copy
   uint32_t* sSkip = reinterpret_cast<uint32_t*>(sCopyLo + 8);      // per 16 targets
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(sSkip + kMaxBconvDst / 16);
+  uint32_t* sSrcQ = sSkip + kMaxBconvDst / 16;                     // per source: q | qhat_inv | Shoup
+  uint32_t* sSrcH = sSrcQ + kMaxSrcBC;
+  uint32_t* sSrcHs = sSrcH + kMaxSrcBC;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sSrcHs + kMaxSrcBC);
   uint64_t* a_empty = a_full + kAStages;
   uint64_t* acc_full = a_empty + kAStages;
   uint64_t* acc_empty = acc_full + 2;
@@ -159,6 +174,12 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
   }
   int n_copy = 0;
   for (int t = 0; t < ba.n_dst; ++t) n_copy += ba.copy_from[t] >= 0;
+  if (tid < kMaxSrcBC) {
+    const bool live = tid < ba.n_src;
+    sSrcQ[tid] = live ? a.pc[ba.src_prime[tid]].q : 1u;
+    sSrcH[tid] = live ? ba.qhat_inv[tid] : 0u;
+    sSrcHs[tid] = live ? ba.qhat_inv_shoup[tid] : 0u;
+  }
   if (tid < kMaxBconvDst / 16) {
     // epilogue skip mask per 16 targets: copies (stored by the producers) and padding
     uint32_t m = 0;
@@ -212,13 +233,6 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
     // each thread then converts its coefficient: y_s = a_s * qhat_inv_s.
     const int r = tid;
     const int nsrc = ba.n_src;
-    uint32_t qs[kMaxSrcBC], hs[kMaxSrcBC], hss[kMaxSrcBC];
-#pragma unroll
-    for (int s = 0; s < kMaxSrcBC; ++s) {
-      qs[s] = s < nsrc ? a.pc[ba.src_prime[s]].q : 1;
-      hs[s] = s < nsrc ? ba.qhat_inv[s] : 0;
-      hss[s] = s < nsrc ? ba.qhat_inv_shoup[s] : 0;
-    }
     auto issue = [&](int it) {
       const int slot = it % kRawBC;
       const int64_t x0 = (t_lo + it) * kRowsBC;
@@ -244,21 +258,28 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
       const int64_t x = (t_lo + it) * kRowsBC + r;
       const bool valid = x < a.per_row;
       const uint32_t* raw = reinterpret_cast<const uint32_t*>(sRaw + slot * kRawTileBC);
-      // branch-free: all 16 source rows are read (rows >= nsrc hold stale data)
-      // and the padding sources have qhat_inv = 0, q = 1, so their y is 0;
-      // rows past per_row are clipped at the store
-      uint32_t xv[kMaxSrcBC], y[kMaxSrcBC];
+      // branch-free: the source rows of the K-steps in use are read (rows >=
+      // nsrc hold stale data; their qhat_inv = 0, q = 1 give y = 0), four
+      // sources = one 16-byte segment of the A tile; rows past per_row are
+      // clipped at the store.  Tensor-store mode computes a copy target as
+      // y_s (Q/q_s) mod q_s = a_s mod q_s (a target that is source s has
+      // factors (Q/q_s) and 0), a copy only if a_s < q_s: non-canonical copy
+      // sources are flagged for the fixup launch.
+      uint32_t y[kMaxSrcBC];
 #pragma unroll
-      for (int s = 0; s < kMaxSrcBC; ++s) xv[s] = raw[s * kRowsBC + r];
+      for (int s0 = 0; s0 < kMaxSrcBC; s0 += 4) {
+        if (s0 >= 8 * KC) break;
+        const uint4 q4 = *reinterpret_cast<const uint4*>(sSrcQ + s0);
+        const uint4 h4 = *reinterpret_cast<const uint4*>(sSrcH + s0);
+        const uint4 p4 = *reinterpret_cast<const uint4*>(sSrcHs + s0);
+        const uint32_t qv[4] = {q4.x, q4.y, q4.z, q4.w}, hv[4] = {h4.x, h4.y, h4.z, h4.w},
+                       pv[4] = {p4.x, p4.y, p4.z, p4.w};
 #pragma unroll
-      for (int s = 0; s < kMaxSrcBC; ++s) y[s] = mul_shoup(xv[s], hs[s], hss[s], qs[s]);
-      // tensor-store mode computes a copy target as y_s (Q/q_s) mod q_s = a_s mod q_s
-      // (the conversion factors of a target that is source s are (Q/q_s) and 0):
-      // a copy only if a_s < q_s -- flag non-canonical copy sources for the fixup
-      if (a.copy_src_mask && valid) {
-#pragma unroll
-        for (int s = 0; s < kMaxSrcBC; ++s)
-          noncanon |= ((a.copy_src_mask >> s) & 1) && xv[s] >= qs[s];
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t xs = raw[(s0 + e) * kRowsBC + r];
+          y[s0 + e] = mul_shoup(xs, hv[e], pv[e], qv[e]);
+          noncanon |= ((a.copy_src_mask >> (s0 + e)) & 1) && valid && xs >= qv[e];
+        }
       }
       // targets that are source primes copy the source row through (rns.py:140-142):
       // per thread here, or row copies after the kernel (tensor-store mode)
@@ -306,7 +327,9 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
     // and one TMA tensor store per chunk writes the box (rows past n_dst and
     // coefficients past per_row clipped); a copy target's column computes
     // a_s mod q_s, i.e. the copy for canonical inputs (fixup kernel otherwise).
-    const int g = (warp - 4) & 3, h = (warp - 4) >> 2, r = g * 32 + (tid & 31);
+    const int we = warp - 4, g = we & 3, h = we >> 3, hh = (we >> 2) & 1;
+    const int r = g * 32 + (tid & 31);
+    const bool issuer = g == 0 && hh == 0 && (tid & 31) == 0;   // the group's store thread
     const uint32_t lane_base = tmem + ((uint32_t)(g * 32) << 16);
     uint32_t* stage0 = sStage + h * 2 * kChunk * kRowsBC;
     const int npairs = (nch + 1) >> 1;
@@ -316,7 +339,8 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
       const int64_t x = x0 + r;
       const bool valid = x < a.per_row;
       for (int cp = 0; cp < npairs; ++cp, ++v) {
-        // unit v = (tile, chunk pair): group h drains chunk 2 cp + h
+        // unit v = (tile, chunk pair): group h drains chunk 2 cp + h, warp
+        // (g, hh) its TMEM lane quarter g and targets [16 hh, 16 hh + 16)
         const int buf = v & 1, ch = 2 * cp + h;
         mbar_wait(&acc_full[buf], (v >> 1) & 1);
         if (ch >= nch) {   // odd last pair: nothing to drain, release at once
@@ -324,77 +348,64 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
           continue;
         }
         uint32_t* stg = stage0 + (k & 1) * kChunk * kRowsBC;
-        if (g == 0) BTRACE(6 + 3 * h, it);
+        if (g == 0 && hh == 0) BTRACE(6 + 3 * h, it);
         tc_fence_after();
-        if (a.use_tstore) named_bar(1 + h, 128);   // this staging buffer's last store has read it
-#pragma unroll 1
-        for (int hh = 0; hh < 2; ++hh) {
-          uint32_t c[4][16];
+        if (a.use_tstore) named_bar(1 + h, 16 * kEpiWarpsBC);   // staging buffer free again
+#pragma unroll
+        for (int q8 = 0; q8 < 2; ++q8) {
+          uint32_t c[4][8];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            tmem_ld16(lane_base + buf * kPairN + h * 128 + i * kChunk + hh * 16, c[i]);
+            tmem_ld8(lane_base + buf * kPairN + h * 128 + i * kChunk + hh * 16 + q8 * 8, c[i]);
           tmem_ld_wait();
-          if (hh == 1) {
+          if (q8 == 1) {
             tc_fence_before();
             mbar_arrive(&acc_empty[buf]);
-            if (g == 0) BTRACE(7 + 3 * h, it);
+            if (g == 0 && hh == 0) BTRACE(7 + 3 * h, it);
           }
-          const int tb = ch * kChunk + hh * 16;
+          const int tb = ch * kChunk + hh * 16 + q8 * 8;
           if (tb >= ba.n_dst) continue;
-          uint32_t qv[16], qi[16];
+          const uint4 qa = *reinterpret_cast<const uint4*>(sQ + tb);
+          const uint4 qb = *reinterpret_cast<const uint4*>(sQ + tb + 4);
+          const uint4 ia = *reinterpret_cast<const uint4*>(sQinv + tb);
+          const uint4 ib = *reinterpret_cast<const uint4*>(sQinv + tb + 4);
+          const uint32_t qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+          const uint32_t qi[8] = {ia.x, ia.y, ia.z, ia.w, ib.x, ib.y, ib.z, ib.w};
+          uint32_t w[8];
 #pragma unroll
-          for (int e = 0; e < 16; e += 4) {
-            const uint4 q4 = *reinterpret_cast<const uint4*>(sQ + tb + e);
-            const uint4 i4 = *reinterpret_cast<const uint4*>(sQinv + tb + e);
-            qv[e] = q4.x; qv[e + 1] = q4.y; qv[e + 2] = q4.z; qv[e + 3] = q4.w;
-            qi[e] = i4.x; qi[e + 1] = i4.y; qi[e + 2] = i4.z; qi[e + 3] = i4.w;
-          }
-          uint32_t w[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const uint32_t lo = c[0][e] + (c[1][e] << 8), hi = c[2][e] + (c[3][e] << 8);
-            const uint64_t f = (uint64_t)lo + ((uint64_t)hi << 16);
-            const uint32_t m = (uint32_t)f * qi[e];
-            const uint32_t v = (uint32_t)((f + (uint64_t)m * qv[e]) >> 32);
-            w[e] = v >= qv[e] ? v - qv[e] : v;
+          for (int e = 0; e < 8; ++e) {
+            const uint32_t t = fold4_redc(c[0][e], c[1][e], c[2][e], c[3][e], qv[e], qi[e]);
+            w[e] = min(t, t - qv[e]);   // [0, 2q) -> [0, q)
           }
           if (a.use_tstore) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) stg[(hh * 16 + e) * kRowsBC + r] = w[e];
+            for (int e = 0; e < 8; ++e) stg[(tb - ch * kChunk + e) * kRowsBC + r] = w[e];
           } else if (valid) {
             // per-thread stores down the target rows (skip = copies and padding)
-            const uint32_t skip = sSkip[tb >> 4];
+            const uint32_t skip = sSkip[tb >> 4] >> (tb & 15);
             uint32_t* o = a.out + (int64_t)tb * a.per_row + x;
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
+            for (int e = 0; e < 8; ++e) {
               st_global_if(o, w[e], ((skip >> e) & 1) == 0);
               o += a.per_row;
             }
           }
         }
         if (a.use_tstore) {
-          // copy targets of this chunk: the source row from the raw slot (the
-          // producers' raw_full wait ordered the TMA fill; re-waited here)
-#ifndef TFHE_BC_TRACE_P
-          if (g == 0) BTRACE(13 + h, it);
-#endif
           fence_proxy_async_smem();   // generic-proxy staging writes -> TMA reads
-          named_bar(1 + h, 128);
-#ifndef TFHE_BC_TRACE_P
-          if (g == 0) BTRACE(15, it);
-#endif
-          if (g == 0 && (tid & 31) == 0) {
+          named_bar(1 + h, 16 * kEpiWarpsBC);
+          if (issuer) {
             tma_store_2d(&a.omap, stg, (int)x0, ch * kChunk);
             bulk_commit();
             bulk_wait_read<1>();   // the other staging buffer is free for the next chunk
           }
           __syncwarp();
         }
-        if (g == 0) BTRACE(8 + 3 * h, it);
+        if (g == 0 && hh == 0) BTRACE(8 + 3 * h, it);
         ++k;
       }
     }
-    if (g == 0 && (tid & 31) == 0 && a.use_tstore) bulk_wait_all();
+    if (issuer && a.use_tstore) bulk_wait_all();
   } else {
     // ---------------------------------------------------------------- MMA issuer
     // one MMA per (tile, chunk pair, K-step): N = 256 covers both chunks'
@@ -610,7 +621,7 @@ int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArg
   }
   const int smem = kMaxPairs * kMaxKC * kBTileBC + kAStages * kMaxKC * kATileBC +
                    kRawBC * kRawTileBC + kStageWords * 4 + kMaxBconvDst * (4 + 4 + 4) +
-                   8 * 4 +
+                   8 * 4 + 3 * kMaxSrcBC * 4 +
                    kMaxBconvDst / 16 * 4 +
                    (2 * kAStages + 4 + 2 * kRawBC) * 8 + 16;
   static bool attr = false;
