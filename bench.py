@@ -320,7 +320,10 @@ def run_b200(args):
                       np.array_equal(y[:2, :1].cpu().numpy().view(np.uint32), xs))
 
     stream = torch.cuda.current_stream(dev)
-    with ClockSampler(local) as clk:
+    from paper_2212_14191_b200 import _lib as tl
+    # per-kernel device times over the timed region: the library brackets each
+    # NTT-pass launch with CUDA events on its own (= this) stream
+    with ClockSampler(local) as clk, tl.kernel_timer() as ktime:
         barrier()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -646,7 +649,9 @@ def run_b200(args):
     if peak is None:
         peak = 2 * 1617.8
         peak_src = "derived: 2 x MEASURED_PEAKS.json bf16_tflops (int8 dense = 2x bf16)"
-    traffic = None
+    # DRAM bytes per launch of the dominant kernel / per NTT call, from one
+    # ncu capture of this configuration (profiles/ntt_dram_traffic.json)
+    traffic, traffic_call = None, None
     tpath = os.path.join(ROOT, "profiles", "ntt_dram_traffic.json")
     if os.path.exists(tpath):
         try:
@@ -654,9 +659,13 @@ def run_b200(args):
                 t = json.load(fh)
             if t.get("batch") == B and t.get("limbs") == L and \
                     tuple(t.get("transform_plan", ())) == tuple(kplan):
-                traffic = t.get("bytes_per_ntt_call")
+                traffic_call = t.get("bytes_per_ntt_call")
+                cols = [r for r in t.get("launches", []) if "col_kernel" in r["kernel"]]
+                if cols:
+                    traffic = sum(r["dram_read_bytes"] + r["dram_write_bytes"]
+                                  for r in cols) / len(cols)
         except Exception:
-            traffic = None
+            traffic, traffic_call = None, None
     hpeak, hsrc = 6546.6, "fallback (B200_PROFILING.md)"
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -668,6 +677,59 @@ def run_b200(args):
     hbm_bound = t_hbm >= 0.8 * t_tensor
     rates = cpu_oracle_rate(primes, args.cpu_members) if world == 1 and args.cpu_members > 0 \
         else None
+    # Roofline of the DOMINANT kernel of the step, timed live: its average
+    # launch duration from the events the library recorded around every
+    # launch in the timed region (tfhe_profile_*, on the launching stream).
+    # Three-factor plan: the column pass (1024-point column transforms, fwd
+    # and inv) reads the u32 limb rows and writes P^T -- 8 N algorithmic bytes
+    # per limb per launch, L*B limbs per launch; the row pass reads P^T and
+    # writes the output (the same 8 N).  The call-level figure beside it counts
+    # only the compulsory 8 N per limb-NTT of the whole call (two passes).
+    fam = {}
+    for name, (cnt, tot) in ktime.times.items():
+        key = name.split("<")[0]
+        c0, t0 = fam.get(key, (0, 0.0))
+        fam[key] = (c0 + cnt, t0 + tot)
+    step_kernel_ms = sum(t for _, t in fam.values())
+    kern_rows = {}
+    for key, (cnt, tot) in fam.items():
+        avg = tot / max(cnt, 1)
+        gbs = L * B * 8 * N / (avg / 1e3) / 1e9
+        kern_rows[key] = {"launches": cnt, "avg_launch_ms": avg, "share_of_step": tot / max(ms, 1e-9),
+                          "achieved_gbs": gbs, "frac": gbs / hpeak}
+    dom = max(fam, key=lambda k: fam[k][1]) if fam else None
+    call_level = {"achieved": achieved_gbs, "unit": "GB/s", "frac": achieved_gbs / hpeak,
+                  "algorithmic": f"8*N = {8 * N} B per limb-NTT over the whole call "
+                                 f"({L * B} limbs per call, two launches)",
+                  "traffic": traffic_call}
+    tensor_view = {"achieved": achieved_tops, "peak": peak, "unit": "TOPS (int8)",
+                   "frac": achieved_tops / peak, "peak_source": peak_src,
+                   "algorithmic": f"32*N*(k0+k1+k2), plan {list(kplan)}: "
+                                  f"{ops_per_limb / 1e9:.3f} G int8-ops per limb-NTT"}
+    if dom is not None and hbm_bound:
+        d = kern_rows[dom]
+        roofline = {"bound": "hbm", "achieved": d["achieved_gbs"], "peak": hpeak, "unit": "GB/s",
+                    "frac": d["frac"], "traffic": traffic,
+                    "kernel": f"{dom} (fwd + inv launches)",
+                    "algorithmic": f"8*N = {8 * N} B per limb (u32 rows in, P^T out) x {L * B} "
+                                   "limbs per launch",
+                    "launch_ms": d["avg_launch_ms"], "launches": d["launches"],
+                    "peak_source": hsrc,
+                    "timing": "CUDA events around every launch in the timed region, "
+                              "on the launching stream (tfhe_profile_read)",
+                    "kernels": kern_rows, "kernels_share_of_timed_region": step_kernel_ms / ms,
+                    "call_level": call_level,
+                    "tensor_view": tensor_view}
+    elif hbm_bound:
+        roofline = dict(call_level, bound="hbm", peak=hpeak, peak_source=hsrc,
+                        kernel="one NTT call", tensor_view=tensor_view)
+    else:
+        roofline = {"bound": "tensor", "achieved": achieved_tops, "peak": peak,
+                    "unit": "TOPS (int8)", "frac": achieved_tops / peak, "traffic": traffic_call,
+                    "algorithmic": f"32*N*(k0+k1+k2), plan {list(kplan)}: "
+                                   f"{ops_per_limb / 1e9:.3f} G int8-ops per limb-NTT x "
+                                   f"{L * B} limbs per call",
+                    "peak_source": peak_src, "kernels": kern_rows}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -677,28 +739,7 @@ def run_b200(args):
                        transform_plan=list(kplan)),
         "poly_ntt_kops": value / L,
         "parity_spot_check": parity,
-        "roofline": ({"bound": "hbm", "achieved": achieved_gbs, "peak": hpeak, "unit": "GB/s",
-                      "frac": achieved_gbs / hpeak, "traffic": traffic,
-                      "algorithmic": f"8*N = {8 * N} B per limb-NTT (u32 in + out) x {L * B} "
-                                     "limbs per call",
-                      "peak_source": hsrc,
-                      "kernel": "ntt_col_kernel + ntt_row_kernel (one NTT call = 2 launches)"
-                      if sum(kplan) == 128 else "ntt_ts_kernel (stage 1 + stage 2 per NTT call)",
-                      "design_traffic": f"16*N per limb-NTT: two HBM passes (P^T round trip), "
-                                        f"{16 * N * L * B} B per call",
-                      "tensor_view": {"achieved": achieved_tops, "peak": peak,
-                                      "unit": "TOPS (int8)", "frac": achieved_tops / peak,
-                                      "peak_source": peak_src,
-                                      "algorithmic": f"32*N*(k0+k1+k2), plan {list(kplan)}: "
-                                                     f"{ops_per_limb / 1e9:.3f} G int8-ops per "
-                                                     "limb-NTT"}}
-                     if hbm_bound else
-                     {"bound": "tensor", "achieved": achieved_tops, "peak": peak,
-                      "unit": "TOPS (int8)", "frac": achieved_tops / peak, "traffic": traffic,
-                      "algorithmic": f"32*N*(k0+k1+k2), plan {list(kplan)}: "
-                                     f"{ops_per_limb / 1e9:.3f} G int8-ops per limb-NTT x "
-                                     f"{L * B} limbs per call",
-                      "peak_source": peak_src}),
+        "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * bytes_per_call,
                 "d2h_bytes_per_step": 2 * bytes_per_call, "steps": e2e_steps,
                 "api": "batched_apply(BatchBuffer(pinned host), 'ntt'/'intt')",
@@ -706,7 +747,7 @@ def run_b200(args):
                 "pcie_duplex_gbs": duplex,
                 "frac_of_pcie_duplex": (4 * bytes_per_call * e2e_steps / e2e_s / 1e9 / duplex)
                 if duplex else None},
-        "gpu_launches": 4 * args.steps,
+        "gpu_launches": sum(c for c, _ in fam.values()) if fam else 4 * args.steps,
         "clocks": clk.summary(),
     }
     if hm:

@@ -192,6 +192,16 @@ int tfhe_rescale_part(TfheCtx* ctx, const uint32_t* ct_local, const uint32_t* to
  * for a private context the caller then destroys. */
 int tfhe_debug_corrupt_twiddle(TfheCtx* ctx, int prime);
 
+/* ---- per-kernel device timing (measurement aid) ---------------------------
+ * While enabled (process-wide), every launch of the library's NTT-pass,
+ * fused-NTT and base-conversion kernels is bracketed by two CUDA events
+ * recorded on its launching stream.  tfhe_profile_read waits for those events
+ * and writes one line per kernel family, "name<TAB>launches<TAB>total_ms\n",
+ * into buf (NUL-terminated, truncated to len), then forgets the records.
+ * Returns the number of families, or a negative code. */
+int tfhe_profile_enable(int enable);
+int tfhe_profile_read(char* buf, size_t len);
+
 #ifdef __cplusplus
 }
 #endif

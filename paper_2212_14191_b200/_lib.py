@@ -73,6 +73,8 @@ SIGNATURES = {
     "tfhe_ctx_transform_plan": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int),
                                                ctypes.POINTER(ctypes.c_int),
                                                ctypes.POINTER(ctypes.c_int)]),
+    "tfhe_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "tfhe_profile_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t]),
 }
 
 _lib = None
@@ -125,3 +127,30 @@ def i32_array(values):
 def u32_array(values):
     vals = [int(v) for v in values]
     return (ctypes.c_uint32 * max(len(vals), 1))(*vals)
+
+
+class kernel_timer:
+    """Per-kernel device timing (tfhe_profile_enable / tfhe_profile_read):
+    inside the `with` block every NTT-pass, fused-NTT and base-conversion
+    launch is bracketed by CUDA events on its own stream; `.times` then maps
+    kernel family -> (launches, total device ms)."""
+
+    def __enter__(self):
+        L = load()
+        L.tfhe_profile_read(None, 0)   # drop stale records
+        L.tfhe_profile_enable(1)
+        self.times = {}
+        return self
+
+    def __exit__(self, *exc):
+        L = load()
+        L.tfhe_profile_enable(0)
+        buf = ctypes.create_string_buffer(1 << 16)
+        n = L.tfhe_profile_read(buf, len(buf))
+        if n < 0:
+            raise DeviceError("tfhe_profile_read failed: " +
+                              (L.tfhe_last_error() or b"").decode(errors="replace"))
+        for line in buf.value.decode().splitlines():
+            name, count, ms = line.split("\t")
+            self.times[name] = (int(count), float(ms))
+        return False

@@ -636,7 +636,9 @@ int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArg
   cudaMemsetAsync(tbuf, 0, 16 * kBTraceN * 8, st);
   a.trace = tbuf;
 #endif
+  prof_begin("bconv_tc_kernel", st);
   bconv_tc_kernel<<<grid, kThreadsBC, smem, st>>>(a, ba);
+  prof_end(st);
   // tensor-store mode: copy targets (rns.py:140-142) equal a_s mod q_s, the
   // copy itself unless the input was non-canonical -- then the fixup copies
   if (a.copy_src_mask) {

@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1219,6 +1221,94 @@ int tfhe_ntt_host(TfheCtx* h, const uint32_t* host_in, uint32_t* host_out,
     return TFHE_ECUDA;
   }
   return 0;
+}
+
+}  // extern "C"
+
+// ============================================================ per-kernel timing
+namespace tfhe {
+namespace {
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+std::atomic<bool> g_prof{false};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof_recs;
+std::vector<cudaEvent_t> g_prof_pool;
+thread_local ProfRec t_open = {nullptr, nullptr, nullptr};
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+void prof_begin(const char* name, cudaStream_t st) {
+  if (!g_prof.load(std::memory_order_relaxed)) return;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  t_open.name = name;
+  t_open.a = prof_event();
+  t_open.b = prof_event();
+  cudaEventRecord(t_open.a, st);
+}
+void prof_end(cudaStream_t st) {
+  if (!t_open.name) return;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  cudaEventRecord(t_open.b, st);
+  g_prof_recs.push_back(t_open);
+  t_open = {nullptr, nullptr, nullptr};
+}
+}  // namespace tfhe
+
+extern "C" {
+
+int tfhe_profile_enable(int enable) {
+  tfhe::g_prof.store(enable != 0);
+  return 0;
+}
+
+int tfhe_profile_read(char* buf, size_t len) {
+  using namespace tfhe;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  std::vector<std::string> names;
+  std::vector<std::pair<int, double>> acc;
+  for (const ProfRec& r : g_prof_recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) {
+      set_error("tfhe_profile_read: event synchronisation failed");
+      return -TFHE_ECUDA;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    size_t k = 0;
+    while (k < names.size() && names[k] != r.name) ++k;
+    if (k == names.size()) {
+      names.push_back(r.name);
+      acc.push_back({0, 0.0});
+    }
+    acc[k].first += 1;
+    acc[k].second += ms;
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof_recs.clear();
+  std::string out;
+  for (size_t k = 0; k < names.size(); ++k) {
+    char line[256];
+    snprintf(line, sizeof(line), "%s\t%d\t%.6f\n", names[k].c_str(), acc[k].first, acc[k].second);
+    out += line;
+  }
+  if (buf && len) {
+    const size_t n = std::min(len - 1, out.size());
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int)names.size();
 }
 
 }  // extern "C"

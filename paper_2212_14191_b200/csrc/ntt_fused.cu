@@ -653,7 +653,9 @@ int launch_ntt_fused(const Ctx& c, const uint32_t* in, uint32_t* out, const Limb
 #endif
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem);
+    prof_begin("ntt_fused_kernel", st);
     kern<<<grid, kFThreads, kFSmem, st>>>(a);
+    prof_end(st);
   };
   if (inverse) {
     if (mode == EPI_SUB_SCALE) go(ntt_fused_kernel<EPI_SUB_SCALE, true>);

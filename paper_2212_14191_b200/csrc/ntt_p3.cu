@@ -1191,7 +1191,9 @@ int launch_p3_col(const Ctx& c, const uint32_t* in, uint32_t* P, const LimbMap& 
 #endif
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kC1Smem);
+    prof_begin(inverse ? "ntt_col_kernel<inv>" : "ntt_col_kernel<fwd>", st);
     kern<<<grid, kPThreads, kC1Smem, st>>>(a);
+    prof_end(st);
   };
   if (inverse) go(ntt_col_kernel<true>);
   else go(ntt_col_kernel<false>);
@@ -1268,7 +1270,11 @@ int launch_p3_row(const Ctx& c, const uint32_t* P, uint32_t* out, const LimbMap&
   a.strided = strided_env >= 0 ? strided_env : (mode == EPI_KS_ACC || mode == EPI_KS_MAC);
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kC2Smem);
+    static const char* const names[] = {"ntt_row_kernel<store>", "ntt_row_kernel<sub_scale>",
+                                        "ntt_row_kernel<ks_mac>", "ntt_row_kernel<ks_acc>"};
+    prof_begin(mode >= 0 && mode < 4 ? names[mode] : "ntt_row_kernel", st);
     kern<<<grid, kRowThreads, kC2Smem, st>>>(a);
+    prof_end(st);
   };
   if (mode == EPI_KS_ACC) go(ntt_row_kernel<EPI_KS_ACC>);
   else if (mode == EPI_SUB_SCALE) go(ntt_row_kernel<EPI_SUB_SCALE>);

@@ -157,5 +157,9 @@ int launch_ntt(const Ctx& c, const uint32_t* in, uint32_t* out, const LimbMap& m
 int build_ntt_tables(Ctx& c);
 
 void set_error(const std::string& msg);
+// per-kernel device timing (tfhe_profile_enable): events around a launch on
+// its stream; no-ops unless enabled
+void prof_begin(const char* name, cudaStream_t st);
+void prof_end(cudaStream_t st);
 
 }  // namespace tfhe

@@ -9,6 +9,8 @@ primes = par.generate_primes(n, [29] * L)
 ctx = DeviceContext.get(n, primes)
 x = torch.randint(0, 1 << 28, (L, B, n), dtype=torch.int32, device="cuda")
 out = torch.empty_like(x)
-for _ in range(3):
+back = torch.empty_like(x)
+for _ in range(2):
     ctx.ntt(x, primes, out=out)
+    ctx.ntt(out, primes, inverse=True, out=back)
 torch.cuda.synchronize()
