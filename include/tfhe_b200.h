@@ -192,6 +192,23 @@ int tfhe_rescale_part(TfheCtx* ctx, const uint32_t* ct_local, const uint32_t* to
  * for a private context the caller then destroys. */
 int tfhe_debug_corrupt_twiddle(TfheCtx* ctx, int prime);
 
+/* ---- client-side CRT (ref rns.py:77-115, ckks.py:194-213) -----------------
+ * tfhe_crt_decompose: n signed coefficients (device; kind 0 = int64, kind 1 =
+ * float64 rounded half to even like np.rint, any finite magnitude) -> n_limbs
+ * canonical residue rows `out` (n_limbs, n), row l mod prime limb_prime[l]:
+ * crt_decompose of the encode / _encode_signed path.
+ * tfhe_crt_compose: residue rows (n_limbs, n) -> the CRT representative
+ * centred in (-Q/2, Q/2] (ckks._centered), as float64 rounded half to even
+ * (Python float(int); +-inf past the double range) into out_f64 (nullable) and
+ * as n_words-word little-endian two's complement into out_words (nullable,
+ * layout (n_words, n)).  tfhe_crt_words: words of Q for that basis (use
+ * n_words >= words + 1 for the sign). */
+int tfhe_crt_decompose(TfheCtx* ctx, const void* coeffs, int kind, int64_t n,
+                       const int32_t* limb_prime, int n_limbs, uint32_t* out, void* stream);
+int tfhe_crt_words(const TfheCtx* ctx, const int32_t* limb_prime, int n_limbs);
+int tfhe_crt_compose(TfheCtx* ctx, const uint32_t* rows, const int32_t* limb_prime, int n_limbs,
+                     int64_t n, double* out_f64, uint32_t* out_words, int n_words, void* stream);
+
 /* ---- per-kernel device timing (measurement aid) ---------------------------
  * While enabled (process-wide), every launch of the library's NTT-pass,
  * fused-NTT and base-conversion kernels is bracketed by two CUDA events

@@ -73,6 +73,11 @@ SIGNATURES = {
     "tfhe_ctx_transform_plan": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int),
                                                ctypes.POINTER(ctypes.c_int),
                                                ctypes.POINTER(ctypes.c_int)]),
+    "tfhe_crt_decompose": (ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int64, _i32p,
+                                          ctypes.c_int, _vp, _vp]),
+    "tfhe_crt_words": (ctypes.c_int, [_vp, _i32p, ctypes.c_int]),
+    "tfhe_crt_compose": (ctypes.c_int, [_vp, _vp, _i32p, ctypes.c_int, ctypes.c_int64, _vp, _vp,
+                                        ctypes.c_int, _vp]),
     "tfhe_profile_enable": (ctypes.c_int, [ctypes.c_int]),
     "tfhe_profile_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t]),
 }

@@ -2,13 +2,16 @@
 generation, encoding / decoding and encryption / decryption.
 
 These run BEFORE and AFTER the evaluated path (the
-lowest-priority row): the random draws, the canonical-embedding FFT and the
-CRT (de)composition of big integers are host work exactly as in the
-reference -- same `numpy.random.default_rng(seed)` stream, drawn in the same
-order with the same calls -- so a given seed yields the reference's keys and
-ciphertexts bit for bit; every transform and element-wise product on the way
-(`to_ntt`, `hada_mult`, `ele_add/sub`, automorphisms of the secret) runs on
-the device path.
+lowest-priority row).  The random draws and the canonical-embedding FFT stay
+host numpy exactly as in the reference -- same `numpy.random.default_rng(seed)`
+stream, drawn in the same order with the same calls, same float64 FFT -- so a
+given seed yields the reference's keys and ciphertexts bit for bit.  The
+integer work runs on the device: rounding and CRT decomposition of the
+encoded / sampled coefficients (`DeviceContext.crt_decompose`, exact for any
+float64 magnitude), the CRT composition + centring + float conversion of
+decode (`DeviceContext.crt_compose`, correctly rounded like Python's
+float(int)), and every transform and element-wise product on the way
+(`to_ntt`, `hada_mult`, `ele_add/sub`, automorphisms of the secret).
 
 `ClientMixin` is mixed into `CkksContext`, so the context offers the
 reference's full API (`keygen`, `make_relin_key`, `make_rotation_key`,
@@ -21,10 +24,11 @@ from __future__ import annotations
 from fractions import Fraction
 
 import numpy as np
+import torch
 
 from . import kernels
 from .errors import ParameterError
-from .rns import crt_compose, crt_decompose
+from .rns import crt_compose
 
 SIGMA = 3.2          # ref ckks.py:23
 NOISE_BOUND = 19     # ~6 sigma truncation (ref ckks.py:24)
@@ -55,8 +59,22 @@ class ClientMixin:
             rows[i] = self.rng.integers(0, q, self.params.n, dtype=np.uint64)
         return RnsPolynomial(rows=rows, basis=tuple(basis), domain=NTT)
 
+    def _device_rows(self, coeffs, basis):
+        """Signed coefficients (int64 or float64 host array) -> COEFF-domain
+        residue rows over `basis`, decomposed on the device (rns.py:77-90;
+        float64 is rounded half to even first, as np.rint)."""
+        from .rns import COEFF, RnsPolynomial
+        t = torch.from_numpy(np.ascontiguousarray(coeffs)).to(self.dev.device)
+        return RnsPolynomial(rows=self.dev.crt_decompose(t, tuple(basis)), basis=tuple(basis),
+                             domain=COEFF)
+
     def _encode_signed(self, vals, basis):
-        return self.to_ntt(crt_decompose(vals, basis))
+        """Small signed integers (ternary / Gaussian samples) -> NTT-domain
+        residue rows (ref ckks.py:100-109: crt_decompose then to_ntt)."""
+        vals = np.asarray(vals)
+        if vals.dtype.kind not in "iu":
+            raise ParameterError("_encode_signed takes an integer array")
+        return self.to_ntt(self._device_rows(vals.astype(np.int64), basis)).to_host()
 
     # -- keys (ref ckks.py:113-170) -------------------------------------------------
     def keygen(self):
@@ -139,19 +157,33 @@ class ClientMixin:
         evals[cidx] = np.conj(z) * float(scale)
         zeta = np.exp(1j * np.pi / n)
         coeffs = np.real(np.fft.fft(evals) / n * zeta ** (-np.arange(n)))
-        ints = [int(c) for c in np.rint(coeffs)]
-        poly = self.to_ntt(crt_decompose(ints, p.q_basis(level)))
+        # ref: ints = [int(c) for c in np.rint(coeffs)] -> crt_decompose; the
+        # device rounds half to even and reduces every magnitude exactly
+        if not np.all(np.isfinite(coeffs)):
+            raise (ValueError if np.isnan(coeffs).any() else OverflowError)(
+                "cannot convert float NaN/infinity to integer")
+        poly = self.to_ntt(self._device_rows(coeffs, p.q_basis(level))).to_host()
         return Plaintext(poly=poly, scale=Fraction(scale), level=level)
 
     def decode(self, pt):
-        return self._decode_ints(self._centered(self.to_coeff(pt.poly)), pt.scale)
+        """Slot values of a plaintext (ref ckks.py:200-213): INTT, CRT
+        composition, centring and float conversion on the device, then the
+        inverse canonical embedding (host float64 FFT)."""
+        poly = self.to_coeff(pt.poly).to_device(self.dev.device)
+        vals = self.dev.crt_compose(poly.rows, poly.basis).cpu().numpy()
+        if not np.all(np.isfinite(vals)):   # Python's float(int) raises past the double range
+            raise OverflowError("int too large to convert to float")
+        return self._decode_floats(vals, pt.scale)
 
-    def _decode_ints(self, coeffs, scale):
+    def _decode_floats(self, vals, scale):
         n = self.params.n
         zeta = np.exp(1j * np.pi / n)
-        vals = np.array([float(c) for c in coeffs]) * zeta ** np.arange(n)
-        evals = n * np.fft.ifft(vals)
+        evals = n * np.fft.ifft(vals * zeta ** np.arange(n))
         return evals[self._rot_index()[0]] / float(scale)
+
+    def _decode_ints(self, coeffs, scale):
+        """Reference form (ckks.py:203-213) over Python ints (host helper)."""
+        return self._decode_floats(np.array([float(c) for c in coeffs]), scale)
 
     @staticmethod
     def _centered(poly):

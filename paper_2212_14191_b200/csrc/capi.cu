@@ -24,6 +24,8 @@ struct TfheCtx {
   // pinned host bounce slots [in 3 | out 3] for pageable host buffers
   uint8_t* h_bounce = nullptr;
   size_t h_bounce_chunk = 0;
+  // crt_compose constants per basis (device), built on first use
+  std::vector<std::pair<std::vector<int16_t>, std::pair<uint32_t*, int>>> crt_cache;
 };
 
 namespace tfhe {
@@ -624,6 +626,7 @@ int tfhe_ctx_create(int device, int log_n, const uint32_t* primes, const uint32_
 void tfhe_ctx_destroy(TfheCtx* h) {
   if (!h) return;
   Ctx& c = h->c;
+  for (auto& e : h->crt_cache) cudaFree(e.second.first);
   if (h->h_bounce) cudaFreeHost(h->h_bounce);
   if (h->h2d) {
     cudaStreamDestroy(h->h2d);
@@ -1309,6 +1312,85 @@ int tfhe_profile_read(char* buf, size_t len) {
     buf[n] = 0;
   }
   return (int)names.size();
+}
+
+}  // extern "C"
+
+// ============================================================ client-side CRT
+extern "C" {
+
+static int crt_rows(const TfheCtx* h, const int32_t* limb_prime, int n_limbs, tfhe::CrtRows& r) {
+  using namespace tfhe;
+  if (!h || !limb_prime || n_limbs < 1 || n_limbs > kMaxCrtRows) {
+    set_error("crt: 1..128 limbs over the context's primes");
+    return TFHE_EINVAL;
+  }
+  r.n = n_limbs;
+  for (int l = 0; l < n_limbs; ++l) {
+    if (limb_prime[l] < 0 || limb_prime[l] >= h->c.n_primes) {
+      set_error("crt: prime index out of range");
+      return TFHE_EINVAL;
+    }
+    r.prime[l] = (int16_t)limb_prime[l];
+  }
+  return 0;
+}
+
+int tfhe_crt_decompose(TfheCtx* h, const void* coeffs, int kind, int64_t n,
+                       const int32_t* limb_prime, int n_limbs, uint32_t* out, void* stream) {
+  using namespace tfhe;
+  CrtRows r;
+  int rc = crt_rows(h, limb_prime, n_limbs, r);
+  if (rc) return rc;
+  if (kind != 0 && kind != 1) {
+    set_error("crt_decompose: kind must be 0 (int64) or 1 (float64, rint)");
+    return TFHE_EINVAL;
+  }
+  if (n < 0 || (n > 0 && (!coeffs || !out))) {
+    set_error("crt_decompose: bad buffers");
+    return TFHE_EINVAL;
+  }
+  return launch_crt_decompose(h->c, coeffs, kind, n, r, out, (cudaStream_t)stream);
+}
+
+int tfhe_crt_words(const TfheCtx* h, const int32_t* limb_prime, int n_limbs) {
+  using namespace tfhe;
+  CrtRows r;
+  int rc = crt_rows(h, limb_prime, n_limbs, r);
+  if (rc) return -rc;
+  return crt_compose_words(h->c, r.prime, r.n);
+}
+
+int tfhe_crt_compose(TfheCtx* h, const uint32_t* rows, const int32_t* limb_prime, int n_limbs,
+                     int64_t n, double* out_f64, uint32_t* out_words, int n_words, void* stream) {
+  using namespace tfhe;
+  CrtRows r;
+  int rc = crt_rows(h, limb_prime, n_limbs, r);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && !rows) || (out_words && n_words < 1)) {
+    set_error("crt_compose: bad buffers");
+    return TFHE_EINVAL;
+  }
+  std::vector<int16_t> key(r.prime, r.prime + r.n);
+  uint32_t* d_cst = nullptr;
+  int W = 0;
+  for (auto& e : h->crt_cache)
+    if (e.first == key) {
+      d_cst = e.second.first;
+      W = e.second.second;
+    }
+  if (!d_cst) {
+    std::vector<uint32_t> cst;
+    W = crt_compose_constants(h->c, r.prime, r.n, cst);
+    if (cudaMalloc(&d_cst, cst.size() * 4) != cudaSuccess ||
+        cudaMemcpy(d_cst, cst.data(), cst.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+      set_error("crt_compose: constant upload failed");
+      return TFHE_ECUDA;
+    }
+    h->crt_cache.push_back({key, {d_cst, W}});
+  }
+  return launch_crt_compose(h->c, rows, n, d_cst, W, r, out_f64, out_words,
+                            out_words ? n_words : 0, (cudaStream_t)stream);
 }
 
 }  // extern "C"

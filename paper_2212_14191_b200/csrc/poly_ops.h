@@ -1,6 +1,7 @@
 // Launchers for the HBM-bound polynomial kernels (poly_ops.cu) and the base
 // conversion (bconv_tc.cu: int8 tensor cores, element-wise for tiny shapes).
 #pragma once
+#include <vector>
 #include "tfhe_internal.h"
 
 namespace tfhe {
@@ -38,6 +39,21 @@ int launch_ks_mac_rot(const Ctx& c, const uint32_t* x, const uint32_t* base, con
                       int rows, int batch, uint32_t t, int perm_x, cudaStream_t st);
 int launch_automorph(const Ctx& c, const uint32_t* in, uint32_t* out, uint32_t t, int ntt_domain,
                      const int16_t* row_prime, int rows, int batch, cudaStream_t st);
+// CRT (de)composition rows: prime index per residue row (csrc/crt.cu)
+constexpr int kMaxCrtRows = 128;
+struct CrtRows {
+  int n;
+  int16_t prime[kMaxCrtRows];
+};
+// kind 0: int64 coefficients; kind 1: float64, rounded half to even (np.rint)
+int launch_crt_decompose(const Ctx& c, const void* in, int kind, int64_t n, const CrtRows& rows,
+                         uint32_t* out, cudaStream_t st);
+// constants for crt_compose (host): returns W = words of Q
+int crt_compose_constants(const Ctx& c, const int16_t* prime_ids, int L, std::vector<uint32_t>& out);
+int crt_compose_words(const Ctx& c, const int16_t* prime_ids, int L);
+int launch_crt_compose(const Ctx& c, const uint32_t* rows, int64_t n, const uint32_t* d_cst, int W,
+                       const CrtRows& lr, double* out_f, uint32_t* out_w, int n_words,
+                       cudaStream_t st);
 // exact_copies = false: rows of targets that are source primes may be left
 // with don't-care values (callers that never read them)
 int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,

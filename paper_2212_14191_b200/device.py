@@ -254,6 +254,42 @@ class DeviceContext:
             "tfhe_bconv")
         return out
 
+    def crt_decompose(self, coeffs, basis, out=None):
+        """Signed coefficients (device int64, or float64 rounded half to even
+        like np.rint) -> canonical residue rows (len(basis), n) (ref
+        rns.py:77-90 crt_decompose)."""
+        n = coeffs.numel()
+        if coeffs.dtype == torch.int64:
+            kind = 0
+        elif coeffs.dtype == torch.float64:
+            kind = 1
+        else:
+            raise ParameterError("crt_decompose takes int64 or float64 coefficients")
+        if out is None:
+            out = torch.empty((len(basis), n), dtype=torch.int32, device=self.device)
+        _lib.check(self.lib.tfhe_crt_decompose(
+            self.handle, _ptr(coeffs), kind, n, _lib.i32_array(self.prime_ids(basis)), len(basis),
+            _ptr(out), _stream(self.device)), "tfhe_crt_decompose")
+        return out
+
+    def crt_compose(self, rows, basis, words=False):
+        """Residue rows (len(basis), n) -> the CRT representative centred in
+        (-Q/2, Q/2] (ref rns.py:93-115 + ckks._centered) as correctly rounded
+        float64, and with words=True also as (n_words, n) two's-complement
+        32-bit words."""
+        n = rows.shape[-1]
+        ids = _lib.i32_array(self.prime_ids(basis))
+        out_f = torch.empty(n, dtype=torch.float64, device=self.device)
+        w = None
+        n_words = 0
+        if words:
+            n_words = self.lib.tfhe_crt_words(self.handle, ids, len(basis)) + 1
+            w = torch.empty((n_words, n), dtype=torch.int32, device=self.device)
+        _lib.check(self.lib.tfhe_crt_compose(
+            self.handle, _ptr(rows), ids, len(basis), n, _ptr(out_f), _ptr(w), n_words,
+            _stream(self.device)), "tfhe_crt_compose")
+        return (out_f, w) if words else out_f
+
     def ckks_workspace(self, level, batch):
         return self.workspace(self.lib.tfhe_ckks_workspace_bytes(self.handle, level, batch))
 

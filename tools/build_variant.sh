@@ -9,7 +9,7 @@ mkdir -p $obj
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3,-fopenmp --expt-relaxed-constexpr -ccbin /usr/bin/g++"
 pids=()
-for s in capi ntt_tc ntt_ts ntt_fused ntt_p3 poly_ops bconv_tc; do
+for s in capi ntt_tc ntt_ts ntt_fused ntt_p3 poly_ops bconv_tc crt; do
   nvcc $FL "$@" -c -o $obj/$s.o $s.cu & pids+=($!)
 done
 for p in "${pids[@]}"; do wait $p; done
