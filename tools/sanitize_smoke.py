@@ -60,6 +60,53 @@ def main():
                            p.alpha, p.dnum)
         assert np.array_equal(got[0][:, 0], rb) and np.array_equal(got[1][:, 0], ra)
         print("ckks ok", preset, flush=True)
+    # N = 2^16 three-factor passes (column + row) and the grouped key switch
+    # (column pass + EPI_KS_ACC row pass) on a 4-limb chain at level 3
+    n = 1 << 16
+    qs = generate_primes(n, [29, 30, 31])
+    ctx = DeviceContext.get(n, tuple(qs))
+    x = O.uniform_rows(rng, qs, (1, n))
+    f = ctx.ntt(dev(x), qs)
+    assert np.array_equal(host(f), O.ntt(x, qs))
+    assert np.array_equal(host(ctx.ntt(f, qs, inverse=True)), x)
+    print("ntt p3 ok", flush=True)
+    from paper_2212_14191_b200.params import generate_chain_widths
+    p = CkksParams(n=n, l_max=3, k=1, dnum=4, chain=generate_chain_widths(n, [29] * 4, [30]))
+    if True:
+        ck = CkksContext(p)
+        level = p.l_max
+        basis = tuple(p.chain.q[:level + 1])
+        ext = tuple(p.chain.q) + tuple(p.chain.p)
+        c0 = np.stack([O.uniform_rows(rng, basis, (1, p.n)) for _ in range(2)])
+        c1 = np.stack([O.uniform_rows(rng, basis, (1, p.n)) for _ in range(2)])
+        key = np.stack([np.stack([O.uniform_rows(rng, ext, (p.n,)) for _ in range(2)])
+                        for _ in range(p.dnum)])
+        got = host(ck.hmult_rescale_batch(CiphertextBatch(dev(c0), level),
+                                          CiphertextBatch(dev(c1), level), dev(key)).data)
+        hb, ha = O.hmult(c0[0][:, 0], c0[1][:, 0], c1[0][:, 0], c1[1][:, 0], basis, key,
+                         p.chain.q, p.chain.p, p.alpha, p.dnum)
+        rb, ra = O.rescale(hb, ha, basis)
+        assert np.array_equal(got[0][:, 0], rb) and np.array_equal(got[1][:, 0], ra)
+        print("ckks p3 ok", flush=True)
+    # tensor-core base conversion (chunk pairs, TMA tensor stores), incl. a
+    # non-canonical copy source (fixup launch)
+    n = 1 << 12
+    primes = generate_primes(n, [30] * 10 + [29] * 50)[:9 + 45]
+    src, dst = primes[:9], primes[9:] + primes[:9]
+    ctx = DeviceContext.get(n, tuple(primes))
+    x = O.uniform_rows(rng, src, (2, n))
+    x[3, 1, 7] = 0xFFFFFFF0
+    got = host(ctx.bconv(dev(x), src, dst))
+    assert np.array_equal(got, O.fast_basis_conv(x, tuple(src), tuple(dst)))
+    print("bconv ok", flush=True)
+    # client-side CRT
+    c = rng.normal(0, 2.0 ** 50, n)
+    rows = host(ctx.crt_decompose(torch.from_numpy(c).cuda(), primes[:5]))
+    assert np.array_equal(rows, np.array([[int(v) % q for v in np.rint(c)] for q in primes[:5]],
+                                         dtype=np.uint32))
+    fl = ctx.crt_compose(dev(rows), primes[:5]).cpu().numpy()
+    assert np.array_equal(fl, np.rint(c))
+    print("crt ok", flush=True)
     torch.cuda.synchronize()
     print("SANITIZE_SMOKE_OK")
 
