@@ -484,7 +484,8 @@ __global__ void __launch_bounds__(kPThreads, 1) ntt_col_kernel(const __grid_cons
         const int i2 = 8 * pos.cb + 4 * tile + q;
         const uint32_t* bt = sH + kHBeta + i2 * 32;
         const uint32_t* bts = sH + kHBetaS + i2 * 32;
-        uint32_t* o = a.P + (((size_t)pos.limb * a.batch + pos.b) * kPn2 + i2) * kPn1 + lane;
+        uint32_t* o = a.P + (((size_t)a.map.out_row[pos.limb] * a.batch + pos.b) * kPn2 + i2) * kPn1 +
+                      lane;
 #pragma unroll
         for (int b4 = 0; b4 < 8; ++b4) {
           // lazy Shoup products: P^T in [0, 2q) (the row pass only byte-splits it)
@@ -1295,9 +1296,20 @@ int launch_ntt_p3_ks_group(const Ctx& c, const uint32_t* in, void* ws, const Lim
     set_error("key-switch group: stage-1 map must hold S * T limbs");
     return 2;
   }
-  LimbMap m1 = s1map;   // P^T row l = s * T + t
-  for (int l = 0; l < m1.n; ++l) m1.out_row[l] = (int16_t)l;
-  int rc = launch_p3_col(c, in, static_cast<uint32_t*>(ws), m1, batch, 0, st);
+  // P^T row l = s * T + t; a slice's own target rows are reused unchanged
+  // (ckks.py:361-364) and their sums skipped by the row pass, so the column
+  // pass leaves those P^T rows unwritten (don't-care)
+  LimbMap m1;
+  m1.n = 0;
+  for (int l = 0; l < s1map.n; ++l) {
+    const int sl = l / tmap.n, t = l % tmap.n;
+    if (epi.j0 + sl == epi.js[t]) continue;
+    m1.prime[m1.n] = s1map.prime[l];
+    m1.in_row[m1.n] = s1map.in_row[l];
+    m1.out_row[m1.n] = (int16_t)l;
+    ++m1.n;
+  }
+  int rc = m1.n ? launch_p3_col(c, in, static_cast<uint32_t*>(ws), m1, batch, 0, st) : 0;
   if (rc) return rc;
   EpiArgs e = epi;
   e.mode = EPI_KS_ACC;
