@@ -46,6 +46,8 @@
 // 32) take an element-wise fast path (bconv_small_kernel) instead of
 // mostly-padding MMA tiles.  Timeline probes: -DTFHE_BC_TRACE.
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -605,18 +607,31 @@ int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArg
     for (int t = 0; t < ba.n_dst; ++t)
       if (ba.copy_from[t] >= 0) a.copy_src_mask |= 1u << ba.copy_from[t];
     if (a.copy_src_mask) {
+      // one flag word per launch from a per-device ring, tagged with a
+      // process-wide launch generation: concurrent launches (other streams or
+      // threads) never share a word unless kFlagSlots are in flight at once
+      constexpr int kFlagSlots = 1024;
+      static std::mutex mu;
       static uint32_t* flags[64] = {nullptr};
-      static uint32_t gen = 0;
-      uint32_t*& f = flags[c.dev & 63];
-      if (!f) {
-        if (cudaMalloc(&f, 4) != cudaSuccess || cudaMemset(f, 0, 4) != cudaSuccess) {
-          set_error("bconv copy flag allocation failed");
-          return 3;
+      static std::atomic<uint32_t> gen{0};
+      uint32_t* f;
+      {
+        std::lock_guard<std::mutex> g(mu);
+        uint32_t*& slot = flags[c.dev & 63];
+        if (!slot) {
+          if (cudaMalloc(&slot, kFlagSlots * 4) != cudaSuccess ||
+              cudaMemset(slot, 0, kFlagSlots * 4) != cudaSuccess) {
+            slot = nullptr;
+            set_error("bconv copy flag allocation failed");
+            return 3;
+          }
         }
+        f = slot;
       }
-      if (++gen == 0) ++gen;
-      a.copy_flag = f;
-      a.copy_gen = gen;
+      uint32_t gg = ++gen;
+      if (gg == 0) gg = ++gen;
+      a.copy_flag = f + gg % kFlagSlots;
+      a.copy_gen = gg;
     }
   }
   const int smem = kMaxPairs * kMaxKC * kBTileBC + kAStages * kMaxKC * kATileBC +

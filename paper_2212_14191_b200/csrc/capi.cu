@@ -26,6 +26,7 @@ struct TfheCtx {
   size_t h_bounce_chunk = 0;
   // crt_compose constants per basis (device), built on first use
   std::vector<std::pair<std::vector<int16_t>, std::pair<uint32_t*, int>>> crt_cache;
+  std::mutex crt_mu;
 };
 
 namespace tfhe {
@@ -1374,6 +1375,7 @@ int tfhe_crt_compose(TfheCtx* h, const uint32_t* rows, const int32_t* limb_prime
   std::vector<int16_t> key(r.prime, r.prime + r.n);
   uint32_t* d_cst = nullptr;
   int W = 0;
+  std::lock_guard<std::mutex> guard(h->crt_mu);
   for (auto& e : h->crt_cache)
     if (e.first == key) {
       d_cst = e.second.first;
