@@ -134,3 +134,28 @@ def test_batched_apply_eltwise_and_frobenius_vs_oracle(n, batch):
             t = O.galois_element(r, n)
             got = batched_apply(bx, "forbenius_map", aux=r, table=table)
             assert np.array_equal(back(got.data), O.apply_automorphism(x, t, primes)), (kind, r)
+
+
+def test_kernel_timer_counts_ntt_pass_launches():
+    """tfhe_profile_enable/read (the bench's per-kernel timing): one N=2^16
+    forward + inverse call = one column-pass and one row-pass launch each,
+    with positive device times; disabled afterwards (no records)."""
+    import torch
+    from paper_2212_14191_b200 import _lib
+    from paper_2212_14191_b200.device import DeviceContext
+    from paper_2212_14191_b200.params import generate_primes
+    n = 1 << 16
+    qs = generate_primes(n, [29, 30])
+    ctx = DeviceContext.get(n, tuple(qs))
+    x = torch.randint(0, 1 << 28, (2, 3, n), dtype=torch.int32, device="cuda")
+    with _lib.kernel_timer() as kt:
+        f = ctx.ntt(x, qs)
+        ctx.ntt(f, qs, inverse=True)
+        torch.cuda.synchronize()
+    got = {k: v for k, v in kt.times.items()}
+    assert got["ntt_col_kernel<fwd>"][0] == 1 and got["ntt_col_kernel<inv>"][0] == 1, got
+    assert got["ntt_row_kernel<store>"][0] == 2, got
+    assert all(ms > 0 for _, ms in got.values()), got
+    with _lib.kernel_timer() as kt2:
+        pass
+    assert kt2.times == {}
