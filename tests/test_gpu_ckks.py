@@ -31,7 +31,7 @@ LARGE = [("n16_l3", "n16", 3, 21), ("resnet20_l3", "resnet20", 3, 22),
 # cases rerun with the key-switch group size capped (TFHE_KS_MAX_S), so the
 # multi-group path (accumulator re-read between groups) meets every shape
 MULTIGROUP = [c for c in LARGE if c[0] in ("n16_l3", "resnet20_l3", "set_c_full", "set_c_l4",
-                                           "p_dnum5_l12", "n14_31b_l5")]
+                                           "p_dnum5_l12", "n14_31b_l5", "n16_31b_l3")]
 
 
 def _params(kind):
