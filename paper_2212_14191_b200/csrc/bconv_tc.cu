@@ -461,46 +461,63 @@ __global__ void __launch_bounds__(kThreadsBC, 1)
 // few targets), where a 128-row MMA tile would carry mostly padding: each
 // thread converts 4 coefficients (uint4) for every target -- the alpha
 // products of one target (< 4 * 2^62) are summed in 64 bits and reduced once.
+template <int NS>
 __global__ void __launch_bounds__(256)
     bconv_small_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                        const PrimeConst* __restrict__ pcs, const __grid_constant__ BconvArgs ba,
-                       int64_t per_row) {
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
-       i += (int64_t)gridDim.x * blockDim.x * 4) {
-    uint32_t a[4][4], y[4][4];
+                       int64_t per_row, int64_t in_cstride, int64_t out_cstride) {
+  in += blockIdx.y * in_cstride;     // component (blockIdx.y) of a multi-component launch
+  out += blockIdx.y * out_cstride;
+  // NS sources (compile time): all source loads of two 4-coefficient groups
+  // are issued before any arithmetic (memory-level parallelism)
+  const int64_t step = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i0 < per_row;
+       i0 += 2 * step) {
+    uint4 v[2][NS];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      if (s >= ba.n_src) break;
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(in + (int64_t)s * per_row + i));
-      a[s][0] = v.x; a[s][1] = v.y; a[s][2] = v.z; a[s][3] = v.w;
-      const uint32_t q = pcs[ba.src_prime[s]].q;
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) y[s][e] = mul_shoup(a[s][e], ba.qhat_inv[s], ba.qhat_inv_shoup[s], q);
-    }
-    for (int t = 0; t < ba.n_dst; ++t) {
-      uint32_t r[4];
-      const int cp = ba.copy_from[t];
-      if (cp >= 0) {
+      for (int s = 0; s < NS; ++s)
+        v[h][s] = i0 + h * step < per_row
+                      ? __ldg(reinterpret_cast<const uint4*>(in + (int64_t)s * per_row + i0 + h * step))
+                      : make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int s = 0; s < 4; ++s)
-          if (s == cp) {
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = i0 + h * step;
+      if (i >= per_row) break;
+      uint32_t a[NS][4], y[NS][4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) r[e] = a[s][e];
-          }
-      } else {
-        const PrimeConst pt = pcs[ba.dst_prime[t]];
-        uint64_t acc[4] = {0, 0, 0, 0};
+      for (int s = 0; s < NS; ++s) {
+        a[s][0] = v[h][s].x; a[s][1] = v[h][s].y; a[s][2] = v[h][s].z; a[s][3] = v[h][s].w;
+        const uint32_t q = pcs[ba.src_prime[s]].q;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          if (s >= ba.n_src) break;
-          const uint64_t f = ba.factor[s * kMaxBconvDst + t];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[e] += (uint64_t)y[s][e] * f;
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) r[e] = reduce64(acc[e], pt.q, pt.mu);
+        for (int e = 0; e < 4; ++e)
+          y[s][e] = mul_shoup(a[s][e], ba.qhat_inv[s], ba.qhat_inv_shoup[s], q);
       }
-      *reinterpret_cast<uint4*>(out + (int64_t)t * per_row + i) = make_uint4(r[0], r[1], r[2], r[3]);
+      for (int t = 0; t < ba.n_dst; ++t) {
+        uint32_t r[4];
+        const int cp = ba.copy_from[t];
+        if (cp >= 0) {
+#pragma unroll
+          for (int s = 0; s < NS; ++s)
+            if (s == cp) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) r[e] = a[s][e];
+            }
+        } else {
+          const PrimeConst pt = pcs[ba.dst_prime[t]];
+          uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const uint64_t f = ba.factor[s * kMaxBconvDst + t];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[e] += (uint64_t)y[s][e] * f;
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) r[e] = reduce64(acc[e], pt.q, pt.mu);
+        }
+        *reinterpret_cast<uint4*>(out + (int64_t)t * per_row + i) = make_uint4(r[0], r[1], r[2], r[3]);
+      }
     }
   }
 }
@@ -525,21 +542,37 @@ __global__ void __launch_bounds__(256)
 }  // namespace
 
 int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,
-                 cudaStream_t st, bool exact_copies) {
+                 cudaStream_t st, bool exact_copies, int n_comp, int64_t in_cstride,
+                 int64_t out_cstride) {
   if (ba.n_dst <= 0) return 0;
-  if (ba.n_src < 1 || ba.n_src > 4 * kMaxKC * 2 || ba.n_dst > kMaxBconvDst) {
+  if (ba.n_src < 1 || ba.n_src > 4 * kMaxKC * 2 || ba.n_dst > kMaxBconvDst || n_comp < 1) {
     set_error("base conversion: 1..16 sources and at most 128 targets");
     return 2;
   }
   if (ba.n_src <= 4 && ba.n_src * ba.n_dst <= 32 && (batch * (int64_t)c.n) % 4 == 0) {
+    // element-wise path: every component in one launch (blockIdx.y)
     const int64_t per_row = (int64_t)batch * c.n;
-    const int64_t blocks = std::min<int64_t>((per_row / 4 + 255) / 256, (int64_t)c.sms * 8);
-    bconv_small_kernel<<<(int)std::max<int64_t>(blocks, 1), 256, 0, st>>>(in, out, c.d_pc, ba,
-                                                                        per_row);
+    const int64_t blocks =
+        std::min<int64_t>((per_row / 4 + 255) / 256, (int64_t)c.sms * 8 / n_comp);
+    const dim3 grid((unsigned)std::max<int64_t>(blocks, 1), n_comp);
+    switch (ba.n_src) {
+      case 1: bconv_small_kernel<1><<<grid, 256, 0, st>>>(in, out, c.d_pc, ba, per_row, in_cstride, out_cstride); break;
+      case 2: bconv_small_kernel<2><<<grid, 256, 0, st>>>(in, out, c.d_pc, ba, per_row, in_cstride, out_cstride); break;
+      case 3: bconv_small_kernel<3><<<grid, 256, 0, st>>>(in, out, c.d_pc, ba, per_row, in_cstride, out_cstride); break;
+      default: bconv_small_kernel<4><<<grid, 256, 0, st>>>(in, out, c.d_pc, ba, per_row, in_cstride, out_cstride); break;
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       set_error(std::string("bconv_small launch: ") + cudaGetErrorString(e));
       return 3;
+    }
+    return 0;
+  }
+  if (n_comp > 1) {
+    for (int k = 0; k < n_comp; ++k) {
+      const int rc = launch_bconv(c, in + k * in_cstride, out + k * out_cstride, ba, batch, st,
+                                  exact_copies);
+      if (rc) return rc;
     }
     return 0;
   }

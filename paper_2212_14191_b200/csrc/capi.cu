@@ -495,10 +495,10 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
     for (int t = 0; t < g.nr; ++t) dst.push_back(g.r0 + t);
     BconvArgs ba;
     if ((rc = fill_bconv(c, src, dst, ba))) return rc;
-    for (int cmp = 0; cmp < 2; ++cmp)
-      if ((rc = launch_bconv(c, ysp + (size_t)cmp * g.K * U, conv + (size_t)cmp * g.nr * U, ba,
-                             batch, st)))
-        return rc;
+    // both components in one call (one launch on the element-wise path)
+    if ((rc = launch_bconv(c, ysp, conv, ba, batch, st, true, 2, (int64_t)g.K * U,
+                           (int64_t)g.nr * U)))
+      return rc;
     md_in = conv;
   }
   if (rs_scratch) return moddown_rescale(c, g, acc, md_in, conv, y, rs_scratch, base, base_rows,

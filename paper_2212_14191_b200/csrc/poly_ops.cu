@@ -43,14 +43,28 @@ __global__ void binary_kernel(const uint32_t* __restrict__ a, const uint32_t* __
   const int row = blockIdx.y;
   const PrimeConst pc = pcs[rp.prime[row]];
   const int64_t base = (int64_t)row * per_row;
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
-       i += (int64_t)gridDim.x * blockDim.x * 4) {
-    uint4 x = ld4(a + base + i), y = ld4(b + base + i), r;
-    r.x = binop<OP>(x.x, y.x, pc);
-    r.y = binop<OP>(x.y, y.y, pc);
-    r.z = binop<OP>(x.z, y.z, pc);
-    r.w = binop<OP>(x.w, y.w, pc);
-    st4(out + base + i, r);
+  // two 4-element groups per iteration, loads first (memory-level parallelism)
+  const int64_t step = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i0 < per_row;
+       i0 += 2 * step) {
+    uint4 x[2], y[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = i0 + h * step < per_row ? i0 + h * step : i0;
+      x[h] = ld4(a + base + i);
+      y[h] = ld4(b + base + i);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = i0 + h * step;
+      if (i >= per_row) break;
+      uint4 r;
+      r.x = binop<OP>(x[h].x, y[h].x, pc);
+      r.y = binop<OP>(x[h].y, y[h].y, pc);
+      r.z = binop<OP>(x[h].z, y[h].z, pc);
+      r.w = binop<OP>(x[h].w, y[h].w, pc);
+      st4(out + base + i, r);
+    }
   }
 }
 
@@ -95,21 +109,35 @@ __global__ void tensor_kernel(const uint32_t* __restrict__ b0, const uint32_t* _
   const int row = blockIdx.y;
   const PrimeConst pc = pcs[rp.prime[row]];
   const int64_t base = (int64_t)row * per_row;
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
-       i += (int64_t)gridDim.x * blockDim.x * 4) {
-    const int64_t o = base + i;
-    uint4 xb0 = ld4(b0 + o), xa0 = ld4(a0 + o), xb1 = ld4(b1 + o), xa1 = ld4(a1 + o);
-    uint4 r0, r1, r2;
-    // d1's two products (< 2^62 each) are summed before one reduction
-#define TFHE_TP(c)                                                                  \
-  r0.c = mul_mod(xb0.c, xb1.c, pc.q, pc.mu);                                        \
-  r1.c = reduce64((uint64_t)xa0.c * xb1.c + (uint64_t)xa1.c * xb0.c, pc.q, pc.mu);  \
-  r2.c = mul_mod(xa0.c, xa1.c, pc.q, pc.mu);
-    TFHE_TP(x) TFHE_TP(y) TFHE_TP(z) TFHE_TP(w)
+  // two 4-element groups per iteration, loads first (memory-level parallelism)
+  const int64_t step = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i0 < per_row;
+       i0 += 2 * step) {
+    uint4 xb0[2], xa0[2], xb1[2], xa1[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t o = base + (i0 + h * step < per_row ? i0 + h * step : i0);
+      xb0[h] = ld4(b0 + o);
+      xa0[h] = ld4(a0 + o);
+      xb1[h] = ld4(b1 + o);
+      xa1[h] = ld4(a1 + o);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (i0 + h * step >= per_row) break;
+      const int64_t o = base + i0 + h * step;
+      uint4 r0, r1, r2;
+      // d1's two products (< 2^62 each) are summed before one reduction
+#define TFHE_TP(c)                                                                          \
+  r0.c = mul_mod(xb0[h].c, xb1[h].c, pc.q, pc.mu);                                          \
+  r1.c = reduce64((uint64_t)xa0[h].c * xb1[h].c + (uint64_t)xa1[h].c * xb0[h].c, pc.q, pc.mu); \
+  r2.c = mul_mod(xa0[h].c, xa1[h].c, pc.q, pc.mu);
+      TFHE_TP(x) TFHE_TP(y) TFHE_TP(z) TFHE_TP(w)
 #undef TFHE_TP
-    st4(d0 + o, r0);
-    st4(d1 + o, r1);
-    st4(d2 + o, r2);
+      st4(d0 + o, r0);
+      st4(d1 + o, r1);
+      st4(d2 + o, r2);
+    }
   }
 }
 
@@ -131,20 +159,37 @@ __global__ void ks_mac_kernel(const uint32_t* __restrict__ x, const uint32_t* __
   const int64_t base = (int64_t)row * per_row;
   const uint32_t* kbr = kb + ma.key_off[row];
   const uint32_t* kar = ka + ma.key_off[row];
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < per_row;
-       i += (int64_t)gridDim.x * blockDim.x * 4) {
-    const int64_t o = base + i;
-    const int coef = (int)(i % n);
-    uint4 v = ld4(x + o), wb = ld4(kbr + coef), wa = ld4(kar + coef);
-    uint4 ob = first ? make_uint4(0, 0, 0, 0) : ld4(acc_b + o);
-    uint4 oa = first ? make_uint4(0, 0, 0, 0) : ld4(acc_a + o);
-#define TFHE_MAC(c)                                                  \
-  ob.c = add_mod(ob.c, mul_mod(v.c, wb.c, pc.q, pc.mu), pc.q);       \
-  oa.c = add_mod(oa.c, mul_mod(v.c, wa.c, pc.q, pc.mu), pc.q);
-    TFHE_MAC(x) TFHE_MAC(y) TFHE_MAC(z) TFHE_MAC(w)
+  // two 4-coefficient groups per iteration, all loads issued before the
+  // arithmetic (memory-level parallelism)
+  const int64_t step = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i0 < per_row;
+       i0 += 2 * step) {
+    uint4 v[2], wb[2], wa[2], ob[2], oa[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = i0 + h * step;
+      const bool ok = i < per_row;
+      const int64_t o = base + (ok ? i : 0);
+      const int coef = (int)(i & (n - 1));   // n is a power of two
+      v[h] = ld4(x + o);
+      wb[h] = ld4(kbr + coef);
+      wa[h] = ld4(kar + coef);
+      ob[h] = first ? make_uint4(0, 0, 0, 0) : ld4(acc_b + o);
+      oa[h] = first ? make_uint4(0, 0, 0, 0) : ld4(acc_a + o);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = i0 + h * step;
+      if (i >= per_row) break;
+      const int64_t o = base + i;
+#define TFHE_MAC(c)                                                           \
+  ob[h].c = add_mod(ob[h].c, mul_mod(v[h].c, wb[h].c, pc.q, pc.mu), pc.q);    \
+  oa[h].c = add_mod(oa[h].c, mul_mod(v[h].c, wa[h].c, pc.q, pc.mu), pc.q);
+      TFHE_MAC(x) TFHE_MAC(y) TFHE_MAC(z) TFHE_MAC(w)
 #undef TFHE_MAC
-    st4(acc_b + o, ob);
-    st4(acc_a + o, oa);
+      st4(acc_b + o, ob[h]);
+      st4(acc_a + o, oa[h]);
+    }
   }
 }
 

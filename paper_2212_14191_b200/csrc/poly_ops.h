@@ -56,8 +56,12 @@ int launch_crt_compose(const Ctx& c, const uint32_t* rows, int64_t n, const uint
                        cudaStream_t st);
 // exact_copies = false: rows of targets that are source primes may be left
 // with don't-care values (callers that never read them)
+// n_comp > 1: that many independent conversions with the same bases, inputs /
+// outputs `in_cstride` / `out_cstride` elements apart (one launch when the
+// element-wise path applies)
 int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArgs& ba, int batch,
-                 cudaStream_t st, bool exact_copies = true);
+                 cudaStream_t st, bool exact_copies = true, int n_comp = 1,
+                 int64_t in_cstride = 0, int64_t out_cstride = 0);
 
 // Fused ModDown + rescale preparation, per row l = (component, chain row i < top):
 //   X = acc[acc_row] * P^-1 + base[base_row]     (in place; base_row < 0: none)
