@@ -83,7 +83,11 @@ constexpr int kC2T = 65536;
 // the two epilogue warpgroups (128 * 128 + 256 * 184 <= 384 * 168)
 constexpr int kRowRegsLow = 128, kRowRegsEpi = 184;
 constexpr int kC2A = 2 * kPTile;                 // K = 64: two K-steps of one M tile
-constexpr int kC2Smem = kC2T + kRawSlots * kPRaw + 2 * kC2A + 32 * 8;
+#ifndef TFHE_P3_ABUFS
+#define TFHE_P3_ABUFS 2
+#endif
+constexpr int kABufs = TFHE_P3_ABUFS;            // MMA operand buffers (1: room for a 3rd raw slot)
+constexpr int kC2Smem = kC2T + kRawSlots * kPRaw + kABufs * kC2A + 64 * 8;
 
 struct ColArgs {
   const uint8_t* tab;      // [prime] 16 KB: T (B operand, 4 planes x 128 rows x 32 K)
@@ -516,17 +520,17 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sT = smem;
   uint8_t* sRaw = smem + kC2T;                  // [kRawSlots] raw tiles (TMA ring)
-  uint8_t* sA = sRaw + kRawSlots * kPRaw;        // [2] buffers of two K-steps
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sA + 2 * kC2A);
-  uint64_t* raw_full = bar + 12;   // [kRawSlots]
-  uint64_t* raw_empty = bar + 14;  // [kRawSlots]
-  uint64_t* a_full = bar + 2;      // [2]
-  uint64_t* a_empty = bar + 4;     // [2]
+  uint8_t* sA = sRaw + kRawSlots * kPRaw;        // [kABufs] buffers of two K-steps
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sA + kABufs * kC2A);
+  uint64_t* a_full = bar + 2;      // [kABufs]
+  uint64_t* a_empty = bar + 4;     // [kABufs]
   uint64_t* acc_full = bar + 6;    // [2]
   uint64_t* acc_empty = bar + 8;   // [2]
   uint64_t* tw_full = bar + 10;
   uint64_t* tw_empty = bar + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* raw_full = bar + 12;              // [kRawSlots]
+  uint64_t* raw_empty = raw_full + kRawSlots;  // [kRawSlots]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + kRawSlots);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // a.units counts slice groups (S units each); whole groups per CTA, either a
@@ -544,8 +548,10 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
       mbar_init(&raw_empty[s], 32 * kPProdWarps);
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&a_full[s], 32 * kPProdWarps);
-      mbar_init(&a_empty[s], 1);
+      if (s < kABufs) {
+        mbar_init(&a_full[s], 32 * kPProdWarps);
+        mbar_init(&a_empty[s], 1);
+      }
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 256);
     }
@@ -627,9 +633,9 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
         if (prev_limb >= 0) tw_ph ^= 1;
         prev_limb = limb;
       }
-      const int buf = it & 1;
-      if (it >= 2) mbar_wait(&a_empty[buf], ((it >> 1) - 1) & 1);
-      uint8_t* dst = sA + buf * kC2A;
+      const int abuf = it % kABufs;
+      if (it >= kABufs) mbar_wait(&a_empty[abuf], ((it / kABufs) - 1) & 1);
+      uint8_t* dst = sA + abuf * kC2A;
 #pragma unroll
       for (int k = 0; k < kPItems; ++k) {
         const int item = warp + kPProdWarps * k;
@@ -643,7 +649,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
           *reinterpret_cast<uint32_t*>(dst + p_off(kk >> 5, j, m, kk & 31)) = w[j];
       }
       fence_proxy_async_smem();
-      mbar_arrive(&a_full[buf]);
+      mbar_arrive(&a_full[abuf]);
     }
   } else if (warp == kPMmaWarp) {
     if (MODE == EPI_KS_ACC) reg_dealloc<kRowRegsLow>();
@@ -659,12 +665,12 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
         mbar_wait(tw_full, tw_ph);
         prev_limb = pos.limb;
       }
-      const int buf = it & 1;
-      mbar_wait(&a_full[buf], (it >> 1) & 1);
+      const int buf = it & 1, abuf = it % kABufs;
+      mbar_wait(&a_full[abuf], (it / kABufs) & 1);
       if (it >= 2) mbar_wait(&acc_empty[buf], ((it >> 1) - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t ab = smem_u32(sA + buf * kC2A);
+        const uint32_t ab = smem_u32(sA + abuf * kC2A);
 #pragma unroll
         for (int kc = 0; kc < 2; ++kc)
 #pragma unroll
@@ -673,7 +679,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
             const uint64_t bd = smem_desc_kmajor(sT_u + (kc * 4 + j) * 8192, 4096, 128);
             mma_i8_ss(tmem + buf * 256, ad, bd, idesc, (kc | j) != 0);
           }
-        mma_commit(&a_empty[buf]);
+        mma_commit(&a_empty[abuf]);
         mma_commit(&acc_full[buf]);
         if (last_of_limb(pos, it)) mma_commit(tw_empty);
       }
