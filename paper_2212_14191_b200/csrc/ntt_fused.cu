@@ -446,6 +446,32 @@ __global__ void __launch_bounds__(kFThreads, 1) ntt_fused_kernel(const __grid_co
       const bool valid = bm < a.batch;
       const size_t cofs = (size_t)kC2 * h * kFn1;   // the warp's first column k2
       const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + bm) * kFN + k1 + cofs;
+      if ((MODE == EPI_KS_MAC && !a.epi.first) || MODE == EPI_SUB_SCALE) {
+        // the next unit's epilogue operand rows (accumulators / x and base,
+        // in HBM) -> L2 while this unit runs: the epilogue reads them column
+        // chunk by column chunk
+        UPos nx = pos;
+        adv(nx);
+        const int nbm = 2 * nx.pair + b;
+        if (it + 1 < cnt && nbm < a.batch) {
+          const uint32_t* p0_;
+          const uint32_t* p1_;
+          if (MODE == EPI_KS_MAC) {
+            const size_t nrow = ((size_t)a.map.out_row[nx.limb] * a.batch + nbm) * kFN + k1 + cofs;
+            p0_ = a.epi.acc_b + nrow;
+            p1_ = a.epi.acc_a + nrow;
+          } else {
+            p0_ = a.epi.x + ((size_t)a.epi.x_row[nx.limb] * a.batch + nbm) * kFN + k1 + cofs;
+            const int br = a.epi.base_row[nx.limb];
+            p1_ = br >= 0 ? a.epi.base + ((size_t)br * a.batch + nbm) * kFN + k1 + cofs : nullptr;
+          }
+#pragma unroll 4
+          for (int e = 0; e < kC2; ++e) {
+            prefetch_l2(p0_ + (size_t)e * kFn1);
+            if (p1_) prefetch_l2(p1_ + (size_t)e * kFn1);
+          }
+        }
+      }
       mbar_wait(acc2_full, it & 1);
       FTRACE(9, it);
       tc_fence_after();

@@ -839,6 +839,21 @@ __global__ void __launch_bounds__(kRowThreads, 1) ntt_row_kernel(const __grid_co
       const int k1 = 128 * pos.kb + 32 * q + lane;
       const size_t pos0 = (size_t)32 * h * kPn1 + k1;   // the warp's first output position
       const size_t orow = ((size_t)a.map.out_row[limb] * a.batch + pos.b) * kPN + pos0;
+      if (MODE == EPI_SUB_SCALE && it + 1 < cnt) {
+        // the next unit's x / base rows (HBM) -> L2 while this unit runs
+        UPos nx = pos;
+        adv(nx);
+        const size_t np0 = (size_t)32 * h * kPn1 + 128 * nx.kb + 32 * q + lane;
+        const uint32_t* nxs = a.epi.x + ((size_t)a.epi.x_row[nx.limb] * a.batch + nx.b) * kPN + np0;
+        const int nbr = a.epi.base_row[nx.limb];
+        const uint32_t* nbs =
+            nbr >= 0 ? a.epi.base + ((size_t)nbr * a.batch + nx.b) * kPN + np0 : nullptr;
+#pragma unroll 4
+        for (int e = 0; e < 32; ++e) {
+          prefetch_l2(nxs + (size_t)e * kPn1);
+          if (nbs) prefetch_l2(nbs + (size_t)e * kPn1);
+        }
+      }
       // EPI_KS_ACC: this slice's key rows (none for the slice's own target row);
       // the first 8 columns are requested before the accumulator wait and each
       // later chunk one chunk ahead, so the L2 latency overlaps the fold / MAC
