@@ -272,6 +272,15 @@ int moddown_rescale(const Ctx& c, const CkksGeom& g, uint32_t* acc, const uint32
 // is never materialised.  INTT(phi(a)) = phi_coeff(INTT(a)) is the INTT's own
 // output scatter, the slice rows' MAC gathers phi(a) and folds P phi(b) into
 // acc_b, so ModDown's (acc_b - y) P^-1 = phi(b) + ksb with no addend pass.
+// HMULT's tensor product launched by keyswitch_impl itself, so that it can
+// also write the slice-row MACs of d2 straight into the freshly carved
+// accumulator (TensorMac) instead of a separate ks_mac pass over d2
+struct TensorIn {
+  const uint32_t* ct0;
+  const uint32_t* ct1;
+  uint32_t* dd;   // d0 | d1 | d2, P elements each
+};
+
 struct RotHoist {
   uint32_t t;
   const uint32_t* b;
@@ -281,7 +290,8 @@ struct RotHoist {
 int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int level, int batch,
                    const uint32_t* key, int dnum, int r0, int nr, uint32_t* out,
                    const uint32_t* base, const int16_t* base_rows, Carve& cv, cudaStream_t st,
-                   uint32_t* rs_scratch = nullptr, const RotHoist* rot = nullptr) {
+                   uint32_t* rs_scratch = nullptr, const RotHoist* rot = nullptr,
+                   const TensorIn* tin = nullptr) {
   const Ctx& c = h->c;
   CkksGeom g = geom(h, level, dnum, r0, nr);
   set_group(g, c, batch);
@@ -307,6 +317,34 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
   if (rot && (!c.use_ts || y_full || rs_scratch || base || (!rot->d_is_phi && !c.use_p3))) {
     set_error("hoisted rotation: unsupported key-switch configuration");
     return TFHE_EINVAL;
+  }
+
+  // 0. (HMULT) the tensor product, with the slice-row MACs of d2 fused: every
+  //    row on the grouped path (they all start the accumulator), slice 0's
+  //    rows on the per-slice path (its MACs overwrite; later slices add)
+  int fused_rows = 0;
+  if (tin) {
+    if (r0 != 0 || g.nr != g.l1 || rot) {
+      set_error("fused tensor product needs the unpartitioned, unrotated key switch");
+      return TFHE_EINVAL;
+    }
+    TensorMac tm;
+    memset(&tm, 0, sizeof(tm));
+    tm.kb = key;
+    tm.ka = key + key_pair / 2;
+    tm.acc_b = acc;
+    tm.acc_a = acc + g.T * U;
+    tm.log_n = c.log_n;
+    fused_rows = c.use_ts ? g.nr : std::min(g.alpha, g.l1);
+    for (int r = 0; r < fused_rows; ++r)
+      tm.key_off[r] = (int64_t)(r / g.alpha) * key_pair + (int64_t)r * c.n;
+    tm.rows = fused_rows;
+    int16_t rp[kMaxRows];
+    for (int i = 0; i < g.l1; ++i) rp[i] = (int16_t)i;
+    const size_t P = (size_t)g.l1 * U;
+    if ((rc = launch_tensor(c, tin->ct0, tin->ct0 + P, tin->ct1, tin->ct1 + P, tin->dd,
+                            tin->dd + P, tin->dd + 2 * P, rp, g.l1, (int64_t)U, st, &tm)))
+      return rc;
   }
 
   // 1. y = INTT(d), every limb of the level  (ModUp's to_coeff, ckks.py:362)
@@ -351,7 +389,8 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
                                   row_prime, key_off, pmod, g.nr, batch, rot->t, !rot->d_is_phi,
                                   st)))
         return rc;
-    } else if ((rc = launch_ks_mac(c, d, key, key + key_pair / 2, acc, acc + g.T * U, row_prime,
+    } else if (fused_rows < g.nr &&
+               (rc = launch_ks_mac(c, d, key, key + key_pair / 2, acc, acc + g.T * U, row_prime,
                                    key_off, g.nr, batch, 1, st))) {
       return rc;
     }
@@ -464,7 +503,7 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
         return rc;
       // slice rows are reused unchanged (ckks.py:361-364): MAC the local ones straight from d
       const int a0 = std::max(lo, g.r0), a1 = std::min(hi, g.r0 + g.nr);
-      if (a1 > a0) {
+      if (a1 > a0 && !(j == 0 && fused_rows > 0)) {   // slice 0's rows: done by the tensor product
         int64_t key_off[kMaxRows];
         for (int r = a0; r < a1; ++r) key_off[r - a0] = (int64_t)r * c.n;
         const size_t t0 = (size_t)(a0 - g.r0);
@@ -813,15 +852,11 @@ int tfhe_hmult(TfheCtx* h, const uint32_t* ct0, const uint32_t* ct1, int level, 
     set_error("ckks workspace too small");
     return TFHE_EINVAL;
   }
-  int16_t rp[kMaxRows];
-  for (int i = 0; i < l1; ++i) rp[i] = (int16_t)i;
-  if ((rc = launch_tensor(h->c, ct0, ct0 + P, ct1, ct1 + P, dd, dd + P, dd + 2 * P, rp, l1,
-                          (int64_t)batch * h->c.n, st)))
-    return rc;
   int16_t rows[kMaxLimbs];
   for (int l = 0; l < 2 * l1; ++l) rows[l] = (int16_t)l;  // (d0, d1) added to (ksb, ksa)
+  const TensorIn tin{ct0, ct1, dd};   // the tensor product runs inside, MACs fused
   return keyswitch_impl(h, dd + 2 * P, nullptr, level, batch, rlk, dnum, 0, l1, out, dd, rows, cv,
-                        st);
+                        st, nullptr, nullptr, &tin);
 }
 
 int tfhe_hmult_rescale(TfheCtx* h, const uint32_t* ct0, const uint32_t* ct1, int level,
@@ -842,17 +877,13 @@ int tfhe_hmult_rescale(TfheCtx* h, const uint32_t* ct0, const uint32_t* ct1, int
     set_error("ckks workspace too small");
     return TFHE_EINVAL;
   }
-  int16_t rp[kMaxRows];
-  for (int i = 0; i < l1; ++i) rp[i] = (int16_t)i;
-  if ((rc = launch_tensor(h->c, ct0, ct0 + P, ct1, ct1 + P, dd, dd + P, dd + 2 * P, rp, l1,
-                          (int64_t)batch * h->c.n, st)))
-    return rc;
   int16_t rows[kMaxLimbs];
   for (int l = 0; l < 2 * l1; ++l) rows[l] = (int16_t)l;
   // d2 (the key-switch input) is dead after ModUp: its first rows hold the top
   // row's coefficient form for the fused rescale
+  const TensorIn tin{ct0, ct1, dd};   // the tensor product runs inside, MACs fused
   return keyswitch_impl(h, dd + 2 * P, nullptr, level, batch, rlk, dnum, 0, l1, out, dd, rows, cv,
-                        st, dd + 2 * P);
+                        st, dd + 2 * P, nullptr, &tin);
 }
 
 int tfhe_rescale(TfheCtx* h, const uint32_t* ct, int level, int batch, uint32_t* out, void* ws,

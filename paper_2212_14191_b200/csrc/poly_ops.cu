@@ -105,7 +105,8 @@ __global__ void tensor_kernel(const uint32_t* __restrict__ b0, const uint32_t* _
                               const uint32_t* __restrict__ b1, const uint32_t* __restrict__ a1,
                               uint32_t* __restrict__ d0, uint32_t* __restrict__ d1,
                               uint32_t* __restrict__ d2, const PrimeConst* __restrict__ pcs,
-                              const __grid_constant__ RowPrimes rp, int64_t per_row) {
+                              const __grid_constant__ RowPrimes rp, int64_t per_row,
+                              const __grid_constant__ TensorMac mac) {
   const int row = blockIdx.y;
   const PrimeConst pc = pcs[rp.prime[row]];
   const int64_t base = (int64_t)row * per_row;
@@ -137,6 +138,21 @@ __global__ void tensor_kernel(const uint32_t* __restrict__ b0, const uint32_t* _
       st4(d0 + o, r0);
       st4(d1 + o, r1);
       st4(d2 + o, r2);
+      if (row < mac.rows) {
+        // the key switch's slice-row MAC on d2 (ckks.py:361-364, keys broadcast
+        // over the batch): acc_b = d2 kb, acc_a = d2 ka, overwriting
+        const int coef = (int)((i0 + h * step) & ((1 << mac.log_n) - 1));
+        const uint4 wb = ld4(mac.kb + mac.key_off[row] + coef);
+        const uint4 wa = ld4(mac.ka + mac.key_off[row] + coef);
+        uint4 ob, oa;
+#define TFHE_TM(c)                          \
+  ob.c = mul_mod(r2.c, wb.c, pc.q, pc.mu);  \
+  oa.c = mul_mod(r2.c, wa.c, pc.q, pc.mu);
+        TFHE_TM(x) TFHE_TM(y) TFHE_TM(z) TFHE_TM(w)
+#undef TFHE_TM
+        st4(mac.acc_b + o, ob);
+        st4(mac.acc_a + o, oa);
+      }
     }
   }
 }
@@ -410,12 +426,16 @@ int launch_unary(const Ctx& c, int op, const uint32_t* a, uint32_t* out, const i
 
 int launch_tensor(const Ctx& c, const uint32_t* b0, const uint32_t* a0, const uint32_t* b1,
                   const uint32_t* a1, uint32_t* d0, uint32_t* d1, uint32_t* d2,
-                  const int16_t* row_prime, int rows, int64_t per_row, cudaStream_t st) {
+                  const int16_t* row_prime, int rows, int64_t per_row, cudaStream_t st,
+                  const TensorMac* mac) {
   if (rows <= 0 || per_row <= 0) return 0;
   RowPrimes rp;
   memcpy(rp.prime, row_prime, sizeof(int16_t) * rows);
+  TensorMac none;
+  memset(&none, 0, sizeof(none));
   dim3 g = grid_rows(per_row, rows, 256);
-  tensor_kernel<<<g, 256, 0, st>>>(b0, a0, b1, a1, d0, d1, d2, c.d_pc, rp, per_row);
+  tensor_kernel<<<g, 256, 0, st>>>(b0, a0, b1, a1, d0, d1, d2, c.d_pc, rp, per_row,
+                                   mac ? *mac : none);
   return check("tensor kernel");
 }
 

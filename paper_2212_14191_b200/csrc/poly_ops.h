@@ -25,9 +25,20 @@ int launch_binary(const Ctx& c, int op, const uint32_t* a, const uint32_t* b, ui
                   const int16_t* row_prime, int rows, int64_t per_row, cudaStream_t st);
 int launch_unary(const Ctx& c, int op, const uint32_t* a, uint32_t* out, const int16_t* row_prime,
                  const uint32_t* scalars, int rows, int64_t per_row, cudaStream_t st);
+// optional slice-row key-switch MAC fused into the tensor product: for rows
+// r < rows of d2, acc_b[r] = d2[r] kb[key_off[r] + coef], acc_a likewise
+struct TensorMac {
+  const uint32_t* kb;
+  const uint32_t* ka;
+  uint32_t* acc_b;
+  uint32_t* acc_a;
+  int rows, log_n;
+  int64_t key_off[kMaxRows];
+};
 int launch_tensor(const Ctx& c, const uint32_t* b0, const uint32_t* a0, const uint32_t* b1,
                   const uint32_t* a1, uint32_t* d0, uint32_t* d1, uint32_t* d2,
-                  const int16_t* row_prime, int rows, int64_t per_row, cudaStream_t st);
+                  const int16_t* row_prime, int rows, int64_t per_row, cudaStream_t st,
+                  const TensorMac* mac = nullptr);
 int launch_ks_mac(const Ctx& c, const uint32_t* x, const uint32_t* kb, const uint32_t* ka,
                   uint32_t* acc_b, uint32_t* acc_a, const int16_t* row_prime,
                   const int64_t* key_off, int rows, int batch, int first, cudaStream_t st);
