@@ -446,6 +446,37 @@ def hconjugate(b, a, basis, conj_key, chain_q, chain_p, alpha, dnum, threads=Non
     return ele_add(bt, ksb, basis), ksa
 
 
+# ---------------------------------------------------------------------------
+# client-side CRT (rns.py:77-115, ckks.py:194-213): Python big integers
+# ---------------------------------------------------------------------------
+
+def crt_decompose(coeffs, basis) -> np.ndarray:
+    """Arbitrary-precision signed ints -> canonical residue rows (len(basis),
+    len(coeffs)) (rns.py:77-90)."""
+    return np.array([[int(c) % q for c in coeffs] for q in basis], dtype=np.uint32)
+
+
+def encode_ints(coeffs) -> list:
+    """encode's rounding of the float64 embedding (ckks.py:194-196):
+    [int(c) for c in np.rint(coeffs)]."""
+    return [int(c) for c in np.rint(np.asarray(coeffs, dtype=np.float64))]
+
+
+def crt_compose_centered(rows, basis) -> list:
+    """CRT representative in [0, Q) (rns.py:93-115) centred into (-Q/2, Q/2]
+    (ckks.py:207-213 _centered)."""
+    rows = np.asarray(rows)
+    big_q = 1
+    for q in basis:
+        big_q *= q
+    terms = [(big_q // q) * pow(big_q // q, -1, q) for q in basis]
+    out = []
+    for j in range(rows.shape[-1]):
+        v = sum(f * int(rows[i, j]) for i, f in enumerate(terms)) % big_q
+        out.append(v - big_q if v > big_q // 2 else v)
+    return out
+
+
 def uniform_rows(rng, basis, shape_tail):
     """cli._random_batch (cli.py:59-64): rng.integers(0, q, shape) per limb."""
     out = np.empty((len(basis),) + tuple(shape_tail), dtype=np.uint32)

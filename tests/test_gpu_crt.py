@@ -13,20 +13,10 @@ def _ctx(n, primes):
     return DeviceContext.get(n, tuple(primes))
 
 
-def _ref_decompose(ints, basis):          # rns.py:77-90
-    return np.array([[c % q for c in ints] for q in basis], dtype=np.uint32)
+from oracle import oracle as O  # noqa: E402
 
-
-def _ref_centered(rows, basis):           # rns.py:93-115 + ckks.py:207-213
-    big_q = 1
-    for q in basis:
-        big_q *= q
-    terms = [((big_q // q) * pow(big_q // q, -1, q), q) for q in basis]
-    out = []
-    for j in range(rows.shape[1]):
-        v = sum(f * int(rows[i, j]) for i, (f, _) in enumerate(terms)) % big_q
-        out.append(v - big_q if v > big_q // 2 else v)
-    return out
+_ref_decompose = O.crt_decompose          # rns.py:77-90
+_ref_centered = O.crt_compose_centered    # rns.py:93-115 + ckks.py:207-213
 
 
 @pytest.mark.parametrize("limbs", [1, 3, 45])
