@@ -428,19 +428,26 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
       const uint32_t* ntt_in = group_conv ? conv : y_full;
       for (int sl = 0; sl < S; ++sl) {
         const int j = j0 + sl, lo = j * g.alpha, hi = std::min(lo + g.alpha, g.l1);
+        int cidx[kMaxRows];   // conv row of target t within the slice (-1: own row)
         if (group_conv) {
-          // fast_basis_conv of the slice to every target prime into conv rows
-          // [sl*T, sl*T+T); the slice's own rows (copies in rns.py:140-142)
-          // are never read -- the inner product skips them -- so they are
-          // left as don't-care values
+          // fast_basis_conv of the slice to the targets it raises, compacted
+          // into conv rows [sl*T, sl*T + T - own): the slice's own rows
+          // (copies in rns.py:140-142) are never read -- the inner product
+          // reuses them unchanged -- so they are not converted at all
           std::vector<int> src, dst;
           for (int q = lo; q < hi; ++q) src.push_back(q);
-          for (int t = 0; t < g.T; ++t) dst.push_back(tprime(g, t));
+          for (int t = 0; t < g.T; ++t) {
+            if (t < g.nr && (g.r0 + t) / g.alpha == j) {
+              cidx[t] = -1;
+              continue;
+            }
+            cidx[t] = (int)dst.size();
+            dst.push_back(tprime(g, t));
+          }
           BconvArgs ba;
           if ((rc = fill_bconv(c, src, dst, ba))) return rc;
           if ((rc = launch_bconv(c, y_full + (size_t)lo * U, conv + (size_t)sl * g.T * U, ba,
-                                 batch, st,
-                                 /*exact_copies=*/false)))
+                                 batch, st, /*exact_copies=*/false)))
             return rc;
         }
         for (int t = 0; t < g.T; ++t) {
@@ -448,8 +455,10 @@ int keyswitch_impl(TfheCtx* h, const uint32_t* d, const uint32_t* y_full, int le
           s1.prime[l] = (int16_t)tprime(g, t);
           // alpha = 1: fast_basis_conv is the identity on the slice's
           // coefficients (Q = q_lo, Q/q = 1): the NTT reads y's row directly
-          // and reduces it mod each target prime inside the byte-sliced GEMM
-          s1.in_row[l] = (int16_t)(group_conv ? l : lo);
+          // and reduces it mod each target prime inside the byte-sliced GEMM.
+          // An own target's limb (never used) reads any valid row.
+          s1.in_row[l] =
+              (int16_t)(group_conv ? sl * g.T + (cidx[t] >= 0 ? cidx[t] : 0) : lo);
           s1.out_row[l] = (int16_t)l;
         }
       }
