@@ -159,3 +159,27 @@ def test_kernel_timer_counts_ntt_pass_launches():
     with _lib.kernel_timer() as kt2:
         pass
     assert kt2.times == {}
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_ntt_random_shapes_vs_oracle(seed):
+    """Random degrees (2^12..2^16), limb counts, batch sizes (incl. odd and 1)
+    and prime widths (26..31 bits): forward equals the oracle, inverse undoes
+    it -- every plan (fused n=4096, TS, three-factor) on ragged shapes."""
+    import torch
+    from paper_2212_14191_b200.device import DeviceContext
+    from paper_2212_14191_b200.params import generate_primes
+    rng = np.random.default_rng(1000 + seed)
+    n = 1 << int(rng.integers(12, 17))
+    limbs = int(rng.integers(1, 4))
+    batch = int(rng.choice([1, 2, 3, 5, 7, 9]))
+    widths = [int(w) for w in rng.integers(26, 32, limbs)]
+    qs = generate_primes(n, widths)
+    ctx = DeviceContext.get(n, tuple(qs))
+    x = O.uniform_rows(rng, qs, (batch, n))
+    f = ctx.ntt(torch.from_numpy(x.view(np.int32)).cuda(), qs)
+    got = f.cpu().numpy().view(np.uint32)
+    sel = [0, batch - 1]                      # oracle cost: first and last member
+    assert np.array_equal(got[:, sel], O.ntt(x[:, sel], qs)), (n, limbs, batch, widths)
+    back = ctx.ntt(f, qs, inverse=True).cpu().numpy().view(np.uint32)
+    assert np.array_equal(back, x), (n, limbs, batch, widths)
