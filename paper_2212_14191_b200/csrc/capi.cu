@@ -116,6 +116,12 @@ void set_group(CkksGeom& g, const Ctx& c, int batch) {
   const size_t cap = std::max<size_t>(cap_gib, 1) << 30;
   int s_mem = (int)std::max<size_t>(1, cap / (row_bytes * g.T));
   g.S = std::max(1, std::min({g.nslices, kMaxLimbs / g.T, s_mem}));
+  // balanced groups: the same number of groups, no small trailing group
+  // (45 slices at S <= 11: 5 x 9 rather than 4 x 11 + 1)
+  {
+    const int ng = (g.nslices + g.S - 1) / g.S;
+    g.S = (g.nslices + ng - 1) / ng;
+  }
   // test knob: TFHE_KS_MAX_S caps the group size so small goldens also run the
   // multi-group path (every group after the first re-reads the accumulator)
   if (const char* e = getenv("TFHE_KS_MAX_S")) {
