@@ -1,3 +1,5 @@
+"""Reproducer of the raw-slot reuse race in the N=2^16 passes (multi-unit CTAs): fixed by the
+fence.proxy.async before a TMA-filled slot is released; kept as a regression aid."""
 import sys, numpy as np, torch
 sys.path.insert(0,'.')
 from oracle import oracle as O
