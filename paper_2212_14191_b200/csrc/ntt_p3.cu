@@ -64,7 +64,7 @@ constexpr int kPItems = 22;                      // ceil(64 warp items / 3 produ
 //   TFHE_P3_CSHOUP = 1: c as a Shoup operand (3 fewer IMAD-pipe cycles per
 //   output than Montgomery) -- its table only fits with one stage-B buffer.
 #ifndef TFHE_P3_CSHOUP
-#define TFHE_P3_CSHOUP 0
+#define TFHE_P3_CSHOUP 1
 #endif
 constexpr int kA2Bufs = TFHE_P3_CSHOUP ? 1 : 2;
 constexpr int kHBeta = 0, kHBetaS = 64 * 32, kHIn = 2 * 64 * 32, kHInS = kHIn + 32 * 36,
