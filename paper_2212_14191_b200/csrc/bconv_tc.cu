@@ -672,10 +672,10 @@ int launch_bconv(const Ctx& c, const uint32_t* in, uint32_t* out, const BconvArg
                    8 * 4 + 3 * kMaxSrcBC * 4 +
                    kMaxBconvDst / 16 * 4 +
                    (2 * kAStages + 4 + 2 * kRawBC) * 8 + 16;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<bool> attr[64];   // function attributes are per device
+  if (!attr[c.dev & 63].load(std::memory_order_relaxed)) {
     cudaFuncSetAttribute(bconv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+    attr[c.dev & 63].store(true, std::memory_order_relaxed);
   }
   const int grid = (int)std::min<int64_t>(a.tiles, c.sms);
 #ifdef TFHE_BC_TRACE
